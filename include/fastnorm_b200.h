@@ -1,0 +1,158 @@
+/*
+ * fastnorm_b200.h -- C ABI of the B200 (sm_100a) batched normalization library.
+ *
+ * This is the drop-in boundary for the reference package's kernel registry.
+ * The reference resolves every kernel by name through
+ *     getattr(module, f"{base}_{suffix}")                 (_backend.py:86-93)
+ * over the flat scalar exports of its Cython module
+ *     {base}_{f32,f64}(tau_min, tau_max, sigma_min, sigma_max, inv_min, inv_max, x1..xn)
+ *                                                         (_kernels.pyx:419-634)
+ * This library exports the same 16 kernel families x 2 precisions, batched over an
+ * AoS array of N rows, as  fn_{base}_{f32,f64}.  The six scaling constants keep the
+ * reference's meaning and order (scale.py:26-30 kernel_args) and are always passed as
+ * doubles; the f32 entry points round them to binary32 exactly like the reference's
+ * `<float>` casts (_kernels.pyx:526-527).
+ *
+ * Layout (all arrays caller-owned, contiguous, C order):
+ *   x     [N, n]  input rows (AoS: x1..xn of row i at x[i*n .. i*n+n-1])
+ *   r     [N]     length           (normalize / norm / naive / quotient families)
+ *   inv   [N]     inverse scale    (scale family; 0 marks an all-zero row)
+ *   unit  [N, n]  unit vector      (normalize / naive / quotient families)
+ *   scaled[N, n]  scaled row       (scale family)
+ *   sq    [N]     squared length, ldexp(ss, 2*log2(inv)) (the *_sq entry points; no
+ *                 reference function exists -- see DESIGN.md "squared norm")
+ *
+ * Device entry points (fn_*): every pointer is device memory (or managed); the call
+ * enqueues work on `stream` (a cudaStream_t, NULL = legacy default stream) and returns
+ * without synchronising.  Host entry points (fn_host_*): every pointer is host memory
+ * (pinned is fastest); the call copies in, computes on the current device, copies out
+ * and returns when the results are in the caller's buffers.
+ *
+ * Errors: kernels never fail on values -- IEEE results for every input, exactly as the
+ * reference (`cdivision=True`, _kernels.pyx:5).  Argument problems return a negative
+ * fn_status; the message is available from fn_last_error() (per thread).  ka must
+ * satisfy the reference's validate_conditions (params.py:134-197), which kernel_args
+ * enforces upstream (scale.py:26-30); the library itself rejects only tau values that
+ * are negative or NaN (they would break the bit-pattern band test).
+ *
+ * Thread safety: stateless apart from the per-thread last-error slot and a per-device
+ * cache of staging buffers used by the fn_host_* entry points (mutex protected).
+ */
+#ifndef FASTNORM_B200_H
+#define FASTNORM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    FN_OK = 0,
+    FN_EINVAL = -1,   /* bad N, NULL pointer, bad ka, unknown op/dim/dtype */
+    FN_ECUDA = -2,    /* a CUDA runtime error; see fn_last_error() */
+    FN_ENODEV = -3,   /* no CUDA device visible */
+    FN_ENOMEM = -4    /* staging allocation failed (host entry points) */
+} fn_status;
+
+/* Kernel families (reference names, tests/test_backends.py:20-27). */
+typedef enum {
+    FN_OP_SCALE = 0,          /* scale{2,3,4}        _kernels.pyx:51-160  */
+    FN_OP_NORMALIZE = 1,      /* normalize{2,3,4}    _kernels.pyx:167-225 */
+    FN_OP_NORM = 2,           /* norm{2,3,4}         _kernels.pyx:228-255 */
+    FN_OP_NAIVE = 3,          /* naive{2,3,4}        _kernels.pyx:262-285 */
+    FN_OP_QUOTIENT = 4,       /* quotient{2,3,4}     _kernels.pyx:288-362 */
+    FN_OP_QUOTIENT3_FAST = 5, /* quotient3_fast      _kernels.pyx:365-412 */
+    FN_OP_NORMALIZE_SQ = 6    /* normalize{2,3,4} + squared length (BASELINE config 3) */
+} fn_op;
+
+typedef enum { FN_F32 = 0, FN_F64 = 1 } fn_dtype;
+
+/* ---- library metadata ------------------------------------------------------------- */
+const char* fn_version(void);         /* e.g. "fastnorm-b200 0.1.0 sm_100a"             */
+const char* fn_build_flags(void);     /* nvcc flags (reference analogue: BUILD_FLAGS)   */
+const char* fn_backend_name(void);    /* "cuda"  (reference analogue: BACKEND_NAME)     */
+const char* fn_last_error(void);      /* message of the last failing call on this thread */
+int fn_device_count(void);
+
+/* ---- generic entry points --------------------------------------------------------- */
+/* head = r (or inv for FN_OP_SCALE); body = unit (or scaled); sq only for
+ * FN_OP_NORMALIZE_SQ.  body must be NULL for FN_OP_NORM.  ka is ignored (may be NULL)
+ * for the naive / quotient families, which take no constants (_kernels.pyx:481-520). */
+int fn_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* body,
+           void* sq, const double* ka, void* stream);
+int fn_host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head,
+                void* body, void* sq, const double* ka);
+
+/* ---- named entry points: one per reference export --------------------------------- */
+/* scale{n}_{f64,f32}      replaces _kernels.pyx:419-439 / :523-546 */
+int fn_scale2_f64(const double* x, int64_t n, double* inv, double* scaled, const double ka[6], void* stream);
+int fn_scale3_f64(const double* x, int64_t n, double* inv, double* scaled, const double ka[6], void* stream);
+int fn_scale4_f64(const double* x, int64_t n, double* inv, double* scaled, const double ka[6], void* stream);
+int fn_scale2_f32(const float* x, int64_t n, float* inv, float* scaled, const double ka[6], void* stream);
+int fn_scale3_f32(const float* x, int64_t n, float* inv, float* scaled, const double ka[6], void* stream);
+int fn_scale4_f32(const float* x, int64_t n, float* inv, float* scaled, const double ka[6], void* stream);
+
+/* normalize{n}_{f64,f32}  replaces _kernels.pyx:442-463 / :549-573 */
+int fn_normalize2_f64(const double* x, int64_t n, double* r, double* unit, const double ka[6], void* stream);
+int fn_normalize3_f64(const double* x, int64_t n, double* r, double* unit, const double ka[6], void* stream);
+int fn_normalize4_f64(const double* x, int64_t n, double* r, double* unit, const double ka[6], void* stream);
+int fn_normalize2_f32(const float* x, int64_t n, float* r, float* unit, const double ka[6], void* stream);
+int fn_normalize3_f32(const float* x, int64_t n, float* r, float* unit, const double ka[6], void* stream);
+int fn_normalize4_f32(const float* x, int64_t n, float* r, float* unit, const double ka[6], void* stream);
+
+/* normalize{n}_sq_{f64,f32}: normalize{n} plus the squared length (config 3). */
+int fn_normalize2_sq_f64(const double* x, int64_t n, double* sq, double* r, double* unit, const double ka[6], void* stream);
+int fn_normalize3_sq_f64(const double* x, int64_t n, double* sq, double* r, double* unit, const double ka[6], void* stream);
+int fn_normalize4_sq_f64(const double* x, int64_t n, double* sq, double* r, double* unit, const double ka[6], void* stream);
+int fn_normalize2_sq_f32(const float* x, int64_t n, float* sq, float* r, float* unit, const double ka[6], void* stream);
+int fn_normalize3_sq_f32(const float* x, int64_t n, float* sq, float* r, float* unit, const double ka[6], void* stream);
+int fn_normalize4_sq_f32(const float* x, int64_t n, float* sq, float* r, float* unit, const double ka[6], void* stream);
+
+/* norm{n}_{f64,f32}       replaces _kernels.pyx:466-478 / :576-592 */
+int fn_norm2_f64(const double* x, int64_t n, double* r, const double ka[6], void* stream);
+int fn_norm3_f64(const double* x, int64_t n, double* r, const double ka[6], void* stream);
+int fn_norm4_f64(const double* x, int64_t n, double* r, const double ka[6], void* stream);
+int fn_norm2_f32(const float* x, int64_t n, float* r, const double ka[6], void* stream);
+int fn_norm3_f32(const float* x, int64_t n, float* r, const double ka[6], void* stream);
+int fn_norm4_f32(const float* x, int64_t n, float* r, const double ka[6], void* stream);
+
+/* naive{n}_{f64,f32}      replaces _kernels.pyx:481-496 / :595-610 */
+int fn_naive2_f64(const double* x, int64_t n, double* r, double* unit, void* stream);
+int fn_naive3_f64(const double* x, int64_t n, double* r, double* unit, void* stream);
+int fn_naive4_f64(const double* x, int64_t n, double* r, double* unit, void* stream);
+int fn_naive2_f32(const float* x, int64_t n, float* r, float* unit, void* stream);
+int fn_naive3_f32(const float* x, int64_t n, float* r, float* unit, void* stream);
+int fn_naive4_f32(const float* x, int64_t n, float* r, float* unit, void* stream);
+
+/* quotient{n}_{f64,f32}   replaces _kernels.pyx:499-514 / :613-628 */
+int fn_quotient2_f64(const double* x, int64_t n, double* r, double* unit, void* stream);
+int fn_quotient3_f64(const double* x, int64_t n, double* r, double* unit, void* stream);
+int fn_quotient4_f64(const double* x, int64_t n, double* r, double* unit, void* stream);
+int fn_quotient2_f32(const float* x, int64_t n, float* r, float* unit, void* stream);
+int fn_quotient3_f32(const float* x, int64_t n, float* r, float* unit, void* stream);
+int fn_quotient4_f32(const float* x, int64_t n, float* r, float* unit, void* stream);
+
+/* quotient3_fast_{f64,f32} replaces _kernels.pyx:517-520 / :631-634 */
+int fn_quotient3_fast_f64(const double* x, int64_t n, double* r, double* unit, void* stream);
+int fn_quotient3_fast_f32(const float* x, int64_t n, float* r, float* unit, void* stream);
+
+/* ---- row statistics (validation counters for the multi-GPU driver) ---------------- */
+/* Counts, over rows [0, n): [0] rows with a NaN component, [1] rows with an infinite
+ * component and no NaN, [2] all-zero rows, [3] rows whose max |x_k| is below tau_min,
+ * [4] rows whose max |x_k| is above tau_max (finite), [5] rows inside the band.
+ * `counts` is a device array of 6 uint64 that is ACCUMULATED into (zero it first). */
+int fn_row_stats(int dim, int dtype, const void* x, int64_t n, uint64_t* counts,
+                 const double* ka, void* stream);
+
+/* ---- seeded synthetic workloads (BASELINE.json configs) ------------- */
+/* Writes rows [row0, row0+n) of workload `cfg` (1..5) into device array x.  Rows are a
+ * pure function of (cfg, seed, global row index), so any sharding produces identical
+ * data.  dim/dtype must match the config (1: 3/f64, 2: 2/f64, 3: 4/f64, 4: 3/f32,
+ * 5: 3/f64). */
+int fn_generate(int cfg, uint64_t seed, int64_t row0, int64_t n, void* x, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FASTNORM_B200_H */

@@ -1,0 +1,300 @@
+// fastnorm_math.cuh -- per-row arithmetic of the normalization kernels (device side).
+//
+// Every function here restates one reference routine of pkg/src/fastnorm/_kernels.pyx
+// (cited per function) with the SAME operation order and one IEEE rounding per
+// written operation: products and sums go through the __{d,f}{mul,add}_rn intrinsics,
+// which nvcc never contracts into FMA (the reference is built -ffp-contract=off,
+// setup.py:9), square roots through __{d,f}sqrt_rn, reciprocals through __{d,f}rcp_rn
+// (correctly rounded 1/x == the reference's IEEE `1.0 / rt`), and the quotient /
+// naive families through __{d,f}div_rn (true IEEE division; x/0 follows IEEE like
+// Cython's cdivision=True, _kernels.pyx:5).  f32 computes entirely in binary32 with
+// subnormals kept (built with -ftz=false), like the reference's `float` instantiation.
+//
+// The scaling families (normalize / norm) classify each row by integer operations on
+// the IEEE bit patterns (exponent extraction): the largest |x_k| is the unsigned max of
+// the sign-cleared bit patterns, and the band test against tau_min / tau_max is an
+// unsigned compare.  DESIGN.md §3 proves this selects exactly the reference cascade's
+// (inv, sigma) for every NaN-free row and produces the reference's all-NaN output for
+// every row holding a NaN; the zero branch is taken iff every component is +-0.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fnb {
+
+// ---------------------------------------------------------------------------------
+// Precision traits: the correctly rounded primitive operations, per binary format.
+// ---------------------------------------------------------------------------------
+template <typename T> struct Fp;
+
+template <> struct Fp<double> {
+    using Bits = unsigned long long;
+    static constexpr Bits kAbsMask = 0x7fffffffffffffffull;
+    __device__ __forceinline__ static Bits bits(double x) { return (Bits)__double_as_longlong(x); }
+    __device__ __forceinline__ static double mul(double a, double b) { return __dmul_rn(a, b); }
+    __device__ __forceinline__ static double add(double a, double b) { return __dadd_rn(a, b); }
+    __device__ __forceinline__ static double div(double a, double b) { return __ddiv_rn(a, b); }
+    __device__ __forceinline__ static double rcp(double a) { return __drcp_rn(a); }
+    __device__ __forceinline__ static double sqrt(double a) { return __dsqrt_rn(a); }
+    __device__ __forceinline__ static double abs(double a) { return fabs(a); }
+    __device__ __forceinline__ static double sign1(double a) { return copysign(1.0, a); }
+    __device__ __forceinline__ static bool isnan_(double a) { return isnan(a); }
+    __device__ __forceinline__ static double ldexp_(double a, int e) { return ldexp(a, e); }
+    __device__ __forceinline__ static int exponent_of_pow2(double p) {
+        // p = 2^k (normal): k from the biased exponent field.
+        return (int)((bits(p) >> 52) & 0x7ff) - 1023;
+    }
+};
+
+template <> struct Fp<float> {
+    using Bits = unsigned int;
+    static constexpr Bits kAbsMask = 0x7fffffffu;
+    __device__ __forceinline__ static Bits bits(float x) { return (Bits)__float_as_uint(x); }
+    __device__ __forceinline__ static float mul(float a, float b) { return __fmul_rn(a, b); }
+    __device__ __forceinline__ static float add(float a, float b) { return __fadd_rn(a, b); }
+    __device__ __forceinline__ static float div(float a, float b) { return __fdiv_rn(a, b); }
+    __device__ __forceinline__ static float rcp(float a) { return __frcp_rn(a); }
+    __device__ __forceinline__ static float sqrt(float a) { return __fsqrt_rn(a); }
+    __device__ __forceinline__ static float abs(float a) { return fabsf(a); }
+    __device__ __forceinline__ static float sign1(float a) { return copysignf(1.0f, a); }
+    __device__ __forceinline__ static bool isnan_(float a) { return isnan(a); }
+    __device__ __forceinline__ static float ldexp_(float a, int e) { return ldexpf(a, e); }
+    __device__ __forceinline__ static int exponent_of_pow2(float p) {
+        return (int)((bits(p) >> 23) & 0xff) - 127;
+    }
+};
+
+// The six kernel arguments (scale.py:26-30), already rounded to T, plus the bit
+// patterns of the two band thresholds for the integer band test.
+template <typename T> struct KArgs {
+    T tau_min, tau_max, sigma_min, sigma_max, inv_min, inv_max;
+    typename Fp<T>::Bits tau_min_bits, tau_max_bits;
+};
+
+// ---------------------------------------------------------------------------------
+// Scaling: integer classification + power-of-two scale (Algs 3/4, Alg 7 lines 4-23).
+// Returns false for the all-zero row.  s_k = fl(sigma * x_k) exactly as the reference
+// (_kernels.pyx:97-112): exact unless the sigma_max product drops below nu.
+// ---------------------------------------------------------------------------------
+template <typename T, int N>
+__device__ __forceinline__ bool scale_classified(const T (&x)[N], const KArgs<T>& ka, T& inv,
+                                                 T (&s)[N]) {
+    using F = Fp<T>;
+    typename F::Bits m = F::bits(x[0]) & F::kAbsMask;
+#pragma unroll
+    for (int k = 1; k < N; ++k) {
+        typename F::Bits a = F::bits(x[k]) & F::kAbsMask;
+        m = a > m ? a : m;
+    }
+    // m is the bit pattern of max |x_k| (NaN > inf > finite in this order).
+    const bool big = m > ka.tau_max_bits;     // includes inf and NaN rows
+    const bool small = m < ka.tau_min_bits;
+    const T sigma = big ? ka.sigma_max : (small ? ka.sigma_min : T(1));
+    inv = big ? ka.inv_max : (small ? ka.inv_min : T(1));
+#pragma unroll
+    for (int k = 0; k < N; ++k) s[k] = F::mul(sigma, x[k]);  // 1*x == x bit for bit
+    return m != 0;
+}
+
+// Left-to-right sum of squares without contraction: ((s1^2 + s2^2) + s3^2) + s4^2.
+template <typename T, int N>
+__device__ __forceinline__ T sum_squares(const T (&s)[N]) {
+    using F = Fp<T>;
+    T acc = F::mul(s[0], s[0]);
+#pragma unroll
+    for (int k = 1; k < N; ++k) acc = F::add(acc, F::mul(s[k], s[k]));
+    return acc;
+}
+
+// normalize{2,3,4}: _kernels.pyx:167-225.  Zero row -> r = 0, unit = 0 (n = 4: the
+// identity quaternion (0,0,0,1), :211-218).  Optional squared length (config 3):
+// sq = ldexp(ss, 2*log2(inv)), correctly rounded.
+template <typename T, int N, bool kSq>
+__device__ __forceinline__ void normalize_row(const T (&x)[N], const KArgs<T>& ka, T& r,
+                                              T (&u)[N], T& sq) {
+    using F = Fp<T>;
+    T inv, s[N];
+    const bool nonzero = scale_classified<T, N>(x, ka, inv, s);
+    const T ss = sum_squares<T, N>(s);
+    const T rt = F::sqrt(ss);
+    const T h = F::rcp(rt);
+    r = nonzero ? F::mul(inv, rt) : T(0);
+#pragma unroll
+    for (int k = 0; k < N; ++k) u[k] = nonzero ? F::mul(h, s[k]) : T(0);
+    if (N == 4) u[N - 1] = nonzero ? u[N - 1] : T(1);
+    if (kSq) {
+        sq = nonzero ? F::ldexp_(ss, 2 * F::exponent_of_pow2(inv)) : T(0);
+    }
+}
+
+// norm{2,3,4}: _kernels.pyx:228-255; bit-identical to normalize's r.
+template <typename T, int N>
+__device__ __forceinline__ T norm_row(const T (&x)[N], const KArgs<T>& ka) {
+    using F = Fp<T>;
+    T inv, s[N];
+    const bool nonzero = scale_classified<T, N>(x, ka, inv, s);
+    const T r = F::mul(inv, F::sqrt(sum_squares<T, N>(s)));
+    return nonzero ? r : T(0);
+}
+
+// scale{2,3,4}: the exported preprocessor keeps the reference's exact comparison
+// cascade, because with a NaN present its (inv, s) outcome depends on the order of
+// the comparisons.  Verbatim branch structure of _kernels.pyx:51-160.
+// Band test of the cascade (_kernels.pyx:63-75 and siblings).  Returns true for the
+// in-band row, whose components are passed through unscaled.
+template <typename T>
+__device__ __forceinline__ bool scale_tail(T m, const KArgs<T>& ka, T& inv, T& sigma) {
+    if (m >= ka.tau_min) {
+        if (m <= ka.tau_max) { inv = T(1); sigma = T(1); return true; }
+        inv = ka.inv_max; sigma = ka.sigma_max; return false;
+    }
+    inv = ka.inv_min; sigma = ka.sigma_min; return false;
+}
+
+template <typename T>
+__device__ __forceinline__ void scale_row(const T (&x)[2], const KArgs<T>& ka, T& inv, T (&s)[2]) {
+    using F = Fp<T>;
+    T m = F::abs(x[0]);  // _kernels.pyx:54-62
+    if (m >= F::abs(x[1])) {
+        if (m == T(0)) { inv = T(0); s[0] = T(0); s[1] = T(0); return; }
+    } else {
+        m = F::abs(x[1]);
+    }
+    T sigma;
+    if (scale_tail(m, ka, inv, sigma)) { s[0] = x[0]; s[1] = x[1]; return; }
+    s[0] = F::mul(sigma, x[0]); s[1] = F::mul(sigma, x[1]);
+}
+
+template <typename T>
+__device__ __forceinline__ void scale_row(const T (&x)[3], const KArgs<T>& ka, T& inv, T (&s)[3]) {
+    using F = Fp<T>;
+    T m = F::abs(x[0]);  // _kernels.pyx:81-96
+    if (m < F::abs(x[1])) {
+        m = F::abs(x[1]);
+        if (m < F::abs(x[2])) m = F::abs(x[2]);
+    } else {
+        if (m >= F::abs(x[2])) {
+            if (m == T(0) && !F::isnan_(x[1])) {
+                inv = T(0); s[0] = T(0); s[1] = T(0); s[2] = T(0); return;
+            }
+        } else {
+            m = F::abs(x[2]);
+        }
+    }
+    T sigma;
+    if (scale_tail(m, ka, inv, sigma)) { s[0] = x[0]; s[1] = x[1]; s[2] = x[2]; return; }
+    s[0] = F::mul(sigma, x[0]); s[1] = F::mul(sigma, x[1]); s[2] = F::mul(sigma, x[2]);
+}
+
+template <typename T>
+__device__ __forceinline__ void scale_row(const T (&x)[4], const KArgs<T>& ka, T& inv, T (&s)[4]) {
+    using F = Fp<T>;
+    T m = F::abs(x[0]);  // _kernels.pyx:119-141
+    if (m < F::abs(x[1])) {
+        m = F::abs(x[1]);
+        if (m < F::abs(x[2])) m = F::abs(x[2]);
+        if (m < F::abs(x[3])) m = F::abs(x[3]);
+    } else {
+        if (m < F::abs(x[2])) {
+            m = F::abs(x[2]);
+            if (m < F::abs(x[3])) m = F::abs(x[3]);
+        } else {
+            if (m >= F::abs(x[3])) {
+                if (m == T(0) && !(F::isnan_(x[1]) || F::isnan_(x[2]))) {
+                    inv = T(0); s[0] = T(0); s[1] = T(0); s[2] = T(0); s[3] = T(0); return;
+                }
+            } else {
+                m = F::abs(x[3]);
+            }
+        }
+    }
+    T sigma;
+    if (scale_tail(m, ka, inv, sigma)) {
+        s[0] = x[0]; s[1] = x[1]; s[2] = x[2]; s[3] = x[3]; return;
+    }
+    s[0] = F::mul(sigma, x[0]); s[1] = F::mul(sigma, x[1]);
+    s[2] = F::mul(sigma, x[2]); s[3] = F::mul(sigma, x[3]);
+}
+
+// naive{2,3,4}: _kernels.pyx:262-285.  r = sqrt(sum x^2), u = x / r (true divisions).
+template <typename T, int N>
+__device__ __forceinline__ void naive_row(const T (&x)[N], T& r, T (&u)[N]) {
+    using F = Fp<T>;
+    const T rr = F::sqrt(sum_squares<T, N>(x));
+    r = rr;
+#pragma unroll
+    for (int k = 0; k < N; ++k) u[k] = F::div(x[k], rr);
+}
+
+// quotient{2,3,4}: _kernels.pyx:288-362 (Alg 1 generalised).  m = max via strict '>',
+// zero row (no NaN) -> all +0 (n = 4: five zeros, no identity quaternion).
+template <typename T, int N>
+__device__ __forceinline__ void quotient_row(const T (&x)[N], T& r, T (&u)[N]) {
+    using F = Fp<T>;
+    T m = F::abs(x[0]);
+#pragma unroll
+    for (int k = 1; k < N; ++k) {
+        const T a = F::abs(x[k]);
+        if (a > m) m = a;
+    }
+    bool anynan = false;
+#pragma unroll
+    for (int k = 0; k < N; ++k) anynan = anynan || F::isnan_(x[k]);
+    if (m == T(0) && !anynan) {
+        r = T(0);
+#pragma unroll
+        for (int k = 0; k < N; ++k) u[k] = T(0);
+        return;
+    }
+    T q[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) q[k] = F::div(x[k], m);
+    const T h = F::sqrt(sum_squares<T, N>(q));
+    r = F::mul(m, h);
+#pragma unroll
+    for (int k = 0; k < N; ++k) u[k] = F::div(q[k], h);
+}
+
+// Shared body of the pivoted fast quotient (_kernels.pyx:370-377 and siblings):
+// p dominates, a and b ride along.  h = sqrt((1 + qa^2) + qb^2), t = sign(p)/h.
+template <typename T>
+__device__ __forceinline__ void qf_pivot(T p, T a, T b, T& r, T& t, T& ua, T& ub) {
+    using F = Fp<T>;
+    const T qa = F::div(a, p);
+    const T qb = F::div(b, p);
+    const T h = F::sqrt(F::add(F::add(T(1), F::mul(qa, qa)), F::mul(qb, qb)));
+    t = F::div(F::sign1(p), h);
+    r = F::mul(F::abs(p), h);
+    ua = F::mul(qa, t);
+    ub = F::mul(qb, t);
+}
+
+// quotient3_fast: _kernels.pyx:365-412 (Alg 2) -- verbatim pivot order and ties.
+template <typename T>
+__device__ __forceinline__ void quotient3_fast_row(const T (&x)[3], T& r, T (&u)[3]) {
+    using F = Fp<T>;
+    T t, ua, ub;
+    if (F::abs(x[0]) > F::abs(x[1])) {
+        if (F::abs(x[2]) > F::abs(x[0])) {
+            qf_pivot(x[2], x[0], x[1], r, t, ua, ub);  // :369-377
+            u[0] = ua; u[1] = ub; u[2] = t;
+        } else {
+            qf_pivot(x[0], x[2], x[1], r, t, ua, ub);  // :378-386
+            u[0] = t; u[1] = ub; u[2] = ua;
+        }
+    } else {
+        if (F::abs(x[2]) >= F::abs(x[1])) {
+            if (x[2] == T(0) && !F::isnan_(x[0])) {  // :388-395
+                r = T(0); u[0] = T(0); u[1] = T(0); u[2] = T(0);
+                return;
+            }
+            qf_pivot(x[2], x[0], x[1], r, t, ua, ub);  // :396-403
+            u[0] = ua; u[1] = ub; u[2] = t;
+        } else {
+            qf_pivot(x[1], x[0], x[2], r, t, ua, ub);  // :404-412
+            u[0] = ua; u[1] = t; u[2] = ub;
+        }
+    }
+}
+
+}  // namespace fnb

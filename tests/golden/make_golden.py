@@ -1,0 +1,175 @@
+"""Generate the golden parity fixtures from the REFERENCE itself.
+
+Run in the build container (needs /root/reference and the reference's compiled kernels
+in oracle/_ref, built by `make -C oracle ref`):
+
+    python tests/golden/make_golden.py
+
+For every kernel family of the reference registry (tests/test_backends.py:20-27) and
+both precisions it evaluates the reference's compiled Cython exports
+(_kernels.pyx:419-634) AND its pure-Python twin (_pykernels.py:298-458), asserts they
+agree bit for bit (the reference's own `_same` rule, test_backends.py:33-38), and
+stores inputs and outputs in golden_vectors.npz.  Inputs follow the reference tests:
+
+* random full-range rows (exponents over the whole format incl. subnormals, random
+  signs; the construction of test_backends.py:41-49, seed 2024);
+* Cartesian products of special values (test_backends.py:29-30 plus band-edge and
+  out-of-band values) in every position;
+* the known-answer rows of test_scale.py / test_normalize.py / test_baselines.py and
+  the probes of SURVEY.md Appendix A.
+
+Loop checksums (_kernels.pyx:646-789) over a small buffer are stored as well
+(iters=37, mask=7 as in test_backends.py:103-104).
+
+The f32 entry points take doubles and cast with <float> (_kernels.pyx:526-527), so the
+stored f32 inputs are those casts (what the kernel actually computes on).
+"""
+
+from __future__ import annotations
+
+import importlib.util
+import itertools
+import math
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+REF = "/root/reference/pkg/src/fastnorm"
+sys.path.insert(0, REPO)
+
+import oracle  # noqa: E402
+
+
+def _load_pykernels():
+    spec = importlib.util.spec_from_file_location("_ref_pykernels", os.path.join(REF, "_pykernels.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+L = math.ldexp
+DBL_MAX = sys.float_info.max
+FLT_MAX = float(np.finfo(np.float32).max)
+
+KA = {
+    "f64": (L(1, -482), L(1, 510), L(1, 592), L(1, -514), L(1, -592), L(1, 514)),
+    "f32": (L(1, -49), L(1, 62), L(1, 100), L(1, -66), L(1, -100), L(1, 66)),
+}
+
+FAMILIES = {
+    2: ["scale", "normalize", "norm", "naive", "quotient"],
+    3: ["scale", "normalize", "norm", "naive", "quotient", "quotient3_fast"],
+    4: ["scale", "normalize", "norm", "naive", "quotient"],
+}
+SCALING = {"scale", "normalize", "norm"}
+
+SPECIALS = {
+    "f64": [0.0, -0.0, 1.0, -1.0, math.inf, -math.inf, math.nan, 5e-324, L(1, -1022),
+            L(1, -482), L(1, 510), DBL_MAX, L(1, -600), -L(3, 600)],
+    "f32": [0.0, -0.0, 1.0, -1.0, math.inf, -math.inf, math.nan, L(1, -149), L(1, -126),
+            L(1, -49), L(1, 62), FLT_MAX, L(1, -80), -L(3, 80)],
+}
+SPECIALS4 = {
+    "f64": [0.0, -0.0, 1.0, math.inf, math.nan, 5e-324, L(1, 600)],
+    "f32": [0.0, -0.0, 1.0, math.inf, math.nan, L(1, -149), L(1, 80)],
+}
+
+KATS = {
+    2: [(3.0, 4.0), (L(1, -1074), 0.0), (L(1, -500), 0.0), (L(1, 520), L(1, 519)),
+        (L(1, -600), 0.0), (L(1, 600), 0.0), (L(1, -1022), math.nextafter(L(1, 510), math.inf)),
+        (L(1, 70), 0.0), (L(1, -60), 0.0), (1.0, -0.5)],
+    3: [(3.0, 4.0, 12.0), (2.0, 10.0, 11.0), (L(1, 600), L(1, 600), L(1, 600)),
+        (DBL_MAX, DBL_MAX, 0.0), (DBL_MAX, DBL_MAX, DBL_MAX), (5e-324, -5e-324, 5e-324),
+        (-3.0, 0.0, -0.0), (math.inf, 1.0, -2.0), (math.inf, -math.inf, 1.0),
+        (math.inf, math.nan, 1.0), (3e38, 3e38, 1.0), (L(1, 511), L(1, -600), -L(1, 1000)),
+        (math.nan, 1.0, 0.0), (math.nan, L(1, 600), 0.0), (L(1, 600), math.nan, 0.0),
+        (0.0, math.nan, 0.0), (12.0, 4.0, 3.0), (4.0, 12.0, 3.0), (4.0, 3.0, 12.0),
+        (-12.0, 4.0, -3.0), (1.0, 1.0, 1.0), (L(1, -1060), -L(3, -1070), L(1, -1074)),
+        (0.0, L(1, -1074), 0.0), (L(1, 70), 0.0, 0.0)],
+    4: [(1.0, 1.0, 1.0, 1.0), (3 * L(1, -520), 0.0, 4 * L(1, -520), 0.0),
+        (L(1, 600), 0.0, 0.0, L(1, 599)), (1.0, 0.0, 0.0, L(1, -500)),
+        (0.0, math.nan, 0.0, 0.0), (0.0, 0.0, math.nan, 0.0), (0.0, 0.0, 0.0, -0.0),
+        (L(1, -1074), 0.0, 0.0, 0.0), (DBL_MAX, DBL_MAX, DBL_MAX, DBL_MAX)],
+}
+
+
+def random_rows(rng, m, dim, single):
+    lo, hi = (-149, 127) if single else (-1074, 1023)
+    e = rng.integers(lo, hi, (m, dim))
+    mant = 1.0 + rng.random((m, dim))
+    s = rng.integers(0, 2, (m, dim)) * 2 - 1
+    v = np.ldexp(mant, e) * s
+    if single:
+        v = v.astype(np.float32).astype(np.float64)
+    return v
+
+
+def same(a, b):
+    if math.isnan(a) or math.isnan(b):
+        return math.isnan(a) and math.isnan(b)
+    return a == b and math.copysign(1.0, a) == math.copysign(1.0, b)
+
+
+def main():
+    comp = oracle.ref_module()
+    if comp is None:
+        oracle.build_ref()
+        comp = oracle.ref_module()
+    pure = _load_pykernels()
+    assert comp.BUILD_FLAGS == "-O3 -ffp-contract=off"
+    rng = np.random.default_rng(2024)
+    out = {}
+    for prec in ("f64", "f32"):
+        single = prec == "f32"
+        ka = KA[prec]
+        for dim in (2, 3, 4):
+            rows = []
+            rows += [list(r) for r in random_rows(rng, 1024, dim, single)]
+            sp = SPECIALS4[prec] if dim == 4 else SPECIALS[prec]
+            rows += [list(t) for t in itertools.product(sp, repeat=dim)]
+            rows += [list(t) for t in KATS[dim]]
+            x64 = np.array(rows, dtype=np.float64)
+            with np.errstate(over="ignore"):
+                x = x64.astype(np.float32).astype(np.float64) if single else x64
+            out[f"{prec}_{dim}_x"] = x
+            for fam in FAMILIES[dim]:
+                name = f"{fam}{dim}_{prec}" if fam != "quotient3_fast" else f"quotient3_fast_{prec}"
+                fc = getattr(comp, name)
+                fp = getattr(pure, name)
+                res = []
+                for row in x.tolist():
+                    args = (*ka, *row) if fam in SCALING else tuple(row)
+                    a = fc(*args)
+                    b = fp(*args)
+                    a = (a,) if not isinstance(a, tuple) else a
+                    b = (b,) if not isinstance(b, tuple) else b
+                    assert all(same(p, q) for p, q in zip(a, b)), (name, row, a, b)
+                    res.append(a)
+                out[f"{prec}_{name}"] = np.array(res, dtype=np.float64)
+            # loop checksums (reference timing loops) over the first 8 random rows
+            buf = x[:8]
+            flat = np.ascontiguousarray(buf.reshape(-1).astype(np.float32 if single else np.float64))
+            loops = {"scaling": f"loop_scaling{dim}", "quotient": f"loop_quotient{dim}",
+                     "naive": f"loop_naive{dim}", "empty": f"loop_empty{dim}"}
+            if dim == 3:
+                loops["quotient_fast"] = "loop_quotient_fast3"
+            for algo, base in loops.items():
+                fn = getattr(comp, f"{base}_{prec}")
+                if algo == "empty":
+                    val = fn(flat, 37, 7)
+                else:
+                    val = fn(flat, 37, 7, *ka)
+                out[f"{prec}_{dim}_loop_{algo}"] = np.array([val], dtype=np.float64)
+    for prec in ("f64", "f32"):
+        out[f"{prec}_ka"] = np.array(KA[prec], dtype=np.float64)
+    path = os.path.join(HERE, "golden_vectors.npz")
+    np.savez_compressed(path, **out)
+    n = sum(v.size for v in out.values())
+    print(f"wrote {path}: {len(out)} arrays, {n} values")
+
+
+if __name__ == "__main__":
+    main()

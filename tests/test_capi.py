@@ -1,0 +1,107 @@
+"""The C-ABI library loads and exports every entry point include/fastnorm_b200.h declares;
+argument errors are reported without touching a GPU (no compute calls here)."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_1606_06508_b200 import _lib
+
+HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                      "include", "fastnorm_b200.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(fn_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_full_registry():
+    names = set(declared_symbols())
+    for prec in ("f32", "f64"):
+        for dim in (2, 3, 4):
+            for fam in ("scale", "normalize", "norm", "naive", "quotient"):
+                assert f"fn_{fam}{dim}_{prec}" in names
+            assert f"fn_normalize{dim}_sq_{prec}" in names
+        assert f"fn_quotient3_fast_{prec}" in names
+    for extra in ("fn_run", "fn_host_run", "fn_generate", "fn_row_stats", "fn_last_error",
+                  "fn_version", "fn_build_flags", "fn_backend_name", "fn_device_count"):
+        assert extra in names
+
+
+def test_library_exports_every_declared_symbol():
+    L = _lib.lib()
+    missing = [s for s in declared_symbols() if not hasattr(L, s)]
+    assert not missing, missing
+
+
+def test_metadata():
+    L = _lib.lib()
+    assert L.fn_backend_name() == b"cuda"
+    assert b"sm_100a" in L.fn_version()
+    flags = _lib.build_flags()
+    assert "compute_100a" in flags and "-fmad=false" in flags and "-ftz=false" in flags
+
+
+def test_argument_errors_without_gpu():
+    L = _lib.lib()
+    x = np.zeros((4, 3))
+    h = np.zeros(4)
+    b = np.zeros((4, 3))
+    ka = np.array([2.0 ** -482, 2.0 ** 510, 2.0 ** 592, 2.0 ** -514, 2.0 ** -592, 2.0 ** 514])
+    vp = ctypes.c_void_p
+    # unknown op / dim / dtype / negative n / NULL outputs -> FN_EINVAL
+    assert L.fn_run(99, 3, 1, x.ctypes.data, 4, h.ctypes.data, b.ctypes.data, None, ka.ctypes.data, None) == -1
+    assert L.fn_run(1, 5, 1, x.ctypes.data, 4, h.ctypes.data, b.ctypes.data, None, ka.ctypes.data, None) == -1
+    assert L.fn_run(1, 3, 7, x.ctypes.data, 4, h.ctypes.data, b.ctypes.data, None, ka.ctypes.data, None) == -1
+    assert L.fn_run(1, 3, 1, x.ctypes.data, -1, h.ctypes.data, b.ctypes.data, None, ka.ctypes.data, None) == -1
+    assert L.fn_run(1, 3, 1, x.ctypes.data, 4, h.ctypes.data, None, None, ka.ctypes.data, None) == -1
+    assert b"body" in L.fn_last_error()
+    # norm has no body output; quotient3_fast is 3-D only; normalize_sq needs sq
+    assert L.fn_run(2, 3, 1, x.ctypes.data, 4, h.ctypes.data, b.ctypes.data, None, ka.ctypes.data, None) == -1
+    assert L.fn_run(5, 2, 1, x.ctypes.data, 4, h.ctypes.data, b.ctypes.data, None, None, None) == -1
+    assert L.fn_run(6, 3, 1, x.ctypes.data, 4, h.ctypes.data, b.ctypes.data, None, ka.ctypes.data, None) == -1
+    # scaling kernels need ka; negative / NaN tau is rejected (bit-pattern band test)
+    assert L.fn_run(1, 3, 1, x.ctypes.data, 4, h.ctypes.data, b.ctypes.data, None, None, None) == -1
+    bad = ka.copy()
+    bad[0] = -1.0
+    assert L.fn_run(1, 3, 1, x.ctypes.data, 4, h.ctypes.data, b.ctypes.data, None, bad.ctypes.data, None) == -1
+    bad[0] = np.nan
+    assert L.fn_run(1, 3, 1, x.ctypes.data, 4, h.ctypes.data, b.ctypes.data, None, bad.ctypes.data, None) == -1
+    assert b"tau" in L.fn_last_error()
+    # n == 0 is a no-op success
+    assert L.fn_run(1, 3, 1, vp(0), 0, vp(0), vp(0), None, ka.ctypes.data, None) == 0
+    assert L.fn_host_run(1, 3, 1, vp(0), 0, vp(0), vp(0), None, ka.ctypes.data) == 0
+    assert L.fn_generate(9, 0, 0, 4, x.ctypes.data, None) == -1
+    assert L.fn_row_stats(3, 1, x.ctypes.data, 4, None, ka.ctypes.data, None) == -1
+
+
+def test_named_entry_points_validate_like_fn_run():
+    L = _lib.lib()
+    f = L.fn_normalize3_f64
+    f.restype = ctypes.c_int
+    f.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                  ctypes.c_void_p, ctypes.c_void_p]
+    x = np.zeros((4, 3))
+    assert f(x.ctypes.data, 4, None, None, None, None) == -1  # NULL outputs
+    g = L.fn_norm4_f32
+    g.restype = ctypes.c_int
+    g.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    assert g(x.ctypes.data, 0, None, None, None) == 0  # empty batch
+
+
+def test_no_cpu_fallback_without_gpu():
+    """Without a CUDA device the product raises instead of computing on the CPU."""
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    import paper_1606_06508_b200 as fn
+
+    with pytest.raises(_lib.CudaLibraryError):
+        fn.normalize3(fn.preset("double"), np.ones((8, 3)))
+    with pytest.raises(_lib.CudaLibraryError):
+        fn.normalize3(fn.preset("double"), 3.0, 4.0, 12.0)

@@ -1,0 +1,199 @@
+"""GPU parity: every kernel family, both precisions, through the C ABI, bit for bit
+against the reference's golden vectors and the pinned oracle (reference rule: NaN
+matches NaN, everything else bit-equal including the sign of zero)."""
+
+import numpy as np
+import pytest
+
+from conftest import FAMILIES, SCALING, kernel_name, same_scalar
+from gpu_helpers import compare_chunked
+
+import oracle
+import paper_1606_06508_b200 as fn
+from paper_1606_06508_b200 import _backend, _cuda_kernels, _lib
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+OPS = {"scale": _lib.OP_SCALE, "normalize": _lib.OP_NORMALIZE, "norm": _lib.OP_NORM,
+       "naive": _lib.OP_NAIVE, "quotient": _lib.OP_QUOTIENT,
+       "quotient3_fast": _lib.OP_QUOTIENT3_FAST}
+PREC = {"f64": "double", "f32": "single"}
+
+
+def _base(fam, dim):
+    return "quotient3_fast" if fam == "quotient3_fast" else f"{fam}{dim}"
+
+
+def _golden_rows(golden, prec, dim):
+    x = golden[f"{prec}_{dim}_x"]
+    return x.astype(np.float32) if prec == "f32" else x
+
+
+def _as_table(res):
+    h = res.head.cpu().numpy() if hasattr(res.head, "cpu") else res.head
+    if res.body is None:
+        return h[:, None].astype(np.float64)
+    b = res.body.cpu().numpy() if hasattr(res.body, "cpu") else res.body
+    return np.concatenate([h[:, None], b], axis=1).astype(np.float64)
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("dim", [2, 3, 4])
+@pytest.mark.parametrize("where", ["device", "device_unaligned", "host"])
+def test_golden_vectors(golden, cuda_dev, prec, dim, where):
+    x = _golden_rows(golden, prec, dim)
+    ka = golden[f"{prec}_ka"]
+    for fam in FAMILIES[dim]:
+        k = _cuda_kernels.batch_kernel(_base(fam, dim), prec)
+        if where == "host":
+            res = k(x, ka if fam in SCALING else None)
+        elif where == "device":
+            res = k(torch.from_numpy(x).to(cuda_dev), ka if fam in SCALING else None)
+        else:  # one-row offset: 8/16/24/32-byte aligned rows -> per-row kernel path
+            big = torch.from_numpy(np.concatenate([x[:1], x])).to(cuda_dev)
+            res = k(big[1:], ka if fam in SCALING else None)
+        torch.cuda.synchronize()
+        got = _as_table(res)
+        ref = golden[f"{prec}_{kernel_name(fam, dim, prec)}"]
+        ok = oracle.same(got, ref)
+        bad = np.argwhere(~ok)
+        assert ok.all(), (fam, where, x[bad[0][0]], got[bad[0][0]], ref[bad[0][0]])
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_scalar_registry_calls(golden, cuda_dev, prec):
+    """The reference's scalar signatures, resolved through the registry, on the GPU."""
+    ka = tuple(golden[f"{prec}_ka"])
+    for dim in (2, 3, 4):
+        x = golden[f"{prec}_{dim}_x"]
+        idx = np.linspace(0, len(x) - 1, 12).astype(int)
+        for fam in FAMILIES[dim]:
+            k = _backend.scalar_kernel(_base(fam, dim), PREC[prec])
+            ref = golden[f"{prec}_{kernel_name(fam, dim, prec)}"]
+            for i in idx:
+                row = [float(v) for v in x[i]]
+                out = k(*ka, *row) if fam in SCALING else k(*row)
+                out = out if isinstance(out, tuple) else (out,)
+                assert all(same_scalar(a, b) for a, b in zip(out, ref[i])), (fam, row, out, ref[i])
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("dim", [2, 3, 4])
+def test_loop_checksums_through_gpu(golden, cuda_dev, prec, dim):
+    ka = tuple(golden[f"{prec}_ka"])
+    x = _golden_rows(golden, prec, dim)[:8]
+    flat = np.ascontiguousarray(x.reshape(-1))
+    algos = ["scaling", "quotient", "naive"] + (["quotient_fast"] if dim == 3 else [])
+    for algo in algos:
+        loop = _backend.loop_kernel(_backend.loop_base(algo, dim), PREC[prec])
+        got = loop(flat, 37, 7, *ka)
+        want = golden[f"{prec}_{dim}_loop_{algo}"][0]
+        assert got == want or (np.isnan(got) and np.isnan(want)), (algo, got, want)
+    got = _backend.loop_kernel(f"loop_empty{dim}", PREC[prec])(flat, 37, 7)
+    assert got == golden[f"{prec}_{dim}_loop_empty"][0]
+
+
+def _random_rows(n, dim, single, seed):
+    rng = np.random.default_rng(seed)
+    lo, hi = (-149, 128) if single else (-1074, 1024)
+    x = np.ldexp(1.0 + rng.random((n, dim)), rng.integers(lo, hi, (n, dim)))
+    x *= rng.integers(0, 2, (n, dim)) * 2 - 1
+    # sprinkle specials: zeros, signed zeros, inf, nan, in every position
+    sp = np.array([0.0, -0.0, np.inf, -np.inf, np.nan])
+    mask = rng.random((n, dim)) < 0.02
+    x[mask] = rng.choice(sp, mask.sum())
+    zero_rows = rng.random(n) < 0.01
+    x[zero_rows] = rng.choice([0.0, -0.0], (zero_rows.sum(), dim))
+    with np.errstate(over="ignore"):
+        return x.astype(np.float32) if single else x
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("dim", [2, 3, 4])
+@pytest.mark.parametrize("aligned", [True, False])
+def test_random_full_range_vs_oracle(cuda_dev, prec, dim, aligned):
+    n = (1 << 20) + 37
+    x = _random_rows(n + 1, dim, prec == "f32", seed=dim * 10 + (prec == "f32"))
+    xd = torch.from_numpy(x).to(cuda_dev)
+    xd = xd[:n] if aligned else xd[1:]
+    ka = np.array(fn.kernel_args(fn.preset(PREC[prec])))
+    for fam in FAMILIES[dim] + ["normalize_sq"]:
+        base = f"normalize{dim}_sq" if fam == "normalize_sq" else _base(fam, dim)
+        op = _lib.OP_NORMALIZE_SQ if fam == "normalize_sq" else OPS[fam]
+        takes = fam in SCALING or fam == "normalize_sq"
+        res = _cuda_kernels.batch_kernel(base, prec)(xd, ka if takes else None)
+        torch.cuda.synchronize()
+        bad, first = compare_chunked(op, xd, res.head, res.body, res.sq, ka if takes else None)
+        assert bad == 0, (fam, prec, dim, aligned, bad, first)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 15, 16, 17, 255, 256, 257, 511, 512, 513, 1023, 4097, 100_003])
+def test_tail_sizes(cuda_dev, n):
+    p = fn.preset("double")
+    ka = np.array(fn.kernel_args(p))
+    x = torch.from_numpy(_random_rows(n, 3, False, seed=n)).to(cuda_dev)
+    res = fn.normalize3(p, x)
+    torch.cuda.synchronize()
+    bad, first = compare_chunked(_lib.OP_NORMALIZE, x, res.length, res.unit, None, ka)
+    assert bad == 0, first
+    ps = fn.preset("single")
+    x32 = torch.from_numpy(_random_rows(n, 2, True, seed=n + 1)).to(cuda_dev)
+    r = fn.norm2(ps, x32)
+    torch.cuda.synchronize()
+    bad, first = compare_chunked(_lib.OP_NORM, x32, r, None, None, np.array(fn.kernel_args(ps)))
+    assert bad == 0, first
+
+
+def test_out_buffers_and_noncontiguous(cuda_dev):
+    p = fn.preset("double")
+    x = torch.from_numpy(_random_rows(5000, 4, False, seed=3)).to(cuda_dev)
+    r = torch.empty(5000, dtype=torch.float64, device=cuda_dev)
+    u = torch.empty((5000, 4), dtype=torch.float64, device=cuda_dev)
+    res = fn.normalize4(p, x, out=(r, u))
+    assert res.length.data_ptr() == r.data_ptr() and res.unit.data_ptr() == u.data_ptr()
+    ref = fn.normalize4(p, x.cpu().numpy())
+    torch.cuda.synchronize()
+    assert oracle.same(r.cpu().numpy(), ref.length).all()
+    assert oracle.same(u.cpu().numpy(), ref.unit).all()
+    # a strided view (every other row) is made contiguous internally
+    xs = x[::2]
+    res2 = fn.normalize4(p, xs)
+    torch.cuda.synchronize()
+    assert oracle.same(res2.unit.cpu().numpy(), ref.unit[::2]).all()
+    with pytest.raises(ValueError):
+        fn.normalize4(p, x, out=(r[:10], u))
+
+
+def test_norm_equals_normalize_length(cuda_dev):
+    for prec, dt in (("double", torch.float64), ("single", torch.float32)):
+        p = fn.preset(prec)
+        x = torch.from_numpy(_random_rows(1 << 20, 3, prec == "single", seed=9)).to(cuda_dev)
+        a = fn.norm3(p, x)
+        b = fn.normalize3(p, x).length
+        torch.cuda.synchronize()
+        assert oracle.same(a.cpu().numpy(), b.cpu().numpy()).all()
+
+
+def test_public_api_examples(cuda_dev):
+    """Known answers of the reference tests, through the batched device path."""
+    d = fn.preset("double")
+    x = torch.tensor([[3.0, 4.0, 0.0, 0.0], [1.0, 1.0, 1.0, 1.0], [0.0, 0.0, 0.0, 0.0],
+                      [2.0 ** -1074, 0.0, 0.0, 0.0]], dtype=torch.float64, device=cuda_dev)
+    res = fn.normalize4(d, x)
+    torch.cuda.synchronize()
+    assert res.length.tolist() == [5.0, 2.0, 0.0, 2.0 ** -1074]
+    assert res.unit[1].tolist() == [0.5] * 4
+    assert res.unit[2].tolist() == [0.0, 0.0, 0.0, 1.0]
+    q = fn.quotient4(x)
+    torch.cuda.synchronize()
+    assert q.unit[2].tolist() == [0.0] * 4 and q.length[1].item() == 2.0
+    nv = fn.naive_normalize2(torch.tensor([[2.0 ** -600, 0.0]], dtype=torch.float64, device=cuda_dev))
+    torch.cuda.synchronize()
+    assert nv.length.item() == 0.0 and nv.unit[0, 0].item() == float("inf")
+    # scalar signatures keep working (one launch per call)
+    assert fn.normalize2(d, 3.0, 4.0).length == 5.0
+    assert fn.norm3(d, 2.0, 10.0, 11.0) == 15.0
+    assert fn.quotient3_robust(0.0, 0.0, 0.0) == (0.0, (0.0, 0.0, 0.0))
+    assert fn.scale2(d, 2.0 ** -500, 0.0) == (2.0 ** -592, (2.0 ** 92, 0.0))

@@ -1,0 +1,81 @@
+"""Oracle vs the live reference (oracle/_ref, compiled from /root/reference by
+`make -C oracle ref`).  Skipped where the reference build is absent.
+
+Extends the golden pin to larger random sweeps (the test_backends.py:41-67 construction)
+and to rows of every BASELINE workload, including the reference timing-loop checksum
+over a workload sample (_kernels.pyx:646-789).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import FAMILIES, SCALING, kernel_name, same_scalar
+
+import oracle
+from paper_1606_06508_b200 import workloads
+
+REF = oracle.ref_module()
+pytestmark = pytest.mark.skipif(REF is None, reason="oracle/_ref not built")
+
+L = math.ldexp
+KA = {
+    "f64": (L(1, -482), L(1, 510), L(1, 592), L(1, -514), L(1, -592), L(1, 514)),
+    "f32": (L(1, -49), L(1, 62), L(1, 100), L(1, -66), L(1, -100), L(1, 66)),
+}
+
+
+def _rows_vs_reference(x: np.ndarray, prec: str, dim: int):
+    ka = KA[prec]
+    for fam in FAMILIES[dim]:
+        fn = getattr(REF, kernel_name(fam, dim, prec))
+        h, b, _ = oracle.run(oracle.BASE_OPS[fam], x, ka)
+        for i, row in enumerate(x.astype(np.float64).tolist()):
+            want = fn(*ka, *row) if fam in SCALING else fn(*row)
+            want = want if isinstance(want, tuple) else (want,)
+            got = (float(h[i]),) if b is None else (float(h[i]), *map(float, b[i]))
+            assert all(same_scalar(p, q) for p, q in zip(got, want)), (fam, prec, row, got, want)
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("dim", [2, 3, 4])
+def test_random_sweep_vs_reference(prec, dim):
+    rng = np.random.default_rng(7 + dim)
+    single = prec == "f32"
+    lo, hi = (-149, 127) if single else (-1074, 1023)
+    m = 3000
+    x = np.ldexp(1.0 + rng.random((m, dim)), rng.integers(lo, hi, (m, dim)))
+    x *= rng.integers(0, 2, (m, dim)) * 2 - 1
+    x = x.astype(np.float32) if single else x
+    _rows_vs_reference(x, prec, dim)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_workload_rows_vs_reference(cfg):
+    c = workloads.CONFIGS[cfg]
+    prec = "f64" if c.dtype == "float64" else "f32"
+    x = workloads.host_rows(cfg, 12345, 2000)
+    if cfg in (4, 5):  # make sure the sample holds the rare special rows too
+        rng = np.random.default_rng(cfg)
+        pool = workloads.host_rows(cfg, 0, 400_000)
+        sp = ~np.isfinite(pool).all(axis=1) | (np.abs(pool).max(axis=1) == 0)
+        if cfg == 5:
+            sp |= np.abs(pool).max(axis=1) > 2.0 ** 1022
+            sp |= np.abs(pool).max(axis=1) < 2.0 ** -1022
+        x = np.concatenate([x, pool[sp][:500]])
+        assert sp.sum() > 100
+        rng.shuffle(x)
+    _rows_vs_reference(x, prec, c.dim)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_loop_checksum_vs_reference(cfg):
+    c = workloads.CONFIGS[cfg]
+    x = workloads.host_rows(cfg, 0, 1 << 14)
+    flat = np.ascontiguousarray(x.reshape(-1))
+    ka = KA["f64"]
+    fn = getattr(REF, f"loop_scaling{c.dim}_f64")
+    want = fn(flat, 1 << 14, (1 << 14) - 1, *ka)
+    got = oracle.loop(oracle.ALGO_SCALING, x, 1 << 14, (1 << 14) - 1, ka)
+    assert got == want
