@@ -72,60 +72,96 @@ def _traffic_per_row():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    """SM clocks and throttle reasons sampled every 10 ms (NVML) during the timed region.
 
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    Falls back to `nvidia-smi -lms 200` when pynvml is unavailable."""
 
-    def __init__(self, index: int):
+    _REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+                0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index: int, period_s: float = 0.01):
         self.index = index
-        self.proc = None
-        self.lines: list[str] = []
+        self.period = period_s
+        self.sm: list[float] = []
+        self.smax = None
+        self.reasons: set[str] = set()
+        self._stop = threading.Event()
+        self._nvml = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
-            self._t.start()
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.smax = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            self._nvml = (pynvml, h)
         except Exception:
-            self.proc = None
+            self._nvml = None
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _sample_nvml(self):
+        pynvml, h = self._nvml
+        self.sm.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+        try:
+            bits = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except Exception:
+            bits = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        for mask, name in self._REASONS.items():
+            if bits & mask:
+                self.reasons.add(name)
+
+    def _run(self):
+        if self._nvml is not None:
+            while not self._stop.is_set():
+                try:
+                    self._sample_nvml()
+                except Exception:
+                    break
+                self._stop.wait(self.period)
+            return
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                     "--format=csv,noheader,nounits", "-lms", "200"],
+                                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            return
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        while not self._stop.is_set():
+            line = proc.stdout.readline()
+            if not line:
+                break
+            parts = [p.strip() for p in line.split(",")]
+            try:
+                self.sm.append(float(parts[0]))
+                self.smax = float(parts[1])
+            except (ValueError, IndexError):
+                continue
+            for name, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    self.reasons.add(name)
+        proc.terminate()
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
+        if self._nvml is not None:
+            try:  # one last sample so very short regions still get one
+                self._sample_nvml()
             except Exception:
-                self.proc.kill()
+                pass
+        self._stop.set()
+        self._t.join(timeout=5)
 
     def summary(self):
-        sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                smax = float(parts[1])
-            except ValueError:
-                continue
-            for name, v in zip(names, parts[3:7]):
-                if v.lower() == "active":
-                    reasons.add(name)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.smax, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.smax,
+                "reasons": sorted(self.reasons), "samples": len(self.sm),
+                "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
 def _dist_env():
@@ -135,11 +171,7 @@ def _dist_env():
     return rank, world, local
 
 
-def shard_range(n_total: int, rank: int, world: int) -> tuple[int, int]:
-    """Contiguous, balanced row shard [lo, hi) of rank (first n%world ranks get +1)."""
-    base, extra = divmod(n_total, world)
-    lo = rank * base + min(rank, extra)
-    return lo, lo + base + (1 if rank < extra else 0)
+from paper_1606_06508_b200.multigpu import shard_range  # noqa: E402
 
 
 # --------------------------------------------------------------------------------------
@@ -230,7 +262,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_1606_06508_b200 as fn
-    from paper_1606_06508_b200 import workloads
+    from paper_1606_06508_b200 import multigpu, workloads
 
     rank, world, local = _dist_env()
     if args.gpus != world and world > 1:
@@ -245,11 +277,7 @@ def run_ours(args):
             dist.barrier()
 
     def max_over_ranks(v: float) -> float:
-        if world == 1:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return multigpu.max_over_ranks(v, device=dev)
 
     p = fn.preset("double")
     ka = fn.kernel_args(p)
@@ -285,11 +313,7 @@ def run_ours(args):
         (ROWS_TOTAL // world * BYTES_PER_ROW) / per_launch_s / 1e9
 
     # ---------------- validation counters: one small NCCL all-reduce ----------------
-    counts = torch.zeros(6, dtype=torch.int64, device=dev)
-    workloads.row_stats_device(x, ka, counts.view(torch.uint64))
-    if world > 1:
-        dist.all_reduce(counts)
-    counts_h = counts.cpu().tolist()
+    counts_h = multigpu.reduce_counts(multigpu.shard_counts_device(x, ka))
     torch.cuda.synchronize(dev)
 
     # ---------------- end to end through the public API, host buffers ----------------
@@ -368,8 +392,7 @@ def run_ours(args):
             "gpu_launches": e2e_launches,
         },
         "validation": {
-            "row_classes": dict(zip(["nan", "inf", "zero", "below_tau_min", "above_tau_max", "in_band"],
-                                    counts_h)),
+            "row_classes": dict(zip(multigpu.COUNTER_NAMES, counts_h)),
             "rows_counted": int(sum(counts_h)),
             "reduce": "NCCL all_reduce(sum) of 6 counters" if world > 1 else "single rank",
         },

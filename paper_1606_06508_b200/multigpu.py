@@ -1,0 +1,56 @@
+"""Multi-GPU host logic: row sharding, max-over-ranks timing and the validation reduce.
+
+Rows are independent (no cross-row arithmetic anywhere in _kernels.pyx:167-412), so the
+batch shards into contiguous row ranges, one per rank (one process per GPU), with no
+collective on the data path.  The only collectives are two tiny all-reduces after the
+timed region: MAX of the elapsed time (the job takes as long as its slowest rank) and
+SUM of six row-class counters (validation statistics).  Works with any
+torch.distributed backend: NCCL on the B200 box, gloo for the CPU tests.
+"""
+
+from __future__ import annotations
+
+COUNTER_NAMES = ("nan", "inf", "zero", "below_tau_min", "above_tau_max", "in_band")
+
+
+def shard_range(n_total: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous balanced shard [lo, hi) of rank; the first n % world ranks get one more."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} / world {world}")
+    if n_total < 0:
+        raise ValueError("n_total must be >= 0")
+    base, extra = divmod(n_total, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def max_over_ranks(value: float, device=None) -> float:
+    """MAX of a per-rank scalar over the default process group (identity if single rank)."""
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def reduce_counts(counts):
+    """In-place SUM all-reduce of an int64 counter tensor; returns it as a list of ints."""
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(counts)
+    return [int(v) for v in counts.cpu().tolist()]
+
+
+def shard_counts_device(x, ka):
+    """Six row-class counters of a device shard (CUDA kernel fn_row_stats), as int64."""
+    import torch
+
+    from paper_1606_06508_b200 import workloads
+
+    counts = torch.zeros(6, dtype=torch.int64, device=x.device)
+    workloads.row_stats_device(x, ka, counts.view(torch.uint64))
+    return counts
