@@ -112,7 +112,7 @@ static int launch(const void* xv, int64_t n, void* hv, void* bv, void* qv, const
     if (aligned && !force_direct() && n >= (int64_t)L::TR) {
         const int64_t ntiles = n / L::TR;
         const int64_t per_sm =
-            std::min<int64_t>(TmaLaunch<T, N, OP>::blocks_per_sm(dev), Tile<T, N>::kCtasPerSm);
+            std::min<int64_t>(TmaLaunch<T, N, OP>::blocks_per_sm(dev), CtasPerSm<OP>::value);
         const int64_t resident = per_sm * sms;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, resident));
         tma_stream_kernel<T, N, OP>

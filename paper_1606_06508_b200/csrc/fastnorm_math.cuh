@@ -269,31 +269,35 @@ __device__ __forceinline__ void qf_pivot(T p, T a, T b, T& r, T& t, T& ua, T& ub
     ub = F::mul(qb, t);
 }
 
-// quotient3_fast: _kernels.pyx:365-412 (Alg 2) -- verbatim pivot order and ties.
+// quotient3_fast: _kernels.pyx:365-412 (Alg 2).  The reference's pivot decision tree
+// (verbatim comparisons, ties and zero test) is evaluated with selects instead of
+// branches, then ONE pivot body runs for every lane: each branch of the reference
+// computes the same formula (qf_pivot) on a permutation of (x1, x2, x3), so selecting
+// the operands first and permuting the results after gives identical values while a
+// warp with mixed pivots no longer executes three division sequences in turn.
+//   |x1| > |x2|:  |x3| > |x1| ? pivot x3 (a=x1, b=x2; u=(ua,ub,t))
+//                              : pivot x1 (a=x3, b=x2; u=(t,ub,ua))
+//   otherwise:    |x3| >= |x2| ? [x3 == 0 && !isnan(x1) -> zero] pivot x3 (u=(ua,ub,t))
+//                              : pivot x2 (a=x1, b=x3; u=(ua,t,ub))
 template <typename T>
 __device__ __forceinline__ void quotient3_fast_row(const T (&x)[3], T& r, T (&u)[3]) {
     using F = Fp<T>;
+    const T a1 = F::abs(x[0]), a2 = F::abs(x[1]), a3 = F::abs(x[2]);
+    const bool c1 = a1 > a2;
+    const bool piv3 = c1 ? (a3 > a1) : (a3 >= a2);
+    const bool piv1 = c1 && !piv3;
+    const bool piv2 = !c1 && !piv3;
+    const bool zero = !c1 && piv3 && x[2] == T(0) && !F::isnan_(x[0]);
+    const T p = piv3 ? x[2] : (piv1 ? x[0] : x[1]);
+    const T a = piv1 ? x[2] : x[0];
+    const T b = piv2 ? x[2] : x[1];
     T t, ua, ub;
-    if (F::abs(x[0]) > F::abs(x[1])) {
-        if (F::abs(x[2]) > F::abs(x[0])) {
-            qf_pivot(x[2], x[0], x[1], r, t, ua, ub);  // :369-377
-            u[0] = ua; u[1] = ub; u[2] = t;
-        } else {
-            qf_pivot(x[0], x[2], x[1], r, t, ua, ub);  // :378-386
-            u[0] = t; u[1] = ub; u[2] = ua;
-        }
-    } else {
-        if (F::abs(x[2]) >= F::abs(x[1])) {
-            if (x[2] == T(0) && !F::isnan_(x[0])) {  // :388-395
-                r = T(0); u[0] = T(0); u[1] = T(0); u[2] = T(0);
-                return;
-            }
-            qf_pivot(x[2], x[0], x[1], r, t, ua, ub);  // :396-403
-            u[0] = ua; u[1] = ub; u[2] = t;
-        } else {
-            qf_pivot(x[1], x[0], x[2], r, t, ua, ub);  // :404-412
-            u[0] = ua; u[1] = t; u[2] = ub;
-        }
+    qf_pivot(p, a, b, r, t, ua, ub);
+    u[0] = piv1 ? t : ua;
+    u[1] = piv2 ? t : ub;
+    u[2] = piv3 ? t : (piv1 ? ua : ub);
+    if (zero) {
+        r = T(0); u[0] = T(0); u[1] = T(0); u[2] = T(0);
     }
 }
 

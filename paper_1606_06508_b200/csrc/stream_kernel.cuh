@@ -190,17 +190,24 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
     return p;
 }
 
-// Default tile geometry per (T, N): ~6-8 KiB of input per stage (a multiple of 16 rows),
-// 4 stages, 2 resident CTAs per SM -> ~48-64 KiB of loads in flight per SM.  Measured on
-// B200 (tools/tune_stream.cu, profiles/r01_tune2.csv): more bytes in flight per SM (4
-// CTAs, or 8 stages) LOSES 6-8 % of DRAM throughput; 2 x 4 x 6 KiB reached 98 % of the
-// measured copy bandwidth.  L2 policy hints measured neutral (within noise) -> off.
+// Default tile geometry per (T, N): ~6-8 KiB of input per stage (a multiple of 16 rows)
+// and ~48 KiB of loads in flight per SM (stages x stage bytes x CTAs per SM).  Measured
+// on B200 (tools/tune_stream.cu; profiles/r01_tune2.csv, r01_tune3.csv): more bytes in
+// flight per SM (4 CTAs, or 8 stages) LOSES 6-8 % of DRAM throughput, while
+// 2 CTAs x 4 stages x 6 KiB reaches the cudaMemcpy bandwidth.  L2 policy hints measured
+// neutral (within noise) -> off.  The division-bound comparison variants (naive,
+// quotient) are FP64-issue bound instead and prefer full occupancy (kCtasPerSm below).
 template <typename T, int N> struct Tile {
     static constexpr int kRows = (N * (int)sizeof(T) <= 16) ? 512 : 256;
-    static constexpr int kStages = 4;
+    static constexpr int kStageBytes = kRows * N * (int)sizeof(T);
+    static constexpr int kStages = kStageBytes <= 6144 ? 4 : 3;
     static constexpr int kThreads = 256;
     static constexpr int kHints = 0;
-    static constexpr int kCtasPerSm = 2;
+};
+
+template <int OP> struct CtasPerSm {
+    static constexpr int value =
+        (OP == FN_OP_NAIVE || OP == FN_OP_QUOTIENT || OP == FN_OP_QUOTIENT3_FAST) ? 8 : 2;
 };
 
 template <typename T, int N, int OP, int TR_, int S_> struct TileLayout {

@@ -1,35 +1,35 @@
 // tune_stream.cu -- tile-geometry sweep for the streaming kernel (developer tool).
 //
-// Times tma_stream_kernel<double, 3, NORMALIZE> (the bench kernel) for several
-// (rows per tile, stages, threads, CTAs per SM) choices on BASELINE config-5 rows, and
-// two speed-of-light references with the same traffic mix (24 B read + 32 B written
-// per row): a 16-byte-vector read/write kernel and cudaMemcpy of the same byte count.
+// Times tma_stream_kernel<T, N, OP, TR, S, NT, HINTS> for several tile geometries and
+// CTAs-per-SM caps on BASELINE workload rows, for the kernel families the configs use,
+// plus speed-of-light references with the same traffic (cudaMemcpy D2D and a naive
+// 16-byte-vector read/write kernel).
 //
-// Build: make -C tools tune    Run: tools/tune_stream [log2_rows=28] [reps=20]
+// Build: make -C tools tune    Run: tools/tune_stream [log2_rows=28] [reps=10] [which=all]
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
-#include <algorithm>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "../paper_1606_06508_b200/csrc/stream_kernel.cuh"
 
 extern "C" int fn_generate(int cfg, uint64_t seed, int64_t row0, int64_t n, void* x, void* stream);
 
-#define CK(x)                                                                     \
-    do {                                                                          \
-        cudaError_t e_ = (x);                                                     \
-        if (e_ != cudaSuccess) {                                                  \
+#define CK(x)                                                                          \
+    do {                                                                               \
+        cudaError_t e_ = (x);                                                          \
+        if (e_ != cudaSuccess) {                                                       \
             fprintf(stderr, "%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e_)); \
-            exit(1);                                                              \
-        }                                                                         \
+            exit(1);                                                                   \
+        }                                                                              \
     } while (0)
 
 using namespace fnb;
 
-// 24 B read + 32 B written per row, 16-byte vectors, grid-stride over row pairs.
 __global__ void sol_kernel(const double2* __restrict__ x, int64_t npairs, double2* __restrict__ r,
                            double2* __restrict__ u) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npairs;
@@ -43,28 +43,45 @@ __global__ void sol_kernel(const double2* __restrict__ x, int64_t npairs, double
 }
 
 struct Bufs {
-    double *x, *r, *u;
+    void *x, *h, *b, *q;
     int64_t n;
 };
 
-template <int TR, int S, int NT, int H>
-float time_variant(const Bufs& b, const KArgs<double>& ka, int ctas_per_sm, int reps, int sms,
-                   int* occ_out) {
-    using L = TileLayout<double, 3, FN_OP_NORMALIZE, TR, S>;
-    auto kern = tma_stream_kernel<double, 3, FN_OP_NORMALIZE, TR, S, NT, H>;
+template <typename T>
+KArgs<T> make_ka() {
+    KArgs<T> ka;
+    const bool f = sizeof(T) == 4;
+    ka.tau_min = (T)(f ? 0x1p-49 : 0x1p-482);
+    ka.tau_max = (T)(f ? 0x1p62 : 0x1p510);
+    ka.sigma_min = (T)(f ? 0x1p100 : 0x1p592);
+    ka.sigma_max = (T)(f ? 0x1p-66 : 0x1p-514);
+    ka.inv_min = (T)(f ? 0x1p-100 : 0x1p-592);
+    ka.inv_max = (T)(f ? 0x1p66 : 0x1p514);
+    memcpy(&ka.tau_min_bits, &ka.tau_min, sizeof(T));
+    memcpy(&ka.tau_max_bits, &ka.tau_max, sizeof(T));
+    return ka;
+}
+
+template <typename T, int N, int OP, int TR, int S, int NT, int H>
+float time_variant(const Bufs& b, int cps, int reps, int sms, int* occ_out) {
+    using L = TileLayout<T, N, OP, TR, S>;
+    auto kern = tma_stream_kernel<T, N, OP, TR, S, NT, H>;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemBytes));
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, L::kSmemBytes));
     *occ_out = occ;
-    int per = ctas_per_sm > 0 ? (ctas_per_sm < occ ? ctas_per_sm : occ) : occ;
-    int64_t ntiles = b.n / TR;
-    int grid = (int)((int64_t)per * sms < ntiles ? (int64_t)per * sms : ntiles);
+    const int per = cps > 0 ? std::min(cps, occ) : occ;
+    const int64_t ntiles = b.n / TR;
+    const int grid = (int)std::min<int64_t>((int64_t)per * sms, ntiles);
+    const KArgs<T> ka = make_ka<T>();
+    const T* x = (const T*)b.x;
+    T *h = (T*)b.h, *bd = (T*)b.b, *q = (T*)b.q;
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
-    for (int i = 0; i < 2; ++i) kern<<<grid, NT, L::kSmemBytes>>>(b.x, b.n, b.r, b.u, nullptr, ka);
+    for (int i = 0; i < 2; ++i) kern<<<grid, NT, L::kSmemBytes>>>(x, b.n, h, bd, q, ka);
     CK(cudaEventRecord(e0));
-    for (int i = 0; i < reps; ++i) kern<<<grid, NT, L::kSmemBytes>>>(b.x, b.n, b.r, b.u, nullptr, ka);
+    for (int i = 0; i < reps; ++i) kern<<<grid, NT, L::kSmemBytes>>>(x, b.n, h, bd, q, ka);
     CK(cudaEventRecord(e1));
     CK(cudaEventSynchronize(e1));
     CK(cudaGetLastError());
@@ -76,85 +93,135 @@ float time_variant(const Bufs& b, const KArgs<double>& ka, int ctas_per_sm, int 
 }
 
 struct Variant {
-    const char* name;
-    int tr, s, nt, h, cps;
-    float (*fn)(const Bufs&, const KArgs<double>&, int, int, int, int*);
+    std::string fam;
+    int cfg, tr, s, nt, h, cps, bytes_per_row;
+    float (*fn)(const Bufs&, int, int, int, int*);
     std::vector<float> ms;
     int occ = 0;
 };
 
-#define V(TR, S, NT, H, CPS) \
-    Variant{"tma", TR, S, NT, H, CPS, &time_variant<TR, S, NT, H>, {}, 0}
+template <typename T, int N, int OP>
+constexpr int row_bytes() {
+    using Op = RowOp<T, N, OP>;
+    return (int)sizeof(T) * (N + 1 + (Op::kBody ? N : 0) + (Op::kSq ? 1 : 0));
+}
+
+#define V(FAM, CFG, T, N, OP, TR, S, NT, H, CPS)                                         \
+    Variant{FAM, CFG, TR, S, NT, H, CPS, row_bytes<T, N, OP>(),                          \
+            &time_variant<T, N, OP, TR, S, NT, H>, {}, 0}
 
 int main(int argc, char** argv) {
-    int lg = argc > 1 ? atoi(argv[1]) : 28;
-    int reps = argc > 2 ? atoi(argv[2]) : 20;
-    Bufs b;
-    b.n = (int64_t)1 << lg;
-    CK(cudaMalloc(&b.x, b.n * 24));
-    CK(cudaMalloc(&b.r, b.n * 8));
-    CK(cudaMalloc(&b.u, b.n * 24));
-    if (fn_generate(5, 5, 0, b.n, b.x, nullptr) != 0) return 1;
-    CK(cudaDeviceSynchronize());
+    const int lg = argc > 1 ? atoi(argv[1]) : 28;
+    const int reps = argc > 2 ? atoi(argv[2]) : 10;
+    const std::string which = argc > 3 ? argv[3] : "all";
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-    KArgs<double> ka;
-    ka.tau_min = 0x1p-482; ka.tau_max = 0x1p510; ka.sigma_min = 0x1p592; ka.sigma_max = 0x1p-514;
-    ka.inv_min = 0x1p-592; ka.inv_max = 0x1p514;
-    memcpy(&ka.tau_min_bits, &ka.tau_min, 8);
-    memcpy(&ka.tau_max_bits, &ka.tau_max, 8);
-    printf("rows=%lld sms=%d\n", (long long)b.n, sms);
+    const int64_t n = (int64_t)1 << lg;
+    Bufs b;
+    b.n = n;
+    // sized for the largest row (4 x f64 in, 4 x f64 body, head, sq)
+    CK(cudaMalloc(&b.x, n * 32));
+    CK(cudaMalloc(&b.h, n * 8));
+    CK(cudaMalloc(&b.b, n * 32));
+    CK(cudaMalloc(&b.q, n * 8));
+    printf("rows=%lld sms=%d\n", (long long)n, sms);
 
-    // speed-of-light references
-    {
+    if (which == "all" || which == "sol") {
+        CK(fn_generate(5, 5, 0, n, b.x, nullptr) == 0 ? cudaSuccess : cudaErrorUnknown);
         cudaEvent_t e0, e1;
         CK(cudaEventCreate(&e0));
         CK(cudaEventCreate(&e1));
-        int64_t np = b.n / 2;
-        for (int g : {sms * 4, sms * 8, sms * 16, sms * 32}) {
-            for (int i = 0; i < 3; ++i)
-                sol_kernel<<<g, 256>>>((const double2*)b.x, np, (double2*)b.r, (double2*)b.u);
+        for (int g : {sms * 8, sms * 32}) {
+            for (int i = 0; i < 2; ++i)
+                sol_kernel<<<g, 256>>>((const double2*)b.x, n / 2, (double2*)b.h, (double2*)b.b);
             CK(cudaEventRecord(e0));
             for (int i = 0; i < reps; ++i)
-                sol_kernel<<<g, 256>>>((const double2*)b.x, np, (double2*)b.r, (double2*)b.u);
+                sol_kernel<<<g, 256>>>((const double2*)b.x, n / 2, (double2*)b.h, (double2*)b.b);
             CK(cudaEventRecord(e1));
             CK(cudaEventSynchronize(e1));
             float ms;
             CK(cudaEventElapsedTime(&ms, e0, e1));
             ms /= reps;
-            printf("sol_vec16,grid=%d,ms=%.4f,GBps=%.1f\n", g, ms, b.n * 56.0 / (ms * 1e-3) / 1e9);
+            printf("sol_vec16_f64x3,grid=%d,ms=%.4f,GBps=%.1f\n", g, ms, n * 56.0 / (ms * 1e-3) / 1e9);
         }
-        // plain device copy of 28 B/row each way (same 56 B/row total traffic)
-        for (int i = 0; i < 3; ++i) CK(cudaMemcpy(b.u, b.x, b.n * 24, cudaMemcpyDeviceToDevice));
+        for (int i = 0; i < 2; ++i) CK(cudaMemcpy(b.b, b.x, n * 24, cudaMemcpyDeviceToDevice));
         CK(cudaEventRecord(e0));
-        for (int i = 0; i < reps; ++i) CK(cudaMemcpy(b.u, b.x, b.n * 24, cudaMemcpyDeviceToDevice));
+        for (int i = 0; i < reps; ++i) CK(cudaMemcpy(b.b, b.x, n * 24, cudaMemcpyDeviceToDevice));
         CK(cudaEventRecord(e1));
         CK(cudaEventSynchronize(e1));
         float ms;
         CK(cudaEventElapsedTime(&ms, e0, e1));
         ms /= reps;
-        printf("memcpy_d2d,bytes=%lld,ms=%.4f,GBps(r+w)=%.1f\n", (long long)(b.n * 24), ms,
-               b.n * 48.0 / (ms * 1e-3) / 1e9);
+        printf("memcpy_d2d,bytes=%lld,ms=%.4f,GBps(r+w)=%.1f\n", (long long)(n * 24), ms,
+               n * 48.0 / (ms * 1e-3) / 1e9);
         fflush(stdout);
     }
-    std::vector<Variant> vs = {
-        V(256, 4, 256, 1, 0), V(256, 4, 256, 1, 2), V(256, 4, 256, 1, 3), V(256, 4, 256, 0, 2),
-        V(256, 4, 256, 3, 2), V(256, 4, 256, 2, 2), V(256, 4, 256, 0, 4), V(256, 4, 256, 3, 4),
-        V(256, 8, 256, 1, 2), V(256, 6, 256, 1, 2), V(512, 4, 256, 1, 2), V(512, 4, 256, 3, 2),
-        V(512, 3, 512, 1, 2), V(512, 6, 512, 1, 1), V(1024, 3, 256, 1, 1), V(1024, 3, 256, 3, 1),
-        V(1024, 4, 512, 1, 1), V(128, 4, 128, 1, 4), V(128, 4, 128, 1, 3), V(128, 8, 128, 1, 3),
-        V(256, 2, 256, 1, 4), V(512, 2, 256, 1, 2),
-    };
+
+    std::vector<Variant> vs;
+    if (which == "all" || which == "f64x3") {
+        vs.push_back(V("normalize3_f64", 5, double, 3, FN_OP_NORMALIZE, 256, 4, 256, 0, 2));
+        vs.push_back(V("normalize3_f64", 5, double, 3, FN_OP_NORMALIZE, 256, 3, 256, 0, 2));
+        vs.push_back(V("normalize3_f64", 5, double, 3, FN_OP_NORMALIZE, 256, 5, 256, 0, 2));
+        vs.push_back(V("normalize3_f64", 5, double, 3, FN_OP_NORMALIZE, 128, 4, 128, 0, 4));
+        vs.push_back(V("normalize3_f64", 5, double, 3, FN_OP_NORMALIZE, 512, 2, 256, 0, 2));
+        vs.push_back(V("normalize3_f64", 5, double, 3, FN_OP_NORMALIZE, 512, 3, 512, 0, 1));
+        vs.push_back(V("normalize3_f64", 5, double, 3, FN_OP_NORMALIZE, 1024, 3, 256, 3, 1));
+        vs.push_back(V("normalize3_f64", 5, double, 3, FN_OP_NORMALIZE, 256, 4, 128, 0, 2));
+        vs.push_back(V("normalize3_f64", 5, double, 3, FN_OP_NORMALIZE, 256, 4, 512, 0, 2));
+        vs.push_back(V("norm3_f64", 5, double, 3, FN_OP_NORM, 256, 4, 256, 0, 2));
+        vs.push_back(V("scale3_f64", 5, double, 3, FN_OP_SCALE, 256, 4, 256, 0, 2));
+        vs.push_back(V("quotient3_f64", 5, double, 3, FN_OP_QUOTIENT, 256, 4, 256, 0, 2));
+        vs.push_back(V("quotient3_f64", 5, double, 3, FN_OP_QUOTIENT, 256, 4, 256, 0, 4));
+        vs.push_back(V("quotient3_fast_f64", 5, double, 3, FN_OP_QUOTIENT3_FAST, 256, 4, 256, 0, 2));
+        vs.push_back(V("quotient3_fast_f64", 5, double, 3, FN_OP_QUOTIENT3_FAST, 256, 4, 256, 0, 4));
+        vs.push_back(V("naive3_f64", 5, double, 3, FN_OP_NAIVE, 256, 4, 256, 0, 2));
+    }
+    if (which == "all" || which == "f64x2") {
+        vs.push_back(V("normalize2_f64", 2, double, 2, FN_OP_NORMALIZE, 512, 4, 256, 0, 2));
+        vs.push_back(V("normalize2_f64", 2, double, 2, FN_OP_NORMALIZE, 256, 4, 256, 0, 2));
+        vs.push_back(V("normalize2_f64", 2, double, 2, FN_OP_NORMALIZE, 512, 2, 256, 0, 3));
+        vs.push_back(V("normalize2_f64", 2, double, 2, FN_OP_NORMALIZE, 256, 4, 256, 0, 3));
+        vs.push_back(V("quotient2_f64", 2, double, 2, FN_OP_QUOTIENT, 512, 4, 256, 0, 2));
+        vs.push_back(V("quotient2_f64", 2, double, 2, FN_OP_QUOTIENT, 256, 4, 256, 0, 4));
+    }
+    if (which == "all" || which == "f64x4") {
+        vs.push_back(V("normalize4_sq_f64", 3, double, 4, FN_OP_NORMALIZE_SQ, 256, 4, 256, 0, 2));
+        vs.push_back(V("normalize4_sq_f64", 3, double, 4, FN_OP_NORMALIZE_SQ, 128, 4, 128, 0, 4));
+        vs.push_back(V("normalize4_sq_f64", 3, double, 4, FN_OP_NORMALIZE_SQ, 256, 3, 256, 0, 2));
+        vs.push_back(V("normalize4_sq_f64", 3, double, 4, FN_OP_NORMALIZE_SQ, 128, 4, 256, 0, 2));
+        vs.push_back(V("normalize4_f64", 3, double, 4, FN_OP_NORMALIZE, 256, 4, 256, 0, 2));
+        vs.push_back(V("quotient4_f64", 3, double, 4, FN_OP_QUOTIENT, 256, 4, 256, 0, 2));
+    }
+    if (which == "all" || which == "f32x3") {
+        vs.push_back(V("normalize3_f32", 4, float, 3, FN_OP_NORMALIZE, 512, 4, 256, 0, 2));
+        vs.push_back(V("normalize3_f32", 4, float, 3, FN_OP_NORMALIZE, 256, 4, 256, 0, 2));
+        vs.push_back(V("normalize3_f32", 4, float, 3, FN_OP_NORMALIZE, 512, 4, 256, 0, 3));
+        vs.push_back(V("normalize3_f32", 4, float, 3, FN_OP_NORMALIZE, 1024, 4, 256, 0, 2));
+        vs.push_back(V("normalize3_f32", 4, float, 3, FN_OP_NORMALIZE, 1024, 2, 256, 0, 2));
+        vs.push_back(V("quotient3_f32", 4, float, 3, FN_OP_QUOTIENT, 512, 4, 256, 0, 2));
+    }
+    // generate the input each variant family needs (configs 2..5) once per group
+    int cur_cfg = -1;
     const int rounds = 3;
-    for (int rd = 0; rd < rounds; ++rd)
-        for (auto& v : vs) v.ms.push_back(v.fn(b, ka, v.cps, reps, sms, &v.occ));
+    for (int rd = 0; rd < rounds; ++rd) {
+        for (auto& v : vs) {
+            if (v.cfg != cur_cfg) {
+                CK(fn_generate(v.cfg, v.cfg, 0, n, b.x, nullptr) == 0 ? cudaSuccess : cudaErrorUnknown);
+                CK(cudaDeviceSynchronize());
+                cur_cfg = v.cfg;
+            }
+            v.ms.push_back(v.fn(b, v.cps, reps, sms, &v.occ));
+        }
+    }
     for (auto& v : vs) {
         std::vector<float> m = v.ms;
         std::sort(m.begin(), m.end());
-        float med = m[m.size() / 2];
-        printf("tma,TR=%d,S=%d,NT=%d,HINTS=%d,occ=%d,ctas_per_sm=%d,ms_med=%.4f,ms_min=%.4f,GBps_med=%.1f,GBps_best=%.1f\n",
-               v.tr, v.s, v.nt, v.h, v.occ, v.cps == 0 ? v.occ : std::min(v.cps, v.occ), med, m[0],
-               b.n * 56.0 / (med * 1e-3) / 1e9, b.n * 56.0 / (m[0] * 1e-3) / 1e9);
+        const float med = m[m.size() / 2];
+        printf("%s,cfg=%d,TR=%d,S=%d,NT=%d,HINTS=%d,occ=%d,ctas_per_sm=%d,B/row=%d,ms_med=%.4f,"
+               "GBps_med=%.1f,GBps_best=%.1f,Gvecps_med=%.2f\n",
+               v.fam.c_str(), v.cfg, v.tr, v.s, v.nt, v.h, v.occ, v.cps == 0 ? v.occ : std::min(v.cps, v.occ),
+               v.bytes_per_row, med, n * (double)v.bytes_per_row / (med * 1e-3) / 1e9,
+               n * (double)v.bytes_per_row / (m[0] * 1e-3) / 1e9, n / (med * 1e-3) / 1e9);
     }
     return 0;
 }
