@@ -152,6 +152,13 @@ int fn_row_stats(int dim, int dtype, const void* x, int64_t n, uint64_t* counts,
  * 5: 3/f64). */
 int fn_generate(int cfg, uint64_t seed, int64_t row0, int64_t n, void* x, void* stream);
 
+/* ---- device self-test of the shared-divisor division (fastnorm_math.cuh) ----------- */
+/* Compares the kernels' correctly-rounded division against the CUDA math library's
+ * IEEE division on n generated operand pairs (full range, mantissa / exponent edge
+ * cases, specials).  out: device array of 3 uint64 (zero it first) -> [0] mismatches,
+ * [1], [2] bit patterns of the first mismatching numerator / divisor. */
+int fn_selftest_div(int dtype, uint64_t seed, int64_t n, uint64_t* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -53,6 +53,8 @@ def _declare(L: ctypes.CDLL) -> None:
     L.fn_host_run.argtypes = [_int, _int, _int, _vp, _i64, _vp, _vp, _vp, _vp]
     L.fn_generate.restype = _int
     L.fn_generate.argtypes = [_int, ctypes.c_uint64, _i64, _i64, _vp, _vp]
+    L.fn_selftest_div.restype = _int
+    L.fn_selftest_div.argtypes = [_int, ctypes.c_uint64, _i64, _vp, _vp]
     L.fn_row_stats.restype = _int
     L.fn_row_stats.argtypes = [_int, _int, _vp, _i64, _vp, _vp, _vp]
 

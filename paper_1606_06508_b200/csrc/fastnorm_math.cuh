@@ -96,6 +96,103 @@ __device__ __forceinline__ bool scale_classified(const T (&x)[N], const KArgs<T>
     return m != 0;
 }
 
+// ---------------------------------------------------------------------------------
+// Correctly rounded division by a shared divisor (the quotient / naive families divide
+// n numerators by the same m, h or r; _kernels.pyx:262-362).
+//
+// Fast path (binary64): y = RN(1/b) once per divisor (__drcp_rn), then per numerator
+//   q0 = RN(a*y); r0 = fma(-b, q0, a); q1 = fma(r0, y, q0)     -> q1 faithful
+//   r1 = fma(-b, q1, a)  (exact: remainder of a faithful quotient, Boldo-Daumas)
+//   q2 = fma(r1, y, q1)  == RN(a/b)  (Markstein: y = RN(1/b), q1 faithful, r1 exact)
+// valid while a >= 2^-967, 2^-1020 <= |b| < 2^1022 and the quotient exponent is in
+// [-967, 1021] (no subnormal intermediate or result).  Outside that range: an exactly
+// zero numerator gives the signed zero; a quotient provably below 2^-1075 rounds to the
+// signed zero (|a/b| < 2^(ea - eb + 1)); everything else (subnormal results, zero /
+// inf / NaN divisors) takes the IEEE __ddiv_rn.  This keeps the very common "tiny
+// component over huge max" case of wide-range rows off the slow path.
+//
+// binary32: the numerator and divisor are widened to binary64 (exactly), divided with
+// the binary64 fast path above (always in range for float operands) and rounded once to
+// binary32.  Double rounding is innocuous for division since 53 >= 2*24 + 2 (the same
+// argument the reference's pure-Python twin relies on, _pykernels.py:7-11), including
+// subnormal float results (a midpoint of the subnormal grid has <= 24 significant bits,
+// so a binary64 quotient can only land on it when it is exact).  Every case is checked
+// bit for bit against __ddiv_rn / __fdiv_rn by fn_selftest_div (tests/test_gpu_parity.py).
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ double div_markstein(double a, double b, double y) {
+    const double q0 = __dmul_rn(a, y);
+    const double r0 = __fma_rn(-b, q0, a);
+    const double q1 = __fma_rn(r0, y, q0);
+    const double r1 = __fma_rn(-b, q1, a);
+    return __fma_rn(r1, y, q1);
+}
+
+__device__ __forceinline__ int biased_exp(double v) {
+    return (int)(((unsigned)__double2hiint(v) >> 20) & 0x7ffu);
+}
+
+__device__ __forceinline__ double signed_zero_of_quotient(double a, double b) {
+    const long long s = (__double_as_longlong(a) ^ __double_as_longlong(b)) & (long long)0x8000000000000000ull;
+    return __longlong_as_double(s);
+}
+
+template <typename T> struct Divider;
+
+// FNB_F64_DIV_MARKSTEIN = 1 selects the shared-reciprocal fast path above for binary64;
+// 0 divides with __ddiv_rn per numerator.  Both are correctly rounded; which is faster
+// depends on how often rows need the subnormal-result slow path (tools/tune_stream).
+#ifndef FNB_F64_DIV_MARKSTEIN
+#define FNB_F64_DIV_MARKSTEIN 0
+#endif
+
+#if !FNB_F64_DIV_MARKSTEIN
+template <> struct Divider<double> {
+    double b;
+    __device__ __forceinline__ explicit Divider(double b_) : b(b_) {}
+    __device__ __forceinline__ double operator()(double a) const { return __ddiv_rn(a, b); }
+};
+#else
+template <> struct Divider<double> {
+    double b, y;
+    int eb;
+    bool bfast;
+    __device__ __forceinline__ explicit Divider(double b_) : b(b_) {
+        eb = biased_exp(b_);
+        bfast = eb >= 3 && eb <= 2044;
+        y = __drcp_rn(bfast ? b_ : 1.0);
+    }
+    __device__ __forceinline__ double operator()(double a) const {
+        const int ea = biased_exp(a);
+        const int d = ea - eb;
+        const double fast = div_markstein(a, b, y);
+        if (bfast && ea >= 56 && ea <= 2046 && d >= -967 && d <= 1021) return fast;
+        const bool b_finite_nonzero = eb <= 2046 && b != 0.0;
+        // exact zero numerator, or a quotient provably below half the least subnormal
+        if (b_finite_nonzero && ea <= 2046 &&
+            (a == 0.0 || (ea >= 1 && eb >= 1 && d <= -1076) || (ea == 0 && eb >= 1076)))
+            return signed_zero_of_quotient(a, b);
+        return __ddiv_rn(a, b);
+    }
+};
+#endif
+
+template <> struct Divider<float> {
+    double b, y;
+    bool bok;
+    __device__ __forceinline__ explicit Divider(float b_) : b((double)b_) {
+        bok = isfinite(b_) && b_ != 0.0f;
+        y = __drcp_rn(bok ? b : 1.0);
+    }
+    __device__ __forceinline__ float operator()(float a) const {
+        const double ad = (double)a;
+        if (bok && isfinite(a)) {
+            if (a == 0.0f) return __double2float_rn(signed_zero_of_quotient(ad, b));
+            return __double2float_rn(div_markstein(ad, b, y));
+        }
+        return __double2float_rn(__ddiv_rn(ad, b));
+    }
+};
+
 // Left-to-right sum of squares without contraction: ((s1^2 + s2^2) + s3^2) + s4^2.
 template <typename T, int N>
 __device__ __forceinline__ T sum_squares(const T (&s)[N]) {
@@ -222,8 +319,9 @@ __device__ __forceinline__ void naive_row(const T (&x)[N], T& r, T (&u)[N]) {
     using F = Fp<T>;
     const T rr = F::sqrt(sum_squares<T, N>(x));
     r = rr;
+    const Divider<T> by_r(rr);
 #pragma unroll
-    for (int k = 0; k < N; ++k) u[k] = F::div(x[k], rr);
+    for (int k = 0; k < N; ++k) u[k] = by_r(x[k]);
 }
 
 // quotient{2,3,4}: _kernels.pyx:288-362 (Alg 1 generalised).  m = max via strict '>',
@@ -247,12 +345,14 @@ __device__ __forceinline__ void quotient_row(const T (&x)[N], T& r, T (&u)[N]) {
         return;
     }
     T q[N];
+    const Divider<T> by_m(m);
 #pragma unroll
-    for (int k = 0; k < N; ++k) q[k] = F::div(x[k], m);
+    for (int k = 0; k < N; ++k) q[k] = by_m(x[k]);
     const T h = F::sqrt(sum_squares<T, N>(q));
     r = F::mul(m, h);
+    const Divider<T> by_h(h);
 #pragma unroll
-    for (int k = 0; k < N; ++k) u[k] = F::div(q[k], h);
+    for (int k = 0; k < N; ++k) u[k] = by_h(q[k]);
 }
 
 // Shared body of the pivoted fast quotient (_kernels.pyx:370-377 and siblings):
@@ -260,8 +360,9 @@ __device__ __forceinline__ void quotient_row(const T (&x)[N], T& r, T (&u)[N]) {
 template <typename T>
 __device__ __forceinline__ void qf_pivot(T p, T a, T b, T& r, T& t, T& ua, T& ub) {
     using F = Fp<T>;
-    const T qa = F::div(a, p);
-    const T qb = F::div(b, p);
+    const Divider<T> by_p(p);
+    const T qa = by_p(a);
+    const T qb = by_p(b);
     const T h = F::sqrt(F::add(F::add(T(1), F::mul(qa, qa)), F::mul(qb, qb)));
     t = F::div(F::sign1(p), h);
     r = F::mul(F::abs(p), h);

@@ -1,0 +1,147 @@
+// selftest.cu -- device self-test of the shared-divisor division (fastnorm_math.cuh).
+//
+// fn_selftest_div(dtype, seed, n, out, stream) evaluates Divider<T>(b)(a) for n
+// generated operand pairs and compares each result bit for bit (NaN == NaN) with the
+// IEEE division of the CUDA math library (__ddiv_rn / __fdiv_rn).  Operands mix
+// full-range random bit patterns, all-ones / power-of-two mantissas, exponents at and
+// around every boundary of the fast path, quotient-algorithm shaped pairs (|a| <= |b|)
+// and IEEE specials.  out[0] = mismatches, out[1] / out[2] = bits of the first
+// mismatching a / b (device array of 3 uint64, zero it first).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "fastnorm_math.cuh"
+#include "../../include/fastnorm_b200.h"
+
+namespace fnb {
+int set_error(int code, const char* msg);
+}
+
+namespace {
+
+__device__ __forceinline__ uint64_t mix(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__device__ uint64_t make_f64(uint64_t w0, uint64_t w1, int kind) {
+    const uint64_t sign = w1 & 0x8000000000000000ull;
+    uint64_t mant = w0 & 0x000FFFFFFFFFFFFFull;
+    uint64_t exp = (w0 >> 52) & 0x7ffull;
+    switch (kind) {
+        case 0: break;                                                  // full range
+        case 1: mant = 0x000FFFFFFFFFFFFFull; break;                    // all-ones mantissa
+        case 2: mant = 0; break;                                        // power of two
+        case 3: mant = (w1 >> 20) & 3; break;                           // just above 2^e
+        case 4: exp = (w1 >> 40) % 80; break;                           // bottom of the range
+        case 5: exp = 2046 - (w1 >> 40) % 40; break;                    // top of the range
+        case 6: exp = 1023 + (int)((w1 >> 40) % 64) - 32; break;        // moderate
+        default: break;
+    }
+    if (exp == 2047) exp = 2046;
+    return sign | (exp << 52) | mant;
+}
+
+__device__ double special_f64(uint64_t w) {
+    switch (w % 8) {
+        case 0: return 0.0;
+        case 1: return -0.0;
+        case 2: return __longlong_as_double(0x7ff0000000000000ll);
+        case 3: return __longlong_as_double(0xfff0000000000000ll);
+        case 4: return __longlong_as_double(0x7ff8000000000000ll);
+        case 5: return __longlong_as_double((long long)((w >> 12) & 0x000FFFFFFFFFFFFFull) | 1);
+        case 6: return 1.7976931348623157e308;
+        default: return 4.9406564584124654e-324;
+    }
+}
+
+__global__ void selftest_f64(uint64_t seed, int64_t n, unsigned long long* out) {
+    unsigned long long bad = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t w0 = mix(seed + 4 * (uint64_t)i), w1 = mix(seed + 4 * (uint64_t)i + 1);
+        const uint64_t w2 = mix(seed + 4 * (uint64_t)i + 2), w3 = mix(seed + 4 * (uint64_t)i + 3);
+        const int cat = (int)(w3 % 16);
+        double a, b;
+        if (cat < 12) {
+            a = __longlong_as_double((long long)make_f64(w0, w1, (int)((w3 >> 8) % 7)));
+            b = __longlong_as_double((long long)make_f64(w2, w1 << 1, (int)((w3 >> 16) % 7)));
+            if (cat >= 9) {  // quotient shaped: |a| <= |b|, exponent gap anywhere
+                const double fa = fabs(a), fb = fabs(b);
+                if (fa > fb) { const double t = a; a = b; b = t; }
+            }
+        } else if (cat < 14) {  // exponent difference pinned near the path boundaries
+            const int targets[8] = {-1078, -1076, -1075, -1074, -1023, -968, -967, 1021};
+            const int d = targets[(w3 >> 8) % 8] + (int)((w3 >> 16) % 5) - 2;
+            int eb = 1 + (int)((w2 >> 52) % 2046);
+            int ea = eb + d;
+            if (ea < 0) ea = 0;
+            if (ea > 2046) { eb -= ea - 2046; ea = 2046; }
+            a = __longlong_as_double((long long)((w1 & 0x8000000000000000ull) | ((uint64_t)ea << 52) |
+                                                 (w0 & 0x000FFFFFFFFFFFFFull)));
+            b = __longlong_as_double((long long)(((uint64_t)(eb < 0 ? 0 : eb) << 52) |
+                                                 (w2 & 0x000FFFFFFFFFFFFFull)));
+        } else {
+            a = (w3 >> 8) & 1 ? special_f64(w0) : __longlong_as_double((long long)make_f64(w0, w1, 0));
+            b = (w3 >> 9) & 1 ? special_f64(w2) : __longlong_as_double((long long)make_f64(w2, w1, 0));
+        }
+        const double got = fnb::Divider<double>(b)(a);
+        const double want = __ddiv_rn(a, b);
+        const bool ok = (__double_as_longlong(got) == __double_as_longlong(want)) ||
+                        (isnan(got) && isnan(want));
+        if (!ok) {
+            ++bad;
+            if (atomicCAS(out + 1, 0ull, (unsigned long long)__double_as_longlong(a)) == 0ull)
+                out[2] = (unsigned long long)__double_as_longlong(b);
+        }
+    }
+    if (bad) atomicAdd(out, bad);
+}
+
+__global__ void selftest_f32(uint64_t seed, int64_t n, unsigned long long* out) {
+    unsigned long long bad = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t w0 = mix(seed + 2 * (uint64_t)i), w1 = mix(seed + 2 * (uint64_t)i + 1);
+        unsigned ua = (unsigned)w0, ub = (unsigned)(w0 >> 32);
+        const int cat = (int)(w1 % 8);
+        if (cat == 1) ub = (ub & 0xff800000u) | 0x007fffffu;      // all-ones mantissa
+        if (cat == 2) ub &= 0xff800000u;                          // power of two
+        if (cat == 3) ua &= 0x807fffffu;                          // subnormal numerator
+        if (cat == 4) ub &= 0x807fffffu;                          // subnormal divisor
+        if (cat == 5) {                                           // quotient shaped
+            if ((ua & 0x7fffffffu) > (ub & 0x7fffffffu)) { unsigned t = ua; ua = ub; ub = t; }
+        }
+        float a = __uint_as_float(ua), b = __uint_as_float(ub);
+        if (cat == 6) a = (w1 >> 8) & 1 ? 0.0f : -0.0f;
+        const float got = fnb::Divider<float>(b)(a);
+        const float want = __fdiv_rn(a, b);
+        const bool ok = (__float_as_uint(got) == __float_as_uint(want)) || (isnan(got) && isnan(want));
+        if (!ok) {
+            ++bad;
+            if (atomicCAS(out + 1, 0ull, (unsigned long long)__float_as_uint(a) | (1ull << 63)) == 0ull)
+                out[2] = (unsigned long long)__float_as_uint(b);
+        }
+    }
+    if (bad) atomicAdd(out, bad);
+}
+
+}  // namespace
+
+extern "C" int fn_selftest_div(int dtype, uint64_t seed, int64_t n, uint64_t* out, void* stream) {
+    if (n < 0 || !out) return fnb::set_error(FN_EINVAL, "bad arguments");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    unsigned long long* o = reinterpret_cast<unsigned long long*>(out);
+    if (dtype == FN_F64)
+        selftest_f64<<<148 * 16, 256, 0, s>>>(seed, n, o);
+    else if (dtype == FN_F32)
+        selftest_f32<<<148 * 16, 256, 0, s>>>(seed, n, o);
+    else
+        return fnb::set_error(FN_EINVAL, "dtype must be FN_F32/FN_F64");
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fnb::set_error(FN_ECUDA, cudaGetErrorString(e));
+    return FN_OK;
+}

@@ -197,3 +197,17 @@ def test_public_api_examples(cuda_dev):
     assert fn.norm3(d, 2.0, 10.0, 11.0) == 15.0
     assert fn.quotient3_robust(0.0, 0.0, 0.0) == (0.0, (0.0, 0.0, 0.0))
     assert fn.scale2(d, 2.0 ** -500, 0.0) == (2.0 ** -592, (2.0 ** 92, 0.0))
+
+
+@pytest.mark.parametrize("dtype", [_lib.F64, _lib.F32])
+def test_division_selftest(cuda_dev, dtype):
+    """The shared-divisor division equals IEEE division bit for bit on 2^28 pairs."""
+    out = torch.zeros(3, dtype=torch.int64, device=cuda_dev)
+    for seed in (1, 2):
+        out.zero_()
+        rc = _lib.lib().fn_selftest_div(dtype, seed, 1 << 27, out.data_ptr(),
+                                        torch.cuda.current_stream().cuda_stream)
+        _lib.check(rc, "fn_selftest_div")
+        torch.cuda.synchronize()
+        bad, a, b = out.tolist()
+        assert bad == 0, (dtype, seed, bad, hex(a & (2**64 - 1)), hex(b & (2**64 - 1)))

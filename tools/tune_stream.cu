@@ -176,6 +176,19 @@ int main(int argc, char** argv) {
         vs.push_back(V("quotient3_fast_f64", 5, double, 3, FN_OP_QUOTIENT3_FAST, 256, 4, 256, 0, 4));
         vs.push_back(V("naive3_f64", 5, double, 3, FN_OP_NAIVE, 256, 4, 256, 0, 2));
     }
+    if (which == "all" || which == "div") {
+        vs.push_back(V("quotient3_f64", 1, double, 3, FN_OP_QUOTIENT, 256, 4, 256, 0, 4));
+        vs.push_back(V("quotient3_fast_f64", 1, double, 3, FN_OP_QUOTIENT3_FAST, 256, 4, 256, 0, 4));
+        vs.push_back(V("naive3_f64", 1, double, 3, FN_OP_NAIVE, 256, 4, 256, 0, 4));
+        vs.push_back(V("quotient3_f64", 5, double, 3, FN_OP_QUOTIENT, 256, 4, 256, 0, 4));
+        vs.push_back(V("quotient3_fast_f64", 5, double, 3, FN_OP_QUOTIENT3_FAST, 256, 4, 256, 0, 4));
+        vs.push_back(V("naive3_f64", 5, double, 3, FN_OP_NAIVE, 256, 4, 256, 0, 4));
+        vs.push_back(V("quotient2_f64", 2, double, 2, FN_OP_QUOTIENT, 256, 4, 256, 0, 4));
+        vs.push_back(V("quotient4_f64", 3, double, 4, FN_OP_QUOTIENT, 256, 4, 256, 0, 4));
+        vs.push_back(V("quotient3_f32", 4, float, 3, FN_OP_QUOTIENT, 512, 4, 256, 0, 4));
+        vs.push_back(V("quotient3_fast_f32", 4, float, 3, FN_OP_QUOTIENT3_FAST, 512, 4, 256, 0, 4));
+        vs.push_back(V("naive3_f32", 4, float, 3, FN_OP_NAIVE, 512, 4, 256, 0, 4));
+    }
     if (which == "all" || which == "f64x2") {
         vs.push_back(V("normalize2_f64", 2, double, 2, FN_OP_NORMALIZE, 512, 4, 256, 0, 2));
         vs.push_back(V("normalize2_f64", 2, double, 2, FN_OP_NORMALIZE, 256, 4, 256, 0, 2));
