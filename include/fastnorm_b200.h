@@ -63,7 +63,14 @@ typedef enum {
     FN_OP_NAIVE = 3,          /* naive{2,3,4}        _kernels.pyx:262-285 */
     FN_OP_QUOTIENT = 4,       /* quotient{2,3,4}     _kernels.pyx:288-362 */
     FN_OP_QUOTIENT3_FAST = 5, /* quotient3_fast      _kernels.pyx:365-412 */
-    FN_OP_NORMALIZE_SQ = 6    /* normalize{2,3,4} + squared length (BASELINE config 3) */
+    FN_OP_NORMALIZE_SQ = 6,   /* normalize{2,3,4} + squared length (BASELINE config 3) */
+    /* Rotations of quaternions (rotation.py:53-111; dim 4, FN_F64 only).  head = R[N,3,3]
+     * row-major.  Rows the reference rejects with ValueError (non-finite; zero for the
+     * general form) get NaN matrices and are counted into *invalid (fn_run_rot). */
+    FN_OP_ROT_UNIT = 7,       /* rotation_unit(q)                      rotation.py:87-111 */
+    FN_OP_ROT_GENERAL = 8,    /* rotation_general(q) via scale4        rotation.py:53-84  */
+    FN_OP_NORMALIZE_ROT = 9   /* normalize4 fused with rotation_unit of its unit output:
+                                 head = r[N], body = unit[N,4], sq slot = R[N,3,3]       */
 } fn_op;
 
 typedef enum { FN_F32 = 0, FN_F64 = 1 } fn_dtype;
@@ -83,6 +90,10 @@ int fn_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, voi
            void* sq, const double* ka, void* stream);
 int fn_host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head,
                 void* body, void* sq, const double* ka);
+/* fn_run for the rotation ops, with a device counter (uint64, accumulated; may be NULL)
+ * of rows the reference would reject. */
+int fn_run_rot(int op, const double* q, int64_t n, double* head, double* body, double* extra,
+               const double* ka, uint64_t* invalid, void* stream);
 
 /* ---- named entry points: one per reference export --------------------------------- */
 /* scale{n}_{f64,f32}      replaces _kernels.pyx:419-439 / :523-546 */
@@ -151,6 +162,12 @@ int fn_row_stats(int dim, int dtype, const void* x, int64_t n, uint64_t* counts,
  * data.  dim/dtype must match the config (1: 3/f64, 2: 2/f64, 3: 4/f64, 4: 3/f32,
  * 5: 3/f64). */
 int fn_generate(int cfg, uint64_t seed, int64_t row0, int64_t n, void* x, void* stream);
+
+/* The reference harness's input regimes (pkg/src/fastnorm/bench.py:146-207):
+ * 0 normal, 1 subnormal, 2 huge, 3 mixed, 4 unit-ish; rows [row0, row0+n) of an
+ * [*, dim] array of dtype, a pure function of (regime, dim, dtype, seed, row). */
+int fn_generate_regime(int regime, int dim, int dtype, uint64_t seed, int64_t row0, int64_t n,
+                       void* x, void* stream);
 
 /* ---- device self-test of the shared-divisor division (fastnorm_math.cuh) ----------- */
 /* Compares the kernels' correctly-rounded division against the CUDA math library's

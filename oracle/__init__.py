@@ -75,6 +75,10 @@ def lib() -> ctypes.CDLL:
             L.orc_run.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
                                   ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
                                   ctypes.c_void_p, ctypes.c_void_p]
+            L.orc_rotation.restype = ctypes.c_int64
+            L.orc_rotation.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64,
+                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                       ctypes.c_void_p]
             L.orc_loop.restype = ctypes.c_double
             L.orc_loop.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
                                    ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p]
@@ -125,6 +129,28 @@ def run(op: int, x: np.ndarray, ka=None, threads: int = 1):
         for t in ts:
             t.join()
     return head, body, sq
+
+
+OP_ROT_UNIT, OP_ROT_GENERAL, OP_NORMALIZE_ROT = 7, 8, 9
+
+
+def rotation(op: int, q: np.ndarray, ka=None):
+    """Oracle rotations of float64 quaternions q[N, 4] (rotation.py:53-111).
+
+    Returns (R[N,3,3], invalid_count) for OP_ROT_UNIT / OP_ROT_GENERAL and
+    (r[N], unit[N,4], R[N,3,3], invalid_count) for OP_NORMALIZE_ROT."""
+    q = np.ascontiguousarray(q, dtype=np.float64)
+    n = q.shape[0]
+    karr, kptr = _ka_ptr(ka)
+    if op == OP_NORMALIZE_ROT:
+        r = np.empty(n)
+        u = np.empty((n, 4))
+        R = np.empty((n, 3, 3))
+        bad = lib().orc_rotation(op, q.ctypes.data, n, r.ctypes.data, u.ctypes.data, R.ctypes.data, kptr)
+        return r, u, R, int(bad)
+    R = np.empty((n, 3, 3))
+    bad = lib().orc_rotation(op, q.ctypes.data, n, R.ctypes.data, None, None, kptr)
+    return R, int(bad)
 
 
 def loop(algo: int, buf: np.ndarray, iters: int, mask: int, ka=None) -> float:

@@ -275,4 +275,68 @@ double orc_loop(int algo, int dim, int dtype, const void* buf, int64_t iters, in
     return loop_f(algo, dim, (const float*)buf, iters, mask, ka);
 }
 
+/*
+ * Rotations of quaternions (rotation.py:53-111), binary64, Python evaluation order.
+ * op 7 = rotation_unit (:87-111), 8 = rotation_general (:53-84, via _scale4 on the
+ * double kernel args), 9 = normalize4 then rotation_unit of the unit output.
+ * Returns the number of rows the reference would reject (ValueError); those rows get
+ * NaN matrices.  head = R[N*9] for 7/8; for 9: head = r[N], body = unit[N*4], R = sq.
+ */
+static int rot_unit(const double* q, double* R) {
+    int ok = isfinite(q[0]) && isfinite(q[1]) && isfinite(q[2]) && isfinite(q[3]);
+    double q1 = q[0], q2 = q[1], q3 = q[2], q4 = q[3];
+    R[0] = 1.0 - 2.0 * (q2 * q2 + q3 * q3);
+    R[1] = 2.0 * (q1 * q2 - q3 * q4);
+    R[2] = 2.0 * (q1 * q3 + q2 * q4);
+    R[3] = 2.0 * (q1 * q2 + q3 * q4);
+    R[4] = 1.0 - 2.0 * (q1 * q1 + q3 * q3);
+    R[5] = 2.0 * (q2 * q3 - q1 * q4);
+    R[6] = 2.0 * (q1 * q3 - q2 * q4);
+    R[7] = 2.0 * (q2 * q3 + q1 * q4);
+    R[8] = 1.0 - 2.0 * (q1 * q1 + q2 * q2);
+    if (!ok)
+        for (int k = 0; k < 9; ++k) R[k] = NAN;
+    return ok;
+}
+
+static int rot_general(const double* ka, const double* x, double* R) {
+    int ok = isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]) && isfinite(x[3]);
+    double inv, q[4];
+    scale4_d(ka, x[0], x[1], x[2], x[3], &inv, q);
+    ok = ok && inv != 0.0;
+    double q1 = q[0], q2 = q[1], q3 = q[2], q4 = q[3];
+    double ss = q1 * q1 + q2 * q2 + q3 * q3 + q4 * q4;
+    R[0] = (q1 * q1 + q4 * q4 - q2 * q2 - q3 * q3) / ss;
+    R[1] = 2.0 * (q1 * q2 - q3 * q4) / ss;
+    R[2] = 2.0 * (q1 * q3 + q2 * q4) / ss;
+    R[3] = 2.0 * (q1 * q2 + q3 * q4) / ss;
+    R[4] = (q2 * q2 + q4 * q4 - q1 * q1 - q3 * q3) / ss;
+    R[5] = 2.0 * (q2 * q3 - q1 * q4) / ss;
+    R[6] = 2.0 * (q1 * q3 - q2 * q4) / ss;
+    R[7] = 2.0 * (q2 * q3 + q1 * q4) / ss;
+    R[8] = (q3 * q3 + q4 * q4 - q1 * q1 - q2 * q2) / ss;
+    if (!ok)
+        for (int k = 0; k < 9; ++k) R[k] = NAN;
+    return ok;
+}
+
+int64_t orc_rotation(int op, const double* q, int64_t n, double* head, double* body, double* rot,
+                     const double* ka) {
+    int64_t bad = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        if (op == 7) {
+            bad += !rot_unit(q + 4 * i, head + 9 * i);
+        } else if (op == 8) {
+            bad += !rot_general(ka, q + 4 * i, head + 9 * i);
+        } else {
+            double r, u[4];
+            normalize_d(4, ka, q + 4 * i, &r, u, 0);
+            head[i] = r;
+            for (int k = 0; k < 4; ++k) body[4 * i + k] = u[k];
+            bad += !rot_unit(u, rot + 9 * i);
+        }
+    }
+    return bad;
+}
+
 const char* orc_build_flags(void) { return "gcc -O3 -ffp-contract=off"; }

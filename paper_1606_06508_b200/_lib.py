@@ -23,6 +23,9 @@ OP_NAIVE = 3
 OP_QUOTIENT = 4
 OP_QUOTIENT3_FAST = 5
 OP_NORMALIZE_SQ = 6
+OP_ROT_UNIT = 7
+OP_ROT_GENERAL = 8
+OP_NORMALIZE_ROT = 9
 F32 = 0
 F64 = 1
 
@@ -49,10 +52,14 @@ def _declare(L: ctypes.CDLL) -> None:
     L.fn_device_count.restype = _int
     L.fn_run.restype = _int
     L.fn_run.argtypes = [_int, _int, _int, _vp, _i64, _vp, _vp, _vp, _vp, _vp]
+    L.fn_run_rot.restype = _int
+    L.fn_run_rot.argtypes = [_int, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]
     L.fn_host_run.restype = _int
     L.fn_host_run.argtypes = [_int, _int, _int, _vp, _i64, _vp, _vp, _vp, _vp]
     L.fn_generate.restype = _int
     L.fn_generate.argtypes = [_int, ctypes.c_uint64, _i64, _i64, _vp, _vp]
+    L.fn_generate_regime.restype = _int
+    L.fn_generate_regime.argtypes = [_int, _int, _int, ctypes.c_uint64, _i64, _i64, _vp, _vp]
     L.fn_selftest_div.restype = _int
     L.fn_selftest_div.argtypes = [_int, ctypes.c_uint64, _i64, _vp, _vp]
     L.fn_row_stats.restype = _int

@@ -20,15 +20,21 @@ import numpy as np
 
 from paper_1606_06508_b200 import _lib
 
-_HAS_BODY = {
-    _lib.OP_SCALE: True,
-    _lib.OP_NORMALIZE: True,
-    _lib.OP_NORMALIZE_SQ: True,
-    _lib.OP_NORM: False,
-    _lib.OP_NAIVE: True,
-    _lib.OP_QUOTIENT: True,
-    _lib.OP_QUOTIENT3_FAST: True,
-}
+def widths(op: int, dim: int) -> tuple[int, int, int]:
+    """Elements per row of the (head, body, extra) outputs of a kernel family."""
+    if op == _lib.OP_NORM:
+        return 1, 0, 0
+    if op == _lib.OP_NORMALIZE_SQ:
+        return 1, dim, 1
+    if op in (_lib.OP_ROT_UNIT, _lib.OP_ROT_GENERAL):
+        return 9, 0, 0
+    if op == _lib.OP_NORMALIZE_ROT:
+        return 1, 4, 9
+    return 1, dim, 0
+
+
+def _shape(n: int, w: int) -> tuple[int, ...]:
+    return (n,) if w == 1 else ((n, 3, 3) if w == 9 else (n, w))
 
 
 class BatchOut(NamedTuple):
@@ -81,40 +87,49 @@ def _check_out(o, shape, like, what):
     return o
 
 
-def run(op: int, dim: int, x, ka_arr: np.ndarray | None, out=None) -> BatchOut:
-    """Run kernel family ``op`` over rows ``x[N, dim]``; return (head, body, sq)."""
+def run(op: int, dim: int, x, ka_arr: np.ndarray | None, out=None, invalid=None) -> BatchOut:
+    """Run kernel family ``op`` over rows ``x[N, dim]``; return (head, body, extra).
+
+    ``invalid`` (device path, rotations): a CUDA int64 tensor the kernel adds the number
+    of rejected rows to."""
     if x.ndim != 2 or x.shape[1] != dim:
         raise ValueError(f"expected rows of shape [N, {dim}], got {tuple(x.shape)}")
-    has_body = _HAS_BODY[op]
-    has_sq = op == _lib.OP_NORMALIZE_SQ
+    w0, w1, w2 = widths(op, dim)
     n = int(x.shape[0])
     L = _lib.lib()
     kptr = None if ka_arr is None else ka_arr.ctypes.data
     outs = tuple(out) if out is not None else ()
-    want = 1 + int(has_body) + int(has_sq)
+    want = 1 + int(w1 > 0) + int(w2 > 0)
     if out is not None and len(outs) != want:
         raise ValueError(f"out must hold {want} arrays")
+    o_head = outs[0] if outs else None
+    o_body = outs[1] if outs and w1 else None
+    o_extra = outs[-1] if outs and w2 else None
 
     if is_torch(x):
         torch = _torch()
         dcode = _dtype_code(str(x.dtype).replace("torch.", ""))
         if x.is_cuda:
             x = x.contiguous()
-            head = _check_out(outs[0] if outs else None, (n,), x, "head")
-            body = _check_out(outs[1] if outs and has_body else None, (n, dim), x, "body")
-            sq = _check_out(outs[-1] if outs and has_sq else None, (n,), x, "sq")
-            head = head if head is not None else torch.empty((n,), dtype=x.dtype, device=x.device)
-            if has_body and body is None:
-                body = torch.empty((n, dim), dtype=x.dtype, device=x.device)
-            if has_sq and sq is None:
-                sq = torch.empty((n,), dtype=x.dtype, device=x.device)
+
+            def alloc(o, w, what):
+                if not w:
+                    return None
+                o = _check_out(o, _shape(n, w), x, what)
+                return o if o is not None else torch.empty(_shape(n, w), dtype=x.dtype, device=x.device)
+
+            head, body, extra = alloc(o_head, w0, "head"), alloc(o_body, w1, "body"), alloc(o_extra, w2, "extra")
+            ptr = (lambda t: None if t is None else t.data_ptr())
             with torch.cuda.device(x.device):
                 stream = torch.cuda.current_stream(x.device).cuda_stream
-                rc = L.fn_run(op, dim, dcode, x.data_ptr(), n, head.data_ptr(),
-                              body.data_ptr() if has_body else None,
-                              sq.data_ptr() if has_sq else None, kptr, stream)
+                if op in (_lib.OP_ROT_UNIT, _lib.OP_ROT_GENERAL, _lib.OP_NORMALIZE_ROT):
+                    rc = L.fn_run_rot(op, x.data_ptr(), n, ptr(head), ptr(body), ptr(extra), kptr,
+                                      ptr(invalid), stream)
+                else:
+                    rc = L.fn_run(op, dim, dcode, x.data_ptr(), n, ptr(head), ptr(body), ptr(extra),
+                                  kptr, stream)
             _lib.check(rc, "fn_run")
-            return BatchOut(head, body if has_body else None, sq if has_sq else None)
+            return BatchOut(head, body, extra)
         # CPU tensor: host path, results as CPU tensors sharing the numpy buffers
         res = run(op, dim, x.contiguous().numpy(), ka_arr,
                   None if out is None else tuple(o.numpy() for o in outs))
@@ -125,16 +140,15 @@ def run(op: int, dim: int, x, ka_arr: np.ndarray | None, out=None) -> BatchOut:
         raise TypeError(f"rows must be a numpy array or torch tensor, got {type(x).__name__}")
     dcode = _dtype_code(str(x.dtype))
     x = np.ascontiguousarray(x)
-    head = _check_out(outs[0] if outs else None, (n,), x, "head")
-    body = _check_out(outs[1] if outs and has_body else None, (n, dim), x, "body")
-    sq = _check_out(outs[-1] if outs and has_sq else None, (n,), x, "sq")
-    head = head if head is not None else np.empty((n,), dtype=x.dtype)
-    if has_body and body is None:
-        body = np.empty((n, dim), dtype=x.dtype)
-    if has_sq and sq is None:
-        sq = np.empty((n,), dtype=x.dtype)
-    rc = L.fn_host_run(op, dim, dcode, x.ctypes.data, n, head.ctypes.data,
-                       body.ctypes.data if has_body else None,
-                       sq.ctypes.data if has_sq else None, kptr)
+
+    def alloc_np(o, w, what):
+        if not w:
+            return None
+        o = _check_out(o, _shape(n, w), x, what)
+        return o if o is not None else np.empty(_shape(n, w), dtype=x.dtype)
+
+    head, body, extra = alloc_np(o_head, w0, "head"), alloc_np(o_body, w1, "body"), alloc_np(o_extra, w2, "extra")
+    ptr = (lambda a: None if a is None else a.ctypes.data)
+    rc = L.fn_host_run(op, dim, dcode, x.ctypes.data, n, ptr(head), ptr(body), ptr(extra), kptr)
     _lib.check(rc, "fn_host_run")
-    return BatchOut(head, body if has_body else None, sq if has_sq else None)
+    return BatchOut(head, body, extra)

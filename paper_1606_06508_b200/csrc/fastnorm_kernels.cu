@@ -60,15 +60,33 @@ static int device_sms(int dev) {
     return g_dev[dev].sms;
 }
 
+// Output record widths (elements per row) of the three output arrays of an op.
+struct Widths {
+    int w0, w1, w2;
+};
+static Widths op_widths(int op, int dim) {
+    switch (op) {
+        case FN_OP_NORM: return {1, 0, 0};
+        case FN_OP_NORMALIZE_SQ: return {1, dim, 1};
+        case FN_OP_ROT_UNIT:
+        case FN_OP_ROT_GENERAL: return {9, 0, 0};
+        case FN_OP_NORMALIZE_ROT: return {1, 4, 9};
+        default: return {1, dim, 0};
+    }
+}
+static bool is_rotation(int op) {
+    return op == FN_OP_ROT_UNIT || op == FN_OP_ROT_GENERAL || op == FN_OP_NORMALIZE_ROT;
+}
+
 // Per-instantiation occupancy (computed once per process and device).
 template <typename T, int N, int OP> struct TmaLaunch {
+    using L = TileLayout<T, N, OP, OpRows<T, N, OP>::value, Tile<T, N>::kStages>;
     static int blocks_per_sm(int dev) {
         static std::mutex mu;
         static int cache[64] = {0};
         std::lock_guard<std::mutex> lk(mu);
         if (dev < 0 || dev >= 64) return 1;
         if (cache[dev] == 0) {
-            using L = TileLayout<T, N, OP, Tile<T, N>::kRows, Tile<T, N>::kStages>;
             auto kern = tma_stream_kernel<T, N, OP>;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemBytes);
             int nb = 0;
@@ -97,30 +115,31 @@ static bool force_direct() {
 template <typename T, int N, int OP>
 static int launch(const void* xv, int64_t n, void* hv, void* bv, void* qv, const KArgs<T>& ka,
                   cudaStream_t stream) {
-    using L = TileLayout<T, N, OP, Tile<T, N>::kRows, Tile<T, N>::kStages>;
+    using TL = TmaLaunch<T, N, OP>;
+    using L = typename TL::L;
+    using Op = typename L::Op;
     const T* x = static_cast<const T*>(xv);
     T* head = static_cast<T*>(hv);
     T* body = static_cast<T*>(bv);
-    T* sq = static_cast<T*>(qv);
+    T* extra = static_cast<T*>(qv);
     if (n == 0) return FN_OK;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
     const int sms = device_sms(dev);
-    const bool aligned = aligned16(x) && aligned16(head) && (!L::Op::kBody || aligned16(body)) &&
-                         (!L::Op::kSq || aligned16(sq));
+    const bool aligned = aligned16(x) && aligned16(head) && (Op::W1 == 0 || aligned16(body)) &&
+                         (Op::W2 == 0 || aligned16(extra));
     if (aligned && !force_direct() && n >= (int64_t)L::TR) {
         const int64_t ntiles = n / L::TR;
-        const int64_t per_sm =
-            std::min<int64_t>(TmaLaunch<T, N, OP>::blocks_per_sm(dev), CtasPerSm<OP>::value);
+        const int64_t per_sm = std::min<int64_t>(TL::blocks_per_sm(dev), CtasPerSm<OP>::value);
         const int64_t resident = per_sm * sms;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, resident));
         tma_stream_kernel<T, N, OP>
-            <<<grid, Tile<T, N>::kThreads, L::kSmemBytes, stream>>>(x, n, head, body, sq, ka);
+            <<<grid, Tile<T, N>::kThreads, L::kSmemBytes, stream>>>(x, n, head, body, extra, ka);
     } else {
         const int64_t want = (n + 255) / 256;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 8));
-        direct_kernel<T, N, OP><<<grid, 256, 0, stream>>>(x, n, head, body, sq, ka);
+        direct_kernel<T, N, OP><<<grid, 256, 0, stream>>>(x, n, head, body, extra, ka);
     }
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
@@ -159,14 +178,18 @@ static int dispatch_dim(int dim, const void* x, int64_t n, void* h, void* b, voi
     }
 }
 
+static bool needs_ka(int op) {
+    return op == FN_OP_SCALE || op == FN_OP_NORMALIZE || op == FN_OP_NORM ||
+           op == FN_OP_NORMALIZE_SQ || op == FN_OP_ROT_GENERAL || op == FN_OP_NORMALIZE_ROT;
+}
+
 template <typename T>
 static int dispatch(int op, int dim, const void* x, int64_t n, void* h, void* b, void* q,
-                    const double* kad, cudaStream_t s) {
-    const bool scaling = op == FN_OP_SCALE || op == FN_OP_NORMALIZE || op == FN_OP_NORM ||
-                         op == FN_OP_NORMALIZE_SQ;
+                    const double* kad, unsigned long long* invalid, cudaStream_t s) {
     KArgs<T> ka;
-    int rc = make_kargs<T>(kad, scaling, ka);
+    int rc = make_kargs<T>(kad, needs_ka(op), ka);
     if (rc != FN_OK) return rc;
+    ka.invalid = invalid;
     switch (op) {
         case FN_OP_SCALE: return dispatch_dim<T, FN_OP_SCALE>(dim, x, n, h, b, q, ka, s);
         case FN_OP_NORMALIZE: return dispatch_dim<T, FN_OP_NORMALIZE>(dim, x, n, h, b, q, ka, s);
@@ -182,30 +205,54 @@ static int dispatch(int op, int dim, const void* x, int64_t n, void* h, void* b,
     }
 }
 
+// Rotations: quaternions in binary64 only (the reference computes them in Python floats).
+static int dispatch_rot(int op, const void* x, int64_t n, void* h, void* b, void* q,
+                        const double* kad, unsigned long long* invalid, cudaStream_t s) {
+    KArgs<double> ka;
+    int rc = make_kargs<double>(kad, needs_ka(op), ka);
+    if (rc != FN_OK) return rc;
+    ka.invalid = invalid;
+    switch (op) {
+        case FN_OP_ROT_UNIT: return launch<double, 4, FN_OP_ROT_UNIT>(x, n, h, b, q, ka, s);
+        case FN_OP_ROT_GENERAL: return launch<double, 4, FN_OP_ROT_GENERAL>(x, n, h, b, q, ka, s);
+        case FN_OP_NORMALIZE_ROT: return launch<double, 4, FN_OP_NORMALIZE_ROT>(x, n, h, b, q, ka, s);
+        default: return fail(FN_EINVAL, "unknown rotation op");
+    }
+}
+
 int check_args(int op, int dim, int dtype, const void* x, int64_t n, const void* head,
                const void* body, const void* sq) {
-    if (op < FN_OP_SCALE || op > FN_OP_NORMALIZE_SQ) return fail(FN_EINVAL, "unknown op");
+    if (op < FN_OP_SCALE || op > FN_OP_NORMALIZE_ROT) return fail(FN_EINVAL, "unknown op");
     if (dim < 2 || dim > 4) return fail(FN_EINVAL, "dim must be 2, 3 or 4");
     if (dtype != FN_F32 && dtype != FN_F64) return fail(FN_EINVAL, "dtype must be FN_F32/FN_F64");
+    if (is_rotation(op) && (dim != 4 || dtype != FN_F64))
+        return fail(FN_EINVAL, "rotations take float64 quaternions (dim 4, FN_F64)");
     if (n < 0) return fail(FN_EINVAL, "n must be >= 0");
     if (n == 0) return FN_OK;
+    const Widths w = op_widths(op, dim);
     if (!x || !head) return fail(FN_EINVAL, "x and head must not be NULL");
-    if (op == FN_OP_NORM) {
-        if (body) return fail(FN_EINVAL, "norm has no body output; pass NULL");
+    if (w.w1 == 0) {
+        if (body) return fail(FN_EINVAL, "this op has no body output; pass NULL");
     } else if (!body) {
         return fail(FN_EINVAL, "body output must not be NULL");
     }
-    if (op == FN_OP_NORMALIZE_SQ && !sq) return fail(FN_EINVAL, "sq must not be NULL");
+    if (w.w2 > 0 && !sq) return fail(FN_EINVAL, "sq/extra output must not be NULL");
     return FN_OK;
+}
+
+int run_ex(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* body, void* sq,
+           const double* ka, unsigned long long* invalid, void* stream) {
+    int rc = check_args(op, dim, dtype, x, n, head, body, sq);
+    if (rc != FN_OK || n == 0) return rc;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (is_rotation(op)) return dispatch_rot(op, x, n, head, body, sq, ka, invalid, s);
+    if (dtype == FN_F64) return dispatch<double>(op, dim, x, n, head, body, sq, ka, invalid, s);
+    return dispatch<float>(op, dim, x, n, head, body, sq, ka, invalid, s);
 }
 
 int run(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* body, void* sq,
         const double* ka, void* stream) {
-    int rc = check_args(op, dim, dtype, x, n, head, body, sq);
-    if (rc != FN_OK || n == 0) return rc;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (dtype == FN_F64) return dispatch<double>(op, dim, x, n, head, body, sq, ka, s);
-    return dispatch<float>(op, dim, x, n, head, body, sq, ka, s);
+    return run_ex(op, dim, dtype, x, n, head, body, sq, ka, nullptr, stream);
 }
 
 // ---------------------------------------------------------------------------------
@@ -261,17 +308,15 @@ int host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, v
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
     const size_t w = dtype == FN_F64 ? 8 : 4;
-    const bool has_body = op != FN_OP_NORM;
-    const bool has_sq = op == FN_OP_NORMALIZE_SQ;
-    // ~48 MiB of input per chunk keeps three chunks in flight well inside L2-independent
-    // streaming while amortising the per-copy latency.
+    const Widths wd = op_widths(op, dim);
+    // ~48 MiB of input per chunk: three chunks in flight, per-copy latency amortised.
     const int64_t chunk_rows = std::max<int64_t>(4096, ((int64_t)48 << 20) / (int64_t)(dim * w));
     const int64_t rows = std::min<int64_t>(n, chunk_rows);
-    const size_t bx = align256(rows * dim * w), bh = align256(rows * w),
-                 bb = has_body ? align256(rows * dim * w) : 0, bq = has_sq ? align256(rows * w) : 0;
+    const size_t bx = align256(rows * dim * w), b0 = align256(rows * wd.w0 * w),
+                 b1 = align256(rows * wd.w1 * w), b2 = align256(rows * wd.w2 * w);
     std::lock_guard<std::mutex> lk(g_stage_mu);
     Staging* st = nullptr;
-    rc = staging_get(dev, bx + bh + bb + bq, &st);
+    rc = staging_get(dev, bx + b0 + b1 + b2, &st);
     if (rc != FN_OK) return rc;
     int64_t chunk = 0;
     for (int64_t r0 = 0; r0 < n; r0 += rows, ++chunk) {
@@ -280,20 +325,22 @@ int host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, v
         cudaStream_t s = st->streams[p];
         char* base = static_cast<char*>(st->buf[p]);
         void* dx = base;
-        void* dh = base + bx;
-        void* db = has_body ? base + bx + bh : nullptr;
-        void* dq = has_sq ? base + bx + bh + bb : nullptr;
+        void* d0 = base + bx;
+        void* d1 = wd.w1 ? base + bx + b0 : nullptr;
+        void* d2 = wd.w2 ? base + bx + b0 + b1 : nullptr;
         e = cudaMemcpyAsync(dx, static_cast<const char*>(x) + r0 * dim * w, m * dim * w,
                             cudaMemcpyHostToDevice, s);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync H2D");
-        rc = run(op, dim, dtype, dx, m, dh, db, dq, ka, s);
+        rc = run(op, dim, dtype, dx, m, d0, d1, d2, ka, s);
         if (rc != FN_OK) return rc;
-        e = cudaMemcpyAsync(static_cast<char*>(head) + r0 * w, dh, m * w, cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess && has_body)
-            e = cudaMemcpyAsync(static_cast<char*>(body) + r0 * dim * w, db, m * dim * w,
+        e = cudaMemcpyAsync(static_cast<char*>(head) + r0 * wd.w0 * w, d0, m * wd.w0 * w,
+                            cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess && wd.w1)
+            e = cudaMemcpyAsync(static_cast<char*>(body) + r0 * wd.w1 * w, d1, m * wd.w1 * w,
                                 cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess && has_sq)
-            e = cudaMemcpyAsync(static_cast<char*>(sq) + r0 * w, dq, m * w, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess && wd.w2)
+            e = cudaMemcpyAsync(static_cast<char*>(sq) + r0 * wd.w2 * w, d2, m * wd.w2 * w,
+                                cudaMemcpyDeviceToHost, s);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync D2H");
     }
     for (int p = 0; p < Staging::kPipes; ++p) {
@@ -329,6 +376,14 @@ int fn_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, voi
 int fn_host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* body,
                 void* sq, const double* ka) {
     return fnb::host_run(op, dim, dtype, x, n, head, body, sq, ka);
+}
+
+int fn_run_rot(int op, const double* q, int64_t n, double* head, double* body, double* extra,
+               const double* ka, uint64_t* invalid, void* stream) {
+    if (op != FN_OP_ROT_UNIT && op != FN_OP_ROT_GENERAL && op != FN_OP_NORMALIZE_ROT)
+        return fnb::set_error(FN_EINVAL, "fn_run_rot takes a rotation op");
+    return fnb::run_ex(op, 4, FN_F64, q, n, head, body, extra, ka,
+                       reinterpret_cast<unsigned long long*>(invalid), stream);
 }
 
 #define FNB_DEF_SCALING(base, OP)                                                              \

@@ -69,6 +69,7 @@ template <> struct Fp<float> {
 template <typename T> struct KArgs {
     T tau_min, tau_max, sigma_min, sigma_max, inv_min, inv_max;
     typename Fp<T>::Bits tau_min_bits, tau_max_bits;
+    unsigned long long* invalid;  // rows rejected by the rotations (may be NULL)
 };
 
 // ---------------------------------------------------------------------------------
@@ -400,6 +401,67 @@ __device__ __forceinline__ void quotient3_fast_row(const T (&x)[3], T& r, T (&u)
     if (zero) {
         r = T(0); u[0] = T(0); u[1] = T(0); u[2] = T(0);
     }
+}
+
+// ---------------------------------------------------------------------------------
+// Rotation matrices of quaternions (rotation.py:53-111), q = (q1, q2, q3, q4) with q4 the
+// scalar part, R row-major.  Python evaluation order, one rounding per operation.  The
+// reference raises ValueError for a non-finite quaternion (both forms, :44-50) and for
+// the zero quaternion (general form, :63-64); the batched form writes NaN for such a row
+// and reports it (return false) so the caller can raise.
+// ---------------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ bool rotation_unit_row(const T (&q)[4], T* R) {
+    using F = Fp<T>;
+    const bool ok = isfinite(q[0]) && isfinite(q[1]) && isfinite(q[2]) && isfinite(q[3]);
+    const T q1 = q[0], q2 = q[1], q3 = q[2], q4 = q[3];
+    const T two = T(2);
+    auto sub = [](T a, T b) { return F::add(a, -b); };
+    R[0] = sub(T(1), F::mul(two, F::add(F::mul(q2, q2), F::mul(q3, q3))));
+    R[1] = F::mul(two, sub(F::mul(q1, q2), F::mul(q3, q4)));
+    R[2] = F::mul(two, F::add(F::mul(q1, q3), F::mul(q2, q4)));
+    R[3] = F::mul(two, F::add(F::mul(q1, q2), F::mul(q3, q4)));
+    R[4] = sub(T(1), F::mul(two, F::add(F::mul(q1, q1), F::mul(q3, q3))));
+    R[5] = F::mul(two, sub(F::mul(q2, q3), F::mul(q1, q4)));
+    R[6] = F::mul(two, sub(F::mul(q1, q3), F::mul(q2, q4)));
+    R[7] = F::mul(two, F::add(F::mul(q2, q3), F::mul(q1, q4)));
+    R[8] = sub(T(1), F::mul(two, F::add(F::mul(q1, q1), F::mul(q2, q2))));
+    if (!ok) {
+#pragma unroll
+        for (int k = 0; k < 9; ++k) R[k] = T(NAN);
+    }
+    return ok;
+}
+
+// rotation_general: scale4 (exact cascade, :61-62), ss = ((q1^2+q2^2)+q3^2)+q4^2 on the
+// scaled components, every entry divided by ss (:66-84).
+template <typename T>
+__device__ __forceinline__ bool rotation_general_row(const T (&x)[4], const KArgs<T>& ka, T* R) {
+    using F = Fp<T>;
+    bool ok = isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]) && isfinite(x[3]);
+    T inv, q[4];
+    scale_row(x, ka, inv, q);
+    ok = ok && inv != T(0);
+    const T q1 = q[0], q2 = q[1], q3 = q[2], q4 = q[3];
+    const T a11 = F::mul(q1, q1), a22 = F::mul(q2, q2), a33 = F::mul(q3, q3), a44 = F::mul(q4, q4);
+    const T ss = F::add(F::add(F::add(a11, a22), a33), a44);
+    const T two = T(2);
+    auto sub = [](T a, T b) { return F::add(a, -b); };
+    const Divider<T> by_ss(ss);
+    R[0] = by_ss(sub(sub(F::add(a11, a44), a22), a33));
+    R[1] = by_ss(F::mul(two, sub(F::mul(q1, q2), F::mul(q3, q4))));
+    R[2] = by_ss(F::mul(two, F::add(F::mul(q1, q3), F::mul(q2, q4))));
+    R[3] = by_ss(F::mul(two, F::add(F::mul(q1, q2), F::mul(q3, q4))));
+    R[4] = by_ss(sub(sub(F::add(a22, a44), a11), a33));
+    R[5] = by_ss(F::mul(two, sub(F::mul(q2, q3), F::mul(q1, q4))));
+    R[6] = by_ss(F::mul(two, sub(F::mul(q1, q3), F::mul(q2, q4))));
+    R[7] = by_ss(F::mul(two, F::add(F::mul(q2, q3), F::mul(q1, q4))));
+    R[8] = by_ss(sub(sub(F::add(a33, a44), a11), a22));
+    if (!ok) {
+#pragma unroll
+        for (int k = 0; k < 9; ++k) R[k] = T(NAN);
+    }
+    return ok;
 }
 
 }  // namespace fnb

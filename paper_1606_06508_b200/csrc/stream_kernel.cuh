@@ -26,86 +26,131 @@
 namespace fnb {
 
 // ---------------------------------------------------------------------------------
-// Row operations: one functor per kernel family.
+// Row operations: one functor per kernel family.  Each row of N inputs produces up to
+// three output records of W0 / W1 / W2 elements (written to three arrays: "head",
+// "body", "extra"); apply() returns false for a row the reference would reject with
+// an exception (rotations only), which the kernel counts.
 // ---------------------------------------------------------------------------------
 template <typename T, int N, int OP> struct RowOp;
 
 template <typename T, int N> struct RowOp<T, N, FN_OP_NORMALIZE> {
-    static constexpr bool kBody = true, kSq = false;
-    __device__ __forceinline__ static void apply(const T (&x)[N], const KArgs<T>& ka, T& head,
-                                                 T (&body)[N], T& sq) {
-        normalize_row<T, N, false>(x, ka, head, body, sq);
+    static constexpr int W0 = 1, W1 = N, W2 = 0;
+    __device__ __forceinline__ static bool apply(const T (&x)[N], const KArgs<T>& ka, T* o0, T* o1, T*) {
+        T sq;
+        normalize_row<T, N, false>(x, ka, o0[0], *reinterpret_cast<T(*)[N]>(o1), sq);
+        return true;
     }
 };
 template <typename T, int N> struct RowOp<T, N, FN_OP_NORMALIZE_SQ> {
-    static constexpr bool kBody = true, kSq = true;
-    __device__ __forceinline__ static void apply(const T (&x)[N], const KArgs<T>& ka, T& head,
-                                                 T (&body)[N], T& sq) {
-        normalize_row<T, N, true>(x, ka, head, body, sq);
+    static constexpr int W0 = 1, W1 = N, W2 = 1;
+    __device__ __forceinline__ static bool apply(const T (&x)[N], const KArgs<T>& ka, T* o0, T* o1, T* o2) {
+        normalize_row<T, N, true>(x, ka, o0[0], *reinterpret_cast<T(*)[N]>(o1), o2[0]);
+        return true;
     }
 };
 template <typename T, int N> struct RowOp<T, N, FN_OP_NORM> {
-    static constexpr bool kBody = false, kSq = false;
-    __device__ __forceinline__ static void apply(const T (&x)[N], const KArgs<T>& ka, T& head,
-                                                 T (&)[N], T&) {
-        head = norm_row<T, N>(x, ka);
+    static constexpr int W0 = 1, W1 = 0, W2 = 0;
+    __device__ __forceinline__ static bool apply(const T (&x)[N], const KArgs<T>& ka, T* o0, T*, T*) {
+        o0[0] = norm_row<T, N>(x, ka);
+        return true;
     }
 };
 template <typename T, int N> struct RowOp<T, N, FN_OP_SCALE> {
-    static constexpr bool kBody = true, kSq = false;
-    __device__ __forceinline__ static void apply(const T (&x)[N], const KArgs<T>& ka, T& head,
-                                                 T (&body)[N], T&) {
-        scale_row(x, ka, head, body);
+    static constexpr int W0 = 1, W1 = N, W2 = 0;
+    __device__ __forceinline__ static bool apply(const T (&x)[N], const KArgs<T>& ka, T* o0, T* o1, T*) {
+        scale_row(x, ka, o0[0], *reinterpret_cast<T(*)[N]>(o1));
+        return true;
     }
 };
 template <typename T, int N> struct RowOp<T, N, FN_OP_NAIVE> {
-    static constexpr bool kBody = true, kSq = false;
-    __device__ __forceinline__ static void apply(const T (&x)[N], const KArgs<T>&, T& head,
-                                                 T (&body)[N], T&) {
-        naive_row<T, N>(x, head, body);
+    static constexpr int W0 = 1, W1 = N, W2 = 0;
+    __device__ __forceinline__ static bool apply(const T (&x)[N], const KArgs<T>&, T* o0, T* o1, T*) {
+        naive_row<T, N>(x, o0[0], *reinterpret_cast<T(*)[N]>(o1));
+        return true;
     }
 };
 template <typename T, int N> struct RowOp<T, N, FN_OP_QUOTIENT> {
-    static constexpr bool kBody = true, kSq = false;
-    __device__ __forceinline__ static void apply(const T (&x)[N], const KArgs<T>&, T& head,
-                                                 T (&body)[N], T&) {
-        quotient_row<T, N>(x, head, body);
+    static constexpr int W0 = 1, W1 = N, W2 = 0;
+    __device__ __forceinline__ static bool apply(const T (&x)[N], const KArgs<T>&, T* o0, T* o1, T*) {
+        quotient_row<T, N>(x, o0[0], *reinterpret_cast<T(*)[N]>(o1));
+        return true;
     }
 };
 template <typename T, int N> struct RowOp<T, N, FN_OP_QUOTIENT3_FAST> {
     static_assert(N == 3, "quotient3_fast is 3-D only (_backend.py:96-98)");
-    static constexpr bool kBody = true, kSq = false;
-    __device__ __forceinline__ static void apply(const T (&x)[N], const KArgs<T>&, T& head,
-                                                 T (&body)[N], T&) {
-        quotient3_fast_row<T>(x, head, body);
+    static constexpr int W0 = 1, W1 = N, W2 = 0;
+    __device__ __forceinline__ static bool apply(const T (&x)[N], const KArgs<T>&, T* o0, T* o1, T*) {
+        quotient3_fast_row<T>(x, o0[0], *reinterpret_cast<T(*)[N]>(o1));
+        return true;
+    }
+};
+// Rotations (rotation.py:53-111; binary64 quaternions only): R is a row-major 3x3.
+template <typename T, int N> struct RowOp<T, N, FN_OP_ROT_UNIT> {
+    static_assert(N == 4, "rotations take quaternions");
+    static constexpr int W0 = 9, W1 = 0, W2 = 0;
+    __device__ __forceinline__ static bool apply(const T (&x)[N], const KArgs<T>&, T* o0, T*, T*) {
+        return rotation_unit_row(x, o0);
+    }
+};
+template <typename T, int N> struct RowOp<T, N, FN_OP_ROT_GENERAL> {
+    static_assert(N == 4, "rotations take quaternions");
+    static constexpr int W0 = 9, W1 = 0, W2 = 0;
+    __device__ __forceinline__ static bool apply(const T (&x)[N], const KArgs<T>& ka, T* o0, T*, T*) {
+        return rotation_general_row(x, ka, o0);
+    }
+};
+// normalize4 fused with rotation_unit of its unit output: r, unit, R in one pass.
+template <typename T, int N> struct RowOp<T, N, FN_OP_NORMALIZE_ROT> {
+    static_assert(N == 4, "rotations take quaternions");
+    static constexpr int W0 = 1, W1 = 4, W2 = 9;
+    __device__ __forceinline__ static bool apply(const T (&x)[N], const KArgs<T>& ka, T* o0, T* o1, T* o2) {
+        T sq;
+        T(&u)[4] = *reinterpret_cast<T(*)[4]>(o1);
+        normalize_row<T, 4, false>(x, ka, o0[0], u, sq);
+        return rotation_unit_row(u, o2);
     }
 };
 
+template <int W> struct Slot { static constexpr int value = W > 0 ? W : 1; };
+
 // One row through global memory (tails, unaligned arrays, tiny batches).
 template <typename T, int N, int OP>
-__device__ __forceinline__ void row_global(const T* __restrict__ x, int64_t i, T* __restrict__ head,
-                                           T* __restrict__ body, T* __restrict__ sq,
+__device__ __forceinline__ bool row_global(const T* __restrict__ x, int64_t i, T* __restrict__ head,
+                                           T* __restrict__ body, T* __restrict__ extra,
                                            const KArgs<T>& ka) {
     using Op = RowOp<T, N, OP>;
-    T xr[N], b[N], h, q;
+    T xr[N], o0[Slot<Op::W0>::value], o1[Slot<Op::W1>::value], o2[Slot<Op::W2>::value];
 #pragma unroll
     for (int c = 0; c < N; ++c) xr[c] = __ldg(x + i * N + c);
-    Op::apply(xr, ka, h, b, q);
-    head[i] = h;
-    if (Op::kBody) {
+    const bool ok = Op::apply(xr, ka, o0, o1, o2);
 #pragma unroll
-        for (int c = 0; c < N; ++c) body[i * N + c] = b[c];
-    }
-    if (Op::kSq) sq[i] = q;
+    for (int c = 0; c < Op::W0; ++c) head[i * Op::W0 + c] = o0[c];
+#pragma unroll
+    for (int c = 0; c < Op::W1; ++c) body[i * Op::W1 + c] = o1[c];
+#pragma unroll
+    for (int c = 0; c < Op::W2; ++c) extra[i * Op::W2 + c] = o2[c];
+    return ok;
+}
+
+// Per-thread count of rejected rows -> one atomic per warp (rotations only).
+__device__ __forceinline__ void count_invalid(unsigned long long* counter, unsigned long long bad) {
+    if (counter == nullptr) return;
+    for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    if ((threadIdx.x & 31) == 0 && bad) atomicAdd(counter, bad);
 }
 
 template <typename T, int N, int OP>
 __global__ void __launch_bounds__(256) direct_kernel(const T* __restrict__ x, int64_t nrows,
                                                      T* __restrict__ head, T* __restrict__ body,
-                                                     T* __restrict__ sq, KArgs<T> ka) {
+                                                     T* __restrict__ extra, KArgs<T> ka) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nrows; i += stride)
-        row_global<T, N, OP>(x, i, head, body, sq, ka);
+    unsigned long long bad = 0;
+    const int64_t start = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t trips = nrows > start ? (nrows - 1 - start) / stride + 1 : 0;
+    // uniform trip count per warp so the shuffle-reduce below sees every lane
+    for (int64_t t = 0, i = start; t < trips; ++t, i += stride)
+        bad += row_global<T, N, OP>(x, i, head, body, extra, ka) ? 0 : 1;
+    count_invalid(ka.invalid, bad);
 }
 
 // ---------------------------------------------------------------------------------
@@ -216,24 +261,33 @@ template <typename T, int N, int OP, int TR_, int S_> struct TileLayout {
     static constexpr int S = S_;
     static constexpr int OB = 3;
     static constexpr int kInBytes = TR * N * (int)sizeof(T);
-    static constexpr int kHeadBytes = TR * (int)sizeof(T);
-    static constexpr int kBodyBytes = Op::kBody ? TR * N * (int)sizeof(T) : 0;
-    static constexpr int kSqBytes = Op::kSq ? TR * (int)sizeof(T) : 0;
-    static constexpr int kOutBytes = kHeadBytes + kBodyBytes + kSqBytes;
+    static constexpr int kB0 = TR * Op::W0 * (int)sizeof(T);
+    static constexpr int kB1 = TR * Op::W1 * (int)sizeof(T);
+    static constexpr int kB2 = TR * Op::W2 * (int)sizeof(T);
+    static constexpr int kOutBytes = kB0 + kB1 + kB2;
     static constexpr int kSmemBytes = S * kInBytes + OB * kOutBytes + S * 8;
-    static_assert(kInBytes % 16 == 0 && kHeadBytes % 16 == 0, "bulk copies need 16 B multiples");
+    static_assert(kInBytes % 16 == 0 && kB0 % 16 == 0 && kB1 % 16 == 0 && kB2 % 16 == 0,
+                  "bulk copies need 16 B multiples");
+};
+
+// Rows per tile for an op: the default, halved while the three output staging tiles
+// would exceed 64 KiB (rotations write 72-112 B per row).
+template <typename T, int N, int OP> struct OpRows {
+    static constexpr int kOutRow = (RowOp<T, N, OP>::W0 + RowOp<T, N, OP>::W1 + RowOp<T, N, OP>::W2) * (int)sizeof(T);
+    static constexpr int value = (3 * kOutRow * Tile<T, N>::kRows > 65536) ? Tile<T, N>::kRows / 2 : Tile<T, N>::kRows;
 };
 
 // HINTS: bit 0 -> input loads carry an L2 evict-first policy (read once);
 //        bit 1 -> output bulk stores carry an L2 evict-first policy.
-template <typename T, int N, int OP, int TR_ = Tile<T, N>::kRows, int S_ = Tile<T, N>::kStages,
+template <typename T, int N, int OP, int TR_ = OpRows<T, N, OP>::value, int S_ = Tile<T, N>::kStages,
           int NT = Tile<T, N>::kThreads, int HINTS = Tile<T, N>::kHints>
 __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x, int64_t nrows,
                                                         T* __restrict__ head, T* __restrict__ body,
-                                                        T* __restrict__ sq, KArgs<T> ka) {
+                                                        T* __restrict__ extra, KArgs<T> ka) {
     using L = TileLayout<T, N, OP, TR_, S_>;
     using Op = typename L::Op;
     constexpr int TR = L::TR, S = L::S, OB = L::OB;
+    constexpr int W0 = Op::W0, W1 = Op::W1, W2 = Op::W2;
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned char* s_in = smem;
     unsigned char* s_out = smem + S * L::kInBytes;
@@ -244,6 +298,7 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
         ntiles > (int64_t)blockIdx.x ? (ntiles - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
     const bool leader = threadIdx.x == 0;
     uint64_t policy = 0;
+    unsigned long long bad = 0;
 
     if (leader) {
         policy = policy_evict_first();
@@ -271,34 +326,34 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
         mbar_wait(&full[s], parity);
 
         const T* tin = reinterpret_cast<const T*>(s_in + s * L::kInBytes);
-        T* th = reinterpret_cast<T*>(s_out + ob * L::kOutBytes);
-        T* tb = th + TR;
-        T* tq = tb + (Op::kBody ? TR * N : 0);
+        T* t0 = reinterpret_cast<T*>(s_out + ob * L::kOutBytes);
+        T* t1 = t0 + TR * W0;
+        T* t2 = t1 + TR * W1;
 #pragma unroll
         for (int j = threadIdx.x; j < TR; j += NT) {
-            T xr[N], b[N], h, q;
+            T xr[N], o0[Slot<W0>::value], o1[Slot<W1>::value], o2[Slot<W2>::value];
 #pragma unroll
             for (int c = 0; c < N; ++c) xr[c] = tin[j * N + c];
-            Op::apply(xr, ka, h, b, q);
-            th[j] = h;
-            if (Op::kBody) {
+            bad += Op::apply(xr, ka, o0, o1, o2) ? 0 : 1;
 #pragma unroll
-                for (int c = 0; c < N; ++c) tb[j * N + c] = b[c];
-            }
-            if (Op::kSq) tq[j] = q;
+            for (int c = 0; c < W0; ++c) t0[j * W0 + c] = o0[c];
+#pragma unroll
+            for (int c = 0; c < W1; ++c) t1[j * W1 + c] = o1[c];
+#pragma unroll
+            for (int c = 0; c < W2; ++c) t2[j * W2 + c] = o2[c];
         }
         fence_proxy_async_smem();  // generic-proxy smem traffic -> visible to bulk copies
         __syncthreads();
         if (leader) {
             const int64_t row0 = tile * TR;
             if (HINTS & 2) {
-                bulk_store_hint(head + row0, th, L::kHeadBytes, policy);
-                if (Op::kBody) bulk_store_hint(body + row0 * N, tb, L::kBodyBytes, policy);
-                if (Op::kSq) bulk_store_hint(sq + row0, tq, L::kSqBytes, policy);
+                bulk_store_hint(head + row0 * W0, t0, L::kB0, policy);
+                if (W1) bulk_store_hint(body + row0 * W1, t1, L::kB1, policy);
+                if (W2) bulk_store_hint(extra + row0 * W2, t2, L::kB2, policy);
             } else {
-                bulk_store(head + row0, th, L::kHeadBytes);
-                if (Op::kBody) bulk_store(body + row0 * N, tb, L::kBodyBytes);
-                if (Op::kSq) bulk_store(sq + row0, tq, L::kSqBytes);
+                bulk_store(head + row0 * W0, t0, L::kB0);
+                if (W1) bulk_store(body + row0 * W1, t1, L::kB1);
+                if (W2) bulk_store(extra + row0 * W2, t2, L::kB2);
             }
             bulk_commit();
             if (k + S < my_tiles) {
@@ -314,11 +369,16 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
         }
     }
 
-    // Rows after the last full tile: plain per-thread path in the last CTA.
+    // Rows after the last full tile: plain per-thread path in the last CTA (the loop
+    // runs the same trip count on every lane of a warp so count_invalid can shuffle).
     if (blockIdx.x == gridDim.x - 1) {
-        for (int64_t i = ntiles * TR + threadIdx.x; i < nrows; i += NT)
-            row_global<T, N, OP>(x, i, head, body, sq, ka);
+        const int64_t tail = nrows - ntiles * TR;
+        for (int64_t j = threadIdx.x & ~31; j < tail; j += NT) {
+            const int64_t i = ntiles * TR + j + (threadIdx.x & 31);
+            if (i < nrows) bad += row_global<T, N, OP>(x, i, head, body, extra, ka) ? 0 : 1;
+        }
     }
+    count_invalid(ka.invalid, bad);
     if (leader) bulk_wait_all();
 }
 

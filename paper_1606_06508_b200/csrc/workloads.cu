@@ -143,6 +143,69 @@ __global__ void gen_cfg5(double* x, int64_t row0, int64_t n, uint64_t key) {
     }
 }
 
+// ---- the reference's input regimes (bench.py:146-207), counter-based ----------------
+// regime 0 normal    |x_k| in [tau_min, tau_max)        (1+m) 2^e, e ~ U[tmin, tmax)
+//        1 subnormal |x_k| in [alpha, nu)               e ~ U[sub_min, norm_min), capped
+//        2 huge      |x_k| > tau_max, sums finite        e ~ U[tmax+1, emax-1)
+//        3 mixed     full range incl. subnormals         e ~ U[sub_min, emax)
+//        4 unit-ish  norms within 2^-10 of one           normalised normals x (1 +- 2^-10 U)
+// computed in binary64 and rounded once to the row type (single: then capped like the
+// reference's clip of the subnormal regime).
+template <typename T, int DIM>
+__global__ void gen_regime(T* x, int64_t row0, int64_t n, uint64_t key, int regime, int tmin, int tmax,
+                           int sub_min, int norm_min, int emax, double nu_minus_alpha) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = row0 + i;
+        double v[DIM];
+        if (regime == 4) {
+            double g[4];
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                const double u1 = (double)((word(key, row, 2 * p) >> 11) + 1) * 0x1p-53;
+                const double u2 = (double)(word(key, row, 2 * p + 1) >> 11) * 0x1p-53;
+                const double rad = sqrt(-2.0 * log(u1));
+                double sn, cs;
+                sincospi(2.0 * u2, &sn, &cs);
+                g[2 * p] = rad * cs;
+                g[2 * p + 1] = rad * sn;
+            }
+            double ss = 0.0;
+#pragma unroll
+            for (int k = 0; k < DIM; ++k) ss = __dadd_rn(ss, __dmul_rn(g[k], g[k]));
+            double nrm = sqrt(ss);
+            if (nrm == 0.0) g[0] = 1.0;
+            nrm = fmax(nrm, 2.2250738585072014e-308);
+            const double u = (double)(word(key, row, 12) >> 11) * 0x1p-53;
+            const double stretch = 1.0 + (u * 2.0 - 1.0) * 0x1p-10;
+#pragma unroll
+            for (int k = 0; k < DIM; ++k) v[k] = (g[k] / nrm) * stretch;
+        } else {
+            int lo, span;
+            if (regime == 0) { lo = tmin; span = tmax - tmin; }
+            else if (regime == 1) { lo = sub_min; span = norm_min - sub_min; }
+            else if (regime == 2) { lo = tmax + 1; span = emax - 1 - (tmax + 1); }
+            else { lo = sub_min; span = emax - sub_min; }
+#pragma unroll
+            for (int k = 0; k < DIM; ++k) {
+                const uint64_t w = word(key, row, k);
+                double mag = ldexp(mant52(word(key, row, 4 + k)), uexp(w, lo, span));
+                if (regime == 1) mag = fmin(mag, nu_minus_alpha);
+                v[k] = sign_of(w) * mag;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < DIM; ++k) {
+            T out = (T)v[k];
+            if (sizeof(T) == 4 && regime == 1) {
+                const T cap = (T)nu_minus_alpha;
+                out = out > cap ? cap : (out < -cap ? -cap : out);
+            }
+            x[i * DIM + k] = out;
+        }
+    }
+}
+
 // ---- validation counters ------------------------------------------------------------
 template <typename T> struct Bits;
 template <> struct Bits<double> {
@@ -210,6 +273,40 @@ extern "C" int fn_generate(int cfg, uint64_t seed, int64_t row0, int64_t n, void
         case 5: gen_cfg5<<<g, 256, 0, s>>>(static_cast<double*>(x), row0, n, key); break;
         default: return fnb::set_error(FN_EINVAL, "cfg must be 1..5");
     }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fnb::set_error(FN_ECUDA, cudaGetErrorString(e));
+    return FN_OK;
+}
+
+extern "C" int fn_generate_regime(int regime, int dim, int dtype, uint64_t seed, int64_t row0,
+                                  int64_t n, void* x, void* stream) {
+    if (regime < 0 || regime > 4) return fnb::set_error(FN_EINVAL, "regime must be 0..4");
+    if (dim < 2 || dim > 4) return fnb::set_error(FN_EINVAL, "dim must be 2, 3 or 4");
+    if (dtype != FN_F32 && dtype != FN_F64) return fnb::set_error(FN_EINVAL, "bad dtype");
+    if (n < 0 || row0 < 0) return fnb::set_error(FN_EINVAL, "n and row0 must be >= 0");
+    if (n == 0) return FN_OK;
+    if (!x) return fnb::set_error(FN_EINVAL, "x is NULL");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const uint64_t cfg_id = 100 + (uint64_t)regime * 16 + (uint64_t)dim * 2 + (uint64_t)dtype;
+    const uint64_t key = mix64(seed ^ (cfg_id * 0xD6E8FEB86659FD93ull));
+    const int g = grid_for(n);
+    const bool f64 = dtype == FN_F64;
+    const int tmin = f64 ? -482 : -49, tmax = f64 ? 510 : 62;
+    const int sub_min = f64 ? -1074 : -149, norm_min = f64 ? -1022 : -126, emax = f64 ? 1023 : 127;
+    const double cap = f64 ? (0x1p-1022 - 0x1p-1074) : (0x1p-126 - 0x1p-149);
+#define FNB_GEN(T, D)                                                                             \
+    gen_regime<T, D><<<g, 256, 0, s>>>(static_cast<T*>(x), row0, n, key, regime, tmin, tmax, sub_min, \
+                                       norm_min, emax, cap)
+    if (f64) {
+        if (dim == 2) FNB_GEN(double, 2);
+        if (dim == 3) FNB_GEN(double, 3);
+        if (dim == 4) FNB_GEN(double, 4);
+    } else {
+        if (dim == 2) FNB_GEN(float, 2);
+        if (dim == 3) FNB_GEN(float, 3);
+        if (dim == 4) FNB_GEN(float, 4);
+    }
+#undef FNB_GEN
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fnb::set_error(FN_ECUDA, cudaGetErrorString(e));
     return FN_OK;

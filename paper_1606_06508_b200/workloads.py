@@ -154,6 +154,77 @@ def host_rows(cfg: int, row0: int, n: int, seed: int | None = None) -> np.ndarra
     raise ValueError(f"unknown config {cfg}")
 
 
+REGIMES = ("normal", "subnormal", "huge", "mixed", "unit-ish")
+_REGIME_FMT = {  # (tau_min exp, tau_max exp, min subnormal, min normal, max) binade exponents
+    "float64": (-482, 510, -1074, -1022, 1023),
+    "float32": (-49, 62, -149, -126, 127),
+}
+
+
+def _regime_key(regime: int, dim: int, dtype: str, seed: int) -> np.uint64:
+    cfg_id = 100 + regime * 16 + dim * 2 + (1 if dtype == "float64" else 0)
+    z = np.array([(seed ^ (cfg_id * _CFG_MUL)) & 0xFFFFFFFFFFFFFFFF], dtype=np.uint64)
+    return _mix(z)[0]
+
+
+def regime_rows(regime: str, dim: int, dtype: str, row0: int, n: int, seed: int = 0) -> np.ndarray:
+    """Host restatement of fn_generate_regime: the reference harness's regimes
+    (bench.py:146-207) on the counter-based generator.  Bit-identical to the device for
+    every regime but unit-ish (Box-Muller through libm)."""
+    r = REGIMES.index(regime)
+    tmin, tmax, sub_min, norm_min, emax = _REGIME_FMT[dtype]
+    key = _regime_key(r, dim, dtype, seed)
+    rows = np.arange(row0, row0 + n, dtype=np.int64)
+    W = lambda j: _words(key, rows, j)  # noqa: E731
+    single = dtype == "float32"
+    cap = (2.0 ** -126 - 2.0 ** -149) if single else (2.0 ** -1022 - 2.0 ** -1074)
+    with np.errstate(over="ignore", invalid="ignore", divide="ignore"):
+        if r == 4:
+            g = []
+            for p in range(2):
+                u1 = ((W(2 * p) >> np.uint64(11)) + np.uint64(1)).astype(np.float64) * 2.0 ** -53
+                u2 = (W(2 * p + 1) >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+                rad = np.sqrt(-2.0 * np.log(u1))
+                g += [rad * np.cos(2.0 * np.pi * u2), rad * np.sin(2.0 * np.pi * u2)]
+            g = np.stack(g[:dim], axis=1)
+            ss = np.zeros(n)
+            for k in range(dim):
+                ss = ss + g[:, k] * g[:, k]
+            nrm = np.sqrt(ss)
+            g[:, 0] = np.where(nrm == 0.0, 1.0, g[:, 0])
+            nrm = np.maximum(nrm, np.finfo(np.float64).tiny)
+            u = (W(12) >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+            vals = (g / nrm[:, None]) * (1.0 + (u * 2.0 - 1.0) * 2.0 ** -10)[:, None]
+        else:
+            lo, span = {0: (tmin, tmax - tmin), 1: (sub_min, norm_min - sub_min),
+                        2: (tmax + 1, emax - 1 - (tmax + 1)), 3: (sub_min, emax - sub_min)}[r]
+            cols = []
+            for k in range(dim):
+                w = W(k)
+                mag = np.ldexp(_mant52(W(4 + k)), _uexp(w, lo, span))
+                if r == 1:
+                    mag = np.minimum(mag, cap)
+                cols.append(_sign(w) * mag)
+            vals = np.stack(cols, axis=1)
+        out = vals.astype(np.float32 if single else np.float64)
+        if single and r == 1:
+            c = np.float32(cap)
+            out = np.clip(out, -c, c)
+    return np.ascontiguousarray(out)
+
+
+def generate_regime_device(regime: str, x, row0: int = 0, seed: int = 0, stream=None) -> None:
+    """Fill a contiguous CUDA tensor x[n, dim] (float32/float64) with regime rows."""
+    import torch
+
+    r = REGIMES.index(regime)
+    dt = _lib.F64 if x.dtype == torch.float64 else _lib.F32
+    s = torch.cuda.current_stream(x.device).cuda_stream if stream is None else stream
+    with torch.cuda.device(x.device):
+        rc = _lib.lib().fn_generate_regime(r, x.shape[1], dt, seed, row0, x.shape[0], x.data_ptr(), s)
+    _lib.check(rc, "fn_generate_regime")
+
+
 def generate_device(cfg: int, x, row0: int = 0, seed: int | None = None, stream=None) -> None:
     """Fill a contiguous CUDA tensor x[n, dim] with rows [row0, row0+n) of ``cfg``."""
     c = CONFIGS[cfg]

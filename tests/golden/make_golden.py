@@ -96,6 +96,39 @@ KATS = {
 }
 
 
+def _load_reference_rotation(compiled):
+    """The reference's rotation.py (and params.py / scale.py it needs), loaded by path
+    under a shim package whose _backend resolves to the reference's compiled kernels --
+    the reference package __init__ (gmpy2) is never executed."""
+    import types
+
+    pkg = types.ModuleType("fastnorm")
+    pkg.__path__ = []
+    backend = types.ModuleType("fastnorm._backend")
+    suffix = {"single": "f32", "double": "f64"}
+    backend.scalar_kernel = lambda base, precision, backend=None: getattr(compiled, f"{base}_{suffix[precision]}")
+    sys.modules["fastnorm"] = pkg
+    sys.modules["fastnorm._backend"] = backend
+    pkg._backend = backend
+    mods = {}
+    for name in ("params", "scale", "rotation"):
+        spec = importlib.util.spec_from_file_location(f"fastnorm.{name}", os.path.join(REF, f"{name}.py"))
+        mod = importlib.util.module_from_spec(spec)
+        sys.modules[f"fastnorm.{name}"] = mod
+        spec.loader.exec_module(mod)
+        setattr(pkg, name, mod)
+        mods[name] = mod
+    return mods["rotation"]
+
+
+ROT_KATS = [(0.0, 0.0, 0.0, 2.0), (1.0, 0.0, 0.0, 0.0), (1.0, 1.0, 1.0, 1.0),
+            (0.0, 0.0, 0.0, 1.0), (L(1, 600), -L(1, 600), 3.0 * L(1, 599), 1.0),
+            (L(1, -1000), 0.0, L(3, -1001), -L(1, -1070)), (DBL_MAX, DBL_MAX, 0.0, 1.0),
+            (5e-324, 0.0, 0.0, 5e-324), (-0.0, 0.0, 1.0, -0.0),
+            (0.0, 0.0, 0.0, 0.0), (-0.0, 0.0, -0.0, 0.0), (math.inf, 0.0, 0.0, 1.0),
+            (0.0, math.nan, 0.0, 1.0), (0.0, 0.0, 0.0, -math.inf)]  # last 5: rejected (ValueError)
+
+
 def random_rows(rng, m, dim, single):
     lo, hi = (-149, 127) if single else (-1074, 1023)
     e = rng.integers(lo, hi, (m, dim))
@@ -165,6 +198,31 @@ def main():
                 out[f"{prec}_{dim}_loop_{algo}"] = np.array([val], dtype=np.float64)
     for prec in ("f64", "f32"):
         out[f"{prec}_ka"] = np.array(KA[prec], dtype=np.float64)
+
+    # rotations (rotation.py:53-111) on quaternions of every magnitude class; rotation_unit
+    # is fed both raw quaternions and the reference's own normalize4 unit outputs.
+    rot = _load_reference_rotation(comp)
+    q = np.concatenate([random_rows(rng, 600, 4, False),
+                        rng.standard_normal((600, 4)),
+                        np.ldexp(rng.standard_normal((300, 4)), rng.integers(-1000, 1000, (300, 1))),
+                        np.array(ROT_KATS)])
+    ka = KA["f64"]
+    units = np.array([comp.normalize4_f64(*ka, *row)[1:] for row in q.tolist()])
+    gen, uni, uni_n = [], [], []
+    for row, urow in zip(q.tolist(), units.tolist()):
+        try:
+            gen.append(rot.rotation_general(row).flat())
+        except ValueError:
+            gen.append((math.nan,) * 9)
+        for dst, src in ((uni, row), (uni_n, urow)):
+            try:
+                dst.append(rot.rotation_unit(src).flat())
+            except ValueError:
+                dst.append((math.nan,) * 9)
+    out["rot_q"] = q
+    out["rot_general"] = np.array(gen)
+    out["rot_unit"] = np.array(uni)
+    out["rot_unit_of_normalized"] = np.array(uni_n)
     path = os.path.join(HERE, "golden_vectors.npz")
     np.savez_compressed(path, **out)
     n = sum(v.size for v in out.values())

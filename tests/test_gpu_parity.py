@@ -211,3 +211,32 @@ def test_division_selftest(cuda_dev, dtype):
         torch.cuda.synchronize()
         bad, a, b = out.tolist()
         assert bad == 0, (dtype, seed, bad, hex(a & (2**64 - 1)), hex(b & (2**64 - 1)))
+
+
+@pytest.mark.parametrize("regime", ["normal", "subnormal", "huge", "mixed", "unit-ish"])
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_reference_regimes(cuda_dev, regime, prec):
+    """The reference harness's input regimes (bench.py:146-207), every family, 2^20 rows."""
+    from paper_1606_06508_b200 import workloads
+
+    dt = torch.float64 if prec == "f64" else torch.float32
+    dtype = "float64" if prec == "f64" else "float32"
+    ka = np.array(fn.kernel_args(fn.preset(PREC[prec])))
+    for dim in (2, 3, 4):
+        n = (1 << 20) + 3
+        x = torch.empty((n, dim), dtype=dt, device=cuda_dev)
+        workloads.generate_regime_device(regime, x, seed=11)
+        host = workloads.regime_rows(regime, dim, dtype, 1000, 5000, seed=11)
+        dev = x[1000:6000].cpu().numpy()
+        if regime == "unit-ish":
+            assert np.allclose(dev, host, rtol=1e-6, atol=1e-7)
+        else:
+            assert (dev.view(np.uint8) == host.view(np.uint8)).all(), (regime, prec, dim)
+        for fam in FAMILIES[dim] + ["normalize_sq"]:
+            base = f"normalize{dim}_sq" if fam == "normalize_sq" else _base(fam, dim)
+            op = _lib.OP_NORMALIZE_SQ if fam == "normalize_sq" else OPS[fam]
+            takes = fam in SCALING or fam == "normalize_sq"
+            res = _cuda_kernels.batch_kernel(base, prec)(x, ka if takes else None)
+            torch.cuda.synchronize()
+            bad, first = compare_chunked(op, x, res.head, res.body, res.sq, ka if takes else None)
+            assert bad == 0, (regime, fam, prec, dim, bad, first)

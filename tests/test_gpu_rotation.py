@@ -1,0 +1,83 @@
+"""Batched rotations on the GPU (reference rotation.py:53-111), bit for bit against the
+reference's own outputs (golden) and the oracle, including the fused normalize4 ->
+rotation_unit kernel, at the config-3 size (2^27 quaternions)."""
+
+import numpy as np
+import pytest
+
+from gpu_helpers import to_np
+
+import oracle
+import paper_1606_06508_b200 as fn
+from paper_1606_06508_b200 import workloads
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.mark.parametrize("where", ["device", "device_unaligned", "host"])
+def test_rotation_golden(golden, cuda_dev, where):
+    q = golden["rot_q"]
+    if where == "device":
+        qd = torch.from_numpy(q).to(cuda_dev)
+    elif where == "device_unaligned":
+        qd = torch.from_numpy(np.concatenate([q[:1], q])).to(cuda_dev)[1:]
+    else:
+        qd = q
+    g = fn.rotation_general(qd, strict=False)
+    u = fn.rotation_unit(qd, strict=False)
+    torch.cuda.synchronize()
+    g = to_np(g) if hasattr(g, "cpu") else g
+    u = to_np(u) if hasattr(u, "cpu") else u
+    assert oracle.same(g.reshape(-1, 9), golden["rot_general"]).all()
+    assert oracle.same(u.reshape(-1, 9), golden["rot_unit"]).all()
+    res = fn.normalize4_rotation(fn.preset("double"), qd)
+    torch.cuda.synchronize()
+    R = to_np(res.rotation) if hasattr(res.rotation, "cpu") else res.rotation
+    assert oracle.same(R.reshape(-1, 9), golden["rot_unit_of_normalized"]).all()
+
+
+def test_rotation_errors_and_kats(cuda_dev):
+    with pytest.raises(ValueError):
+        fn.rotation_general((0.0, 0.0, 0.0, 0.0))
+    with pytest.raises(ValueError):
+        fn.rotation_general((float("inf"), 0.0, 0.0, 1.0))
+    with pytest.raises(ValueError):
+        fn.rotation_unit((float("nan"), 0.0, 0.0, 1.0))
+    assert fn.rotation_general((0.0, 0.0, 0.0, 2.0)).rows == ((1.0, 0.0, 0.0), (0.0, 1.0, 0.0), (0.0, 0.0, 1.0))
+    assert fn.rotation_general((1.0, 0.0, 0.0, 0.0)).rows == ((1.0, 0.0, 0.0), (0.0, -1.0, 0.0), (0.0, 0.0, -1.0))
+    assert fn.rotation_general((1.0, 1.0, 1.0, 1.0)).rows == ((0.0, 0.0, 1.0), (1.0, 0.0, 0.0), (0.0, 1.0, 0.0))
+    q = torch.tensor([[0.0, 0.0, 0.0, 1.0], [0.0, 0.0, 0.0, 0.0]], dtype=torch.float64, device=cuda_dev)
+    with pytest.raises(ValueError):
+        fn.rotation_general(q)
+    R = fn.rotation_general(q, strict=False)
+    torch.cuda.synchronize()
+    assert torch.isnan(R[1]).all() and R[0].tolist() == [[1.0, 0.0, 0.0], [0.0, 1.0, 0.0], [0.0, 0.0, 1.0]]
+    fn.rotation_unit(q)  # the zero quaternion is finite: accepted by the unit form
+    with pytest.raises(TypeError):
+        fn.rotation_unit(q.float())
+
+
+def test_rotations_cfg3_full(cuda_dev):
+    """All 2^27 config-3 quaternions through the three rotation kernels vs the oracle."""
+    ka = np.array(fn.kernel_args(fn.preset("double")))
+    n = workloads.CONFIGS[3].rows
+    q = torch.empty((n, 4), dtype=torch.float64, device=cuda_dev)
+    workloads.generate_device(3, q)
+    res = fn.normalize4_rotation(fn.preset("double"), q)
+    G = fn.rotation_general(q)
+    torch.cuda.synchronize()
+    chunk = 1 << 24
+    for lo in range(0, n, chunk):
+        hi = min(n, lo + chunk)
+        qh = to_np(q[lo:hi])
+        r, u, R, bad = oracle.rotation(oracle.OP_NORMALIZE_ROT, qh, ka)
+        assert bad == 0
+        assert oracle.same(to_np(res.length[lo:hi]), r).all()
+        assert oracle.same(to_np(res.unit[lo:hi]), u).all()
+        assert oracle.same(to_np(res.rotation[lo:hi]), R).all()
+        Rg, bad = oracle.rotation(oracle.OP_ROT_GENERAL, qh, ka)
+        assert bad == 0 and oracle.same(to_np(G[lo:hi]), Rg).all()
+    U = fn.rotation_unit(res.unit)
+    torch.cuda.synchronize()
+    assert bool((U.view(torch.int64) == res.rotation.view(torch.int64)).all())

@@ -54,3 +54,18 @@ def test_golden_covers_special_classes(golden):
             assert (np.abs(x).max(axis=1) == 0).sum() >= 2
             tiny = np.finfo(np.float32 if prec == "f32" else np.float64).tiny
             assert ((np.abs(x) < tiny) & (x != 0)).any(axis=1).sum() > 10
+
+
+def test_oracle_rotations_match_reference_golden(golden, oracle_mod):
+    """rotation_general / rotation_unit (rotation.py:53-111) as evaluated by the reference
+    module itself, including rows it rejects (stored as NaN)."""
+    q = golden["rot_q"]
+    ka = golden["f64_ka"]
+    R, bad = oracle_mod.rotation(oracle_mod.OP_ROT_GENERAL, q, ka)
+    assert oracle_mod.same(R.reshape(-1, 9), golden["rot_general"]).all() and bad == 5
+    R, bad = oracle_mod.rotation(oracle_mod.OP_ROT_UNIT, q)
+    assert oracle_mod.same(R.reshape(-1, 9), golden["rot_unit"]).all() and bad == 3
+    r, u, R, bad = oracle_mod.rotation(oracle_mod.OP_NORMALIZE_ROT, q, ka)
+    assert oracle_mod.same(R.reshape(-1, 9), golden["rot_unit_of_normalized"]).all()
+    h, b, _ = oracle_mod.run(oracle_mod.OP_NORMALIZE, q, ka)
+    assert oracle_mod.same(r, h).all() and oracle_mod.same(u, b).all()

@@ -70,3 +70,26 @@ def test_row_stats_host(cfg):
     prec = "single" if x.dtype == np.float32 else "double"
     c = workloads.row_stats_host(x, kernel_args(preset(prec)))
     assert int(c.sum()) == len(x)
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("dim", [2, 3, 4])
+def test_reference_regime_ranges(dtype, dim):
+    """Regime contracts of the reference harness (bench.py:151-158, test_bench.py)."""
+    p = preset("double" if dtype == "float64" else "single")
+    n = 20000
+    x = workloads.regime_rows("normal", dim, dtype, 0, n).astype(np.float64)
+    assert (np.abs(x) >= p.tau_min).all() and (np.abs(x) <= p.tau_max).all()
+    x = workloads.regime_rows("subnormal", dim, dtype, 0, n).astype(np.float64)
+    assert (np.abs(x) >= p.alpha).all() and (np.abs(x) < p.nu).all()
+    x = workloads.regime_rows("huge", dim, dtype, 0, n).astype(np.float64)
+    assert (np.abs(x) > p.tau_max).all() and np.isfinite(x).all()
+    x = workloads.regime_rows("mixed", dim, dtype, 0, n).astype(np.float64)
+    assert np.isfinite(x).all() and (x != 0).all()
+    assert (np.abs(x) < p.nu).any() and (np.abs(x) > p.tau_max).any()
+    x = workloads.regime_rows("unit-ish", dim, dtype, 0, n).astype(np.float64)
+    norms = np.sqrt((x * x).sum(axis=1))
+    assert (np.abs(norms - 1.0) <= 2.0 ** -10 + 1e-6).all()
+    a = workloads.regime_rows("mixed", dim, dtype, 100, 50)
+    b = workloads.regime_rows("mixed", dim, dtype, 0, 200)[100:150]
+    assert (a.view(np.uint8) == b.view(np.uint8)).all()

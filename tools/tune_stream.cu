@@ -103,7 +103,7 @@ struct Variant {
 template <typename T, int N, int OP>
 constexpr int row_bytes() {
     using Op = RowOp<T, N, OP>;
-    return (int)sizeof(T) * (N + 1 + (Op::kBody ? N : 0) + (Op::kSq ? 1 : 0));
+    return (int)sizeof(T) * (N + Op::W0 + Op::W1 + Op::W2);
 }
 
 #define V(FAM, CFG, T, N, OP, TR, S, NT, H, CPS)                                         \
@@ -119,11 +119,11 @@ int main(int argc, char** argv) {
     const int64_t n = (int64_t)1 << lg;
     Bufs b;
     b.n = n;
-    // sized for the largest row (4 x f64 in, 4 x f64 body, head, sq)
+    // sized for the largest records (4 x f64 in; head / extra up to a 3x3 f64 matrix)
     CK(cudaMalloc(&b.x, n * 32));
-    CK(cudaMalloc(&b.h, n * 8));
+    CK(cudaMalloc(&b.h, n * 72));
     CK(cudaMalloc(&b.b, n * 32));
-    CK(cudaMalloc(&b.q, n * 8));
+    CK(cudaMalloc(&b.q, n * 72));
     printf("rows=%lld sms=%d\n", (long long)n, sms);
 
     if (which == "all" || which == "sol") {
@@ -188,6 +188,13 @@ int main(int argc, char** argv) {
         vs.push_back(V("quotient3_f32", 4, float, 3, FN_OP_QUOTIENT, 512, 4, 256, 0, 4));
         vs.push_back(V("quotient3_fast_f32", 4, float, 3, FN_OP_QUOTIENT3_FAST, 512, 4, 256, 0, 4));
         vs.push_back(V("naive3_f32", 4, float, 3, FN_OP_NAIVE, 512, 4, 256, 0, 4));
+    }
+    if (which == "all" || which == "rot") {
+        vs.push_back(V("rotation_unit_f64", 3, double, 4, FN_OP_ROT_UNIT, 256, 3, 256, 0, 2));
+        vs.push_back(V("rotation_general_f64", 3, double, 4, FN_OP_ROT_GENERAL, 256, 3, 256, 0, 2));
+        vs.push_back(V("rotation_general_f64", 3, double, 4, FN_OP_ROT_GENERAL, 256, 3, 256, 0, 4));
+        vs.push_back(V("normalize4_rot_f64", 3, double, 4, FN_OP_NORMALIZE_ROT, 128, 3, 256, 0, 2));
+        vs.push_back(V("normalize4_rot_f64", 3, double, 4, FN_OP_NORMALIZE_ROT, 128, 4, 128, 0, 3));
     }
     if (which == "all" || which == "f64x2") {
         vs.push_back(V("normalize2_f64", 2, double, 2, FN_OP_NORMALIZE, 512, 4, 256, 0, 2));
