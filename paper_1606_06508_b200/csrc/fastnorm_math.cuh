@@ -139,25 +139,12 @@ __device__ __forceinline__ double signed_zero_of_quotient(double a, double b) {
 
 template <typename T> struct Divider;
 
-// FNB_F64_DIV_MARKSTEIN = 1 selects the shared-reciprocal fast path above for binary64;
-// 0 divides with __ddiv_rn per numerator.  Both are correctly rounded; which is faster
-// depends on how often rows need the subnormal-result slow path (tools/tune_stream).
-#ifndef FNB_F64_DIV_MARKSTEIN
-#define FNB_F64_DIV_MARKSTEIN 0
-#endif
-
-#if !FNB_F64_DIV_MARKSTEIN
-template <> struct Divider<double> {
-    double b;
-    __device__ __forceinline__ explicit Divider(double b_) : b(b_) {}
-    __device__ __forceinline__ double operator()(double a) const { return __ddiv_rn(a, b); }
-};
-#else
-template <> struct Divider<double> {
+// Binary64 shared-divisor division with the Markstein fast path described above.
+struct MarksteinDivider {
     double b, y;
     int eb;
     bool bfast;
-    __device__ __forceinline__ explicit Divider(double b_) : b(b_) {
+    __device__ __forceinline__ explicit MarksteinDivider(double b_) : b(b_) {
         eb = biased_exp(b_);
         bfast = eb >= 3 && eb <= 2044;
         y = __drcp_rn(bfast ? b_ : 1.0);
@@ -174,6 +161,26 @@ template <> struct Divider<double> {
             return signed_zero_of_quotient(a, b);
         return __ddiv_rn(a, b);
     }
+};
+
+// FNB_F64_DIV_MARKSTEIN = 1 selects MarksteinDivider for the binary64 quotient / naive
+// families; 0 divides with __ddiv_rn per numerator.  Both are correctly rounded; on
+// wide-range rows (config 5) the subnormal-result slow path dominates and plain
+// __ddiv_rn measured faster (profiles/r01d_div_*.csv), so 0 is the default.  Rotations,
+// whose divisor ss sits in the scaled band, always use MarksteinDivider.
+#ifndef FNB_F64_DIV_MARKSTEIN
+#define FNB_F64_DIV_MARKSTEIN 0
+#endif
+
+#if !FNB_F64_DIV_MARKSTEIN
+template <> struct Divider<double> {
+    double b;
+    __device__ __forceinline__ explicit Divider(double b_) : b(b_) {}
+    __device__ __forceinline__ double operator()(double a) const { return __ddiv_rn(a, b); }
+};
+#else
+template <> struct Divider<double> : MarksteinDivider {
+    __device__ __forceinline__ explicit Divider(double b_) : MarksteinDivider(b_) {}
 };
 #endif
 
@@ -447,7 +454,7 @@ __device__ __forceinline__ bool rotation_general_row(const T (&x)[4], const KArg
     const T ss = F::add(F::add(F::add(a11, a22), a33), a44);
     const T two = T(2);
     auto sub = [](T a, T b) { return F::add(a, -b); };
-    const Divider<T> by_ss(ss);
+    const MarksteinDivider by_ss(ss);  // ss in the scaled band: the fast path applies
     R[0] = by_ss(sub(sub(F::add(a11, a44), a22), a33));
     R[1] = by_ss(F::mul(two, sub(F::mul(q1, q2), F::mul(q3, q4))));
     R[2] = by_ss(F::mul(two, F::add(F::mul(q1, q3), F::mul(q2, q4))));

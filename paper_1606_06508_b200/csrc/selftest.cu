@@ -1,6 +1,7 @@
 // selftest.cu -- device self-test of the shared-divisor division (fastnorm_math.cuh).
 //
-// fn_selftest_div(dtype, seed, n, out, stream) evaluates Divider<T>(b)(a) for n
+// fn_selftest_div(dtype, seed, n, out, stream) evaluates MarksteinDivider (binary64)
+// and Divider<float> (binary32) for n
 // generated operand pairs and compares each result bit for bit (NaN == NaN) with the
 // IEEE division of the CUDA math library (__ddiv_rn / __fdiv_rn).  Operands mix
 // full-range random bit patterns, all-ones / power-of-two mantissas, exponents at and
@@ -88,7 +89,7 @@ __global__ void selftest_f64(uint64_t seed, int64_t n, unsigned long long* out) 
             a = (w3 >> 8) & 1 ? special_f64(w0) : __longlong_as_double((long long)make_f64(w0, w1, 0));
             b = (w3 >> 9) & 1 ? special_f64(w2) : __longlong_as_double((long long)make_f64(w2, w1, 0));
         }
-        const double got = fnb::Divider<double>(b)(a);
+        const double got = fnb::MarksteinDivider(b)(a);
         const double want = __ddiv_rn(a, b);
         const bool ok = (__double_as_longlong(got) == __double_as_longlong(want)) ||
                         (isnan(got) && isnan(want));
