@@ -262,12 +262,22 @@ int run(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* 
 // on the two copy engines while the kernel of a third chunk runs.
 // ---------------------------------------------------------------------------------
 struct Staging {
-    static constexpr int kPipes = 3;
-    cudaStream_t streams[kPipes] = {};
-    void* buf[kPipes] = {};
+    static constexpr int kMaxPipes = 8;
+    int pipes = 3;
+    cudaStream_t streams[kMaxPipes] = {};
+    void* buf[kMaxPipes] = {};
     size_t bytes = 0;
     bool init = false;
 };
+
+// Host-path pipeline shape: FASTNORM_B200_HOST_PIPES (2..8, default 3) streams and
+// FASTNORM_B200_HOST_CHUNK_MB (default 48) MiB of input per chunk.
+static int env_int(const char* name, int dflt, int lo, int hi) {
+    const char* e = getenv(name);
+    if (!e) return dflt;
+    const int v = atoi(e);
+    return v < lo ? lo : (v > hi ? hi : v);
+}
 static std::mutex g_stage_mu;
 static std::vector<Staging> g_stage;
 
@@ -276,19 +286,20 @@ static int staging_get(int dev, size_t bytes_per_pipe, Staging** out) {
     Staging& st = g_stage[dev];
     cudaError_t e;
     if (!st.init) {
-        for (int p = 0; p < Staging::kPipes; ++p) {
+        st.pipes = env_int("FASTNORM_B200_HOST_PIPES", 3, 2, Staging::kMaxPipes);
+        for (int p = 0; p < st.pipes; ++p) {
             e = cudaStreamCreateWithFlags(&st.streams[p], cudaStreamNonBlocking);
             if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
         }
         st.init = true;
     }
     if (st.bytes < bytes_per_pipe) {
-        for (int p = 0; p < Staging::kPipes; ++p) {
+        for (int p = 0; p < st.pipes; ++p) {
             if (st.buf[p]) cudaFree(st.buf[p]);
             st.buf[p] = nullptr;
         }
         st.bytes = 0;
-        for (int p = 0; p < Staging::kPipes; ++p) {
+        for (int p = 0; p < st.pipes; ++p) {
             e = cudaMalloc(&st.buf[p], bytes_per_pipe);
             if (e != cudaSuccess) return fail(FN_ENOMEM, "cudaMalloc staging buffer failed");
         }
@@ -310,7 +321,8 @@ int host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, v
     const size_t w = dtype == FN_F64 ? 8 : 4;
     const Widths wd = op_widths(op, dim);
     // ~48 MiB of input per chunk: three chunks in flight, per-copy latency amortised.
-    const int64_t chunk_rows = std::max<int64_t>(4096, ((int64_t)48 << 20) / (int64_t)(dim * w));
+    const int64_t chunk_mb = env_int("FASTNORM_B200_HOST_CHUNK_MB", 48, 1, 1024);
+    const int64_t chunk_rows = std::max<int64_t>(4096, (chunk_mb << 20) / (int64_t)(dim * w));
     const int64_t rows = std::min<int64_t>(n, chunk_rows);
     const size_t bx = align256(rows * dim * w), b0 = align256(rows * wd.w0 * w),
                  b1 = align256(rows * wd.w1 * w), b2 = align256(rows * wd.w2 * w);
@@ -320,7 +332,7 @@ int host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, v
     if (rc != FN_OK) return rc;
     int64_t chunk = 0;
     for (int64_t r0 = 0; r0 < n; r0 += rows, ++chunk) {
-        const int p = (int)(chunk % Staging::kPipes);
+        const int p = (int)(chunk % st->pipes);
         const int64_t m = std::min<int64_t>(rows, n - r0);
         cudaStream_t s = st->streams[p];
         char* base = static_cast<char*>(st->buf[p]);
@@ -343,7 +355,7 @@ int host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, v
                                 cudaMemcpyDeviceToHost, s);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync D2H");
     }
-    for (int p = 0; p < Staging::kPipes; ++p) {
+    for (int p = 0; p < st->pipes; ++p) {
         e = cudaStreamSynchronize(st->streams[p]);
         if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
     }

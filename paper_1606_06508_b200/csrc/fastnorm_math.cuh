@@ -166,8 +166,9 @@ struct MarksteinDivider {
 // FNB_F64_DIV_MARKSTEIN = 1 selects MarksteinDivider for the binary64 quotient / naive
 // families; 0 divides with __ddiv_rn per numerator.  Both are correctly rounded; on
 // wide-range rows (config 5) the subnormal-result slow path dominates and plain
-// __ddiv_rn measured faster (profiles/r01d_div_*.csv), so 0 is the default.  Rotations,
-// whose divisor ss sits in the scaled band, always use MarksteinDivider.
+// __ddiv_rn measured faster (profiles/r01d_div_*.csv); for rotation_general (9 entries
+// over one ss) it also measured slower (5338 vs 5552 GB/s, profiles/r01f_tune_rot.csv).
+// So 0 is the default; the variant stays selectable and is checked by fn_selftest_div.
 #ifndef FNB_F64_DIV_MARKSTEIN
 #define FNB_F64_DIV_MARKSTEIN 0
 #endif
@@ -454,7 +455,7 @@ __device__ __forceinline__ bool rotation_general_row(const T (&x)[4], const KArg
     const T ss = F::add(F::add(F::add(a11, a22), a33), a44);
     const T two = T(2);
     auto sub = [](T a, T b) { return F::add(a, -b); };
-    const MarksteinDivider by_ss(ss);  // ss in the scaled band: the fast path applies
+    const Divider<T> by_ss(ss);
     R[0] = by_ss(sub(sub(F::add(a11, a44), a22), a33));
     R[1] = by_ss(F::mul(two, sub(F::mul(q1, q2), F::mul(q3, q4))));
     R[2] = by_ss(F::mul(two, F::add(F::mul(q1, q3), F::mul(q2, q4))));
