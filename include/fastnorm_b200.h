@@ -169,6 +169,20 @@ int fn_generate(int cfg, uint64_t seed, int64_t row0, int64_t n, void* x, void* 
 int fn_generate_regime(int regime, int dim, int dtype, uint64_t seed, int64_t row0, int64_t n,
                        void* x, void* stream);
 
+/* ---- error-bound sweep (reference oracle.py:151-250, in double-double) ----------- */
+/* For rows x[N,dim] with computed r[N], unit[N,dim] (device arrays of dtype), checks the
+ * paper's bounds for the scaling algorithm.  limits = {u, alpha, nu, omega} of the format.
+ * counts[12] (accumulated): nan-output, nonzero-length, finite-unit, sin-phi, direction,
+ *   finite-length, length-in-range, length-near-underflow, quaternion-product,
+ *   rows measured (finite nonzero input), rows skipped, rows with any violation.
+ * maxbits[4] (atomicMax on the bit patterns; zero them first): max relative length
+ *   error, max absolute length error, max direction error, max sin(phi).
+ * argmax[5]: row index of each maximum (best effort), argmax[4] = first violating row
+ *   (atomicMin; initialise to UINT64_MAX). */
+int fn_measure_bounds(int dim, int dtype, const void* x, const void* r, const void* unit, int64_t n,
+                      const double* limits, uint64_t* counts, uint64_t* maxbits, uint64_t* argmax,
+                      void* stream);
+
 /* ---- device self-test of the shared-divisor division (fastnorm_math.cuh) ----------- */
 /* Compares the kernels' correctly-rounded division against the CUDA math library's
  * IEEE division on n generated operand pairs (full range, mantissa / exponent edge

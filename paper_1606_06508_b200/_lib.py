@@ -60,6 +60,8 @@ def _declare(L: ctypes.CDLL) -> None:
     L.fn_generate.argtypes = [_int, ctypes.c_uint64, _i64, _i64, _vp, _vp]
     L.fn_generate_regime.restype = _int
     L.fn_generate_regime.argtypes = [_int, _int, _int, ctypes.c_uint64, _i64, _i64, _vp, _vp]
+    L.fn_measure_bounds.restype = _int
+    L.fn_measure_bounds.argtypes = [_int, _int, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]
     L.fn_selftest_div.restype = _int
     L.fn_selftest_div.argtypes = [_int, ctypes.c_uint64, _i64, _vp, _vp]
     L.fn_row_stats.restype = _int
