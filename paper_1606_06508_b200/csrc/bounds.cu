@@ -210,7 +210,7 @@ __global__ void bounds_kernel(const T* __restrict__ x, const T* __restrict__ rh,
                     if (in_range) {
                         if (abs_err_s > tol_s) viol |= 1u << V_LEN_IN;
                     } else {
-                        if (abs_err_s > tol_s + ldexp(0.5 * lim.alpha, -e)) viol |= 1u << V_LEN_UNDER;
+                        if (abs_err_s > tol_s + ldexp(lim.alpha, -e - 1)) viol |= 1u << V_LEN_UNDER;  // alpha/2 at scale
                     }
                 }
             }

@@ -52,13 +52,12 @@ def test_bounds_hold_on_cfg5_and_cfg4(cuda_dev):
 def _exact_metrics(xs, r_hat, unit):
     q = [Fraction(v) for v in xs]
     s = sum(v * v for v in q)
-    r = math.sqrt(s)  # only for the relative tolerance below; exact checks use Fractions
     # direction error^2 = sum (u_k - x_k / r)^2, evaluated with r from a 200-bit isqrt
     bits = 200
     r_fx = Fraction(math.isqrt((s.numerator * s.denominator) << (2 * bits)), s.denominator << bits)
     d2 = sum((Fraction(uk) - xk / r_fx) ** 2 for uk, xk in zip(unit, q))
     rel = abs(Fraction(r_hat) - r_fx) / r_fx
-    return float(rel), math.sqrt(float(d2)), r
+    return float(rel), math.sqrt(float(d2))
 
 
 def test_metrics_match_exact_rationals(cuda_dev):
@@ -70,7 +69,7 @@ def test_metrics_match_exact_rationals(cuda_dev):
         xh, rh, uh = x.cpu().numpy(), out.length.cpu().numpy(), out.unit.cpu().numpy()
         rels, dirs = [], []
         for i in range(len(xh)):
-            rel, d, _ = _exact_metrics(xh[i].tolist(), float(rh[i]), uh[i].tolist())
+            rel, d = _exact_metrics(xh[i].tolist(), float(rh[i]), uh[i].tolist())
             rels.append(rel)
             dirs.append(d)
         assert s.max_metrics["rel_length_err"] == pytest.approx(max(rels) / p.u, rel=1e-9, abs=1e-9)
