@@ -90,6 +90,11 @@ int fn_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, voi
            void* sq, const double* ka, void* stream);
 int fn_host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head,
                 void* body, void* sq, const double* ka);
+/* fn_host_run over several devices of one process: rows are split into ndev contiguous
+ * balanced shards, one host thread per device runs the pipelined host path on its
+ * shard (no inter-device traffic; each device brings its own PCIe link). */
+int fn_host_run_multi(int op, int dim, int dtype, const void* x, int64_t n, void* head,
+                      void* body, void* sq, const double* ka, const int* devices, int ndev);
 /* fn_run for the rotation ops, with a device counter (uint64, accumulated; may be NULL)
  * of rows the reference would reject. */
 int fn_run_rot(int op, const double* q, int64_t n, double* head, double* body, double* extra,

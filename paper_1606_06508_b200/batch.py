@@ -14,6 +14,8 @@ No path computes on the CPU: without the CUDA library every call raises.
 
 from __future__ import annotations
 
+import threading
+from contextlib import contextmanager
 from typing import Any, NamedTuple
 
 import numpy as np
@@ -35,6 +37,24 @@ def widths(op: int, dim: int) -> tuple[int, int, int]:
 
 def _shape(n: int, w: int) -> tuple[int, ...]:
     return (n,) if w == 1 else ((n, 3, 3) if w == 9 else (n, w))
+
+
+_host = threading.local()
+
+
+@contextmanager
+def host_devices(devices):
+    """Within the scope (this thread), host-array calls shard their rows over
+    ``devices`` (CUDA ordinals), one host thread per device (fn_host_run_multi)."""
+    devs = [int(d) for d in devices]
+    if not devs:
+        raise ValueError("host_devices needs at least one device")
+    prev = getattr(_host, "devices", None)
+    _host.devices = devs
+    try:
+        yield devs
+    finally:
+        _host.devices = prev
 
 
 class BatchOut(NamedTuple):
@@ -149,6 +169,13 @@ def run(op: int, dim: int, x, ka_arr: np.ndarray | None, out=None, invalid=None)
 
     head, body, extra = alloc_np(o_head, w0, "head"), alloc_np(o_body, w1, "body"), alloc_np(o_extra, w2, "extra")
     ptr = (lambda a: None if a is None else a.ctypes.data)
-    rc = L.fn_host_run(op, dim, dcode, x.ctypes.data, n, ptr(head), ptr(body), ptr(extra), kptr)
-    _lib.check(rc, "fn_host_run")
+    devs = getattr(_host, "devices", None)
+    if devs:
+        darr = np.array(devs, dtype=np.int32)
+        rc = L.fn_host_run_multi(op, dim, dcode, x.ctypes.data, n, ptr(head), ptr(body), ptr(extra),
+                                 kptr, darr.ctypes.data, len(devs))
+        _lib.check(rc, "fn_host_run_multi")
+    else:
+        rc = L.fn_host_run(op, dim, dcode, x.ctypes.data, n, ptr(head), ptr(body), ptr(extra), kptr)
+        _lib.check(rc, "fn_host_run")
     return BatchOut(head, body, extra)

@@ -8,7 +8,9 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -278,12 +280,28 @@ static int env_int(const char* name, int dflt, int lo, int hi) {
     const int v = atoi(e);
     return v < lo ? lo : (v > hi ? hi : v);
 }
+// One staging set and one mutex per device; the table itself is guarded by g_stage_mu.
 static std::mutex g_stage_mu;
-static std::vector<Staging> g_stage;
+static std::vector<std::unique_ptr<Staging>> g_stage;
+static std::vector<std::unique_ptr<std::mutex>> g_stage_dev_mu;
 
+static std::mutex& device_mutex(int dev) {
+    std::lock_guard<std::mutex> lk(g_stage_mu);
+    while ((int)g_stage.size() <= dev) {
+        g_stage.emplace_back(new Staging());
+        g_stage_dev_mu.emplace_back(new std::mutex());
+    }
+    return *g_stage_dev_mu[dev];
+}
+
+// Caller holds device_mutex(dev).
 static int staging_get(int dev, size_t bytes_per_pipe, Staging** out) {
-    if ((int)g_stage.size() <= dev) g_stage.resize(dev + 1);
-    Staging& st = g_stage[dev];
+    Staging* stp;
+    {
+        std::lock_guard<std::mutex> lk(g_stage_mu);
+        stp = g_stage[dev].get();
+    }
+    Staging& st = *stp;
     cudaError_t e;
     if (!st.init) {
         st.pipes = env_int("FASTNORM_B200_HOST_PIPES", 3, 2, Staging::kMaxPipes);
@@ -326,7 +344,7 @@ int host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, v
     const int64_t rows = std::min<int64_t>(n, chunk_rows);
     const size_t bx = align256(rows * dim * w), b0 = align256(rows * wd.w0 * w),
                  b1 = align256(rows * wd.w1 * w), b2 = align256(rows * wd.w2 * w);
-    std::lock_guard<std::mutex> lk(g_stage_mu);
+    std::lock_guard<std::mutex> lk(device_mutex(dev));
     Staging* st = nullptr;
     rc = staging_get(dev, bx + b0 + b1 + b2, &st);
     if (rc != FN_OK) return rc;
@@ -362,6 +380,49 @@ int host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, v
     return FN_OK;
 }
 
+// Row shards over several devices, one host thread per device, each running the
+// chunked host pipeline above on its own streams and staging buffers.  No data moves
+// between devices (rows are independent, _kernels.pyx:167-412).
+int host_run_multi(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* body,
+                   void* sq, const double* ka, const int* devices, int ndev) {
+    if (ndev < 1 || !devices) return fail(FN_EINVAL, "need at least one device");
+    int rc = check_args(op, dim, dtype, x, n, head, body, sq);
+    if (rc != FN_OK || n == 0) return rc;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+    for (int k = 0; k < ndev; ++k)
+        if (devices[k] < 0 || devices[k] >= count) return fail(FN_EINVAL, "device index out of range");
+    const size_t w = dtype == FN_F64 ? 8 : 4;
+    const Widths wd = op_widths(op, dim);
+    std::vector<int> rcs(ndev, FN_OK);
+    std::vector<std::string> errs(ndev);
+    std::vector<std::thread> pool;
+    const int64_t base = n / ndev, extra = n % ndev;
+    int64_t lo = 0;
+    for (int k = 0; k < ndev; ++k) {
+        const int64_t m = base + (k < extra ? 1 : 0);
+        const int64_t r0 = lo;
+        lo += m;
+        pool.emplace_back([&, k, r0, m]() {
+            cudaError_t ee = cudaSetDevice(devices[k]);
+            if (ee != cudaSuccess) {
+                rcs[k] = cuda_fail(ee, "cudaSetDevice");
+            } else if (m > 0) {
+                rcs[k] = host_run(op, dim, dtype, static_cast<const char*>(x) + r0 * dim * w, m,
+                                  static_cast<char*>(head) + r0 * wd.w0 * w,
+                                  wd.w1 ? static_cast<char*>(body) + r0 * wd.w1 * w : nullptr,
+                                  wd.w2 ? static_cast<char*>(sq) + r0 * wd.w2 * w : nullptr, ka);
+            }
+            if (rcs[k] != FN_OK) errs[k] = g_last_error;
+        });
+    }
+    for (auto& t : pool) t.join();
+    for (int k = 0; k < ndev; ++k)
+        if (rcs[k] != FN_OK) return fail(rcs[k], "device " + std::to_string(devices[k]) + ": " + errs[k]);
+    return FN_OK;
+}
+
 }  // namespace fnb
 
 // =====================================================================================
@@ -388,6 +449,11 @@ int fn_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, voi
 int fn_host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* body,
                 void* sq, const double* ka) {
     return fnb::host_run(op, dim, dtype, x, n, head, body, sq, ka);
+}
+
+int fn_host_run_multi(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* body,
+                      void* sq, const double* ka, const int* devices, int ndev) {
+    return fnb::host_run_multi(op, dim, dtype, x, n, head, body, sq, ka, devices, ndev);
 }
 
 int fn_run_rot(int op, const double* q, int64_t n, double* head, double* body, double* extra,

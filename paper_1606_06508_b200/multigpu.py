@@ -6,9 +6,15 @@ collective on the data path.  The only collectives are two tiny all-reduces afte
 timed region: MAX of the elapsed time (the job takes as long as its slowest rank) and
 SUM of six row-class counters (validation statistics).  Works with any
 torch.distributed backend: NCCL on the B200 box, gloo for the CPU tests.
+
+For a single process driving several GPUs with host arrays, ``host_devices([...])``
+shards every host-array call over those devices (fn_host_run_multi: one host thread
+and one PCIe link per device).
 """
 
 from __future__ import annotations
+
+from paper_1606_06508_b200.batch import host_devices  # noqa: F401  (re-export)
 
 COUNTER_NAMES = ("nan", "inf", "zero", "below_tau_min", "above_tau_max", "in_band")
 

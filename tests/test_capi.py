@@ -105,3 +105,16 @@ def test_no_cpu_fallback_without_gpu():
         fn.normalize3(fn.preset("double"), np.ones((8, 3)))
     with pytest.raises(_lib.CudaLibraryError):
         fn.normalize3(fn.preset("double"), 3.0, 4.0, 12.0)
+
+
+def test_host_run_multi_argument_errors():
+    L = _lib.lib()
+    x = np.zeros((4, 3))
+    h = np.zeros(4)
+    b = np.zeros((4, 3))
+    ka = np.array([2.0 ** -482, 2.0 ** 510, 2.0 ** 592, 2.0 ** -514, 2.0 ** -592, 2.0 ** 514])
+    devs = np.array([0], dtype=np.int32)
+    assert L.fn_host_run_multi(1, 3, 1, x.ctypes.data, 4, h.ctypes.data, b.ctypes.data, None,
+                               ka.ctypes.data, None, 0) == -1
+    assert L.fn_host_run_multi(1, 3, 1, x.ctypes.data, 0, h.ctypes.data, b.ctypes.data, None,
+                               ka.ctypes.data, devs.ctypes.data, 1) == 0

@@ -240,3 +240,19 @@ def test_reference_regimes(cuda_dev, regime, prec):
             torch.cuda.synchronize()
             bad, first = compare_chunked(op, x, res.head, res.body, res.sq, ka if takes else None)
             assert bad == 0, (regime, fam, prec, dim, bad, first)
+
+
+def test_host_run_multi_device_sharding(cuda_dev):
+    """fn_host_run_multi: shards over a device list (here device 0 three times, three
+    host threads) give the same bits as the single-device host path."""
+    from paper_1606_06508_b200.multigpu import host_devices
+
+    p = fn.preset("double")
+    x = _random_rows(300_001, 3, False, seed=77)
+    ref = fn.normalize3(p, x)
+    with host_devices([0, 0, 0]):
+        got = fn.normalize3(p, x)
+        q = fn.quotient2(x[:, :2].copy())
+    assert oracle.same(got.length, ref.length).all() and oracle.same(got.unit, ref.unit).all()
+    qr = fn.quotient2(x[:, :2].copy())
+    assert oracle.same(q.unit, qr.unit).all()
