@@ -189,6 +189,27 @@ int main(int argc, char** argv) {
         vs.push_back(V("quotient3_fast_f32", 4, float, 3, FN_OP_QUOTIENT3_FAST, 512, 4, 256, 0, 4));
         vs.push_back(V("naive3_f32", 4, float, 3, FN_OP_NAIVE, 512, 4, 256, 0, 4));
     }
+    if (which == "all" || which == "norm") {
+        vs.push_back(V("norm3_f64", 5, double, 3, FN_OP_NORM, 256, 4, 256, 0, 2));
+        vs.push_back(V("norm3_f64", 5, double, 3, FN_OP_NORM, 256, 4, 256, 0, 3));
+        vs.push_back(V("norm3_f64", 5, double, 3, FN_OP_NORM, 256, 4, 256, 0, 4));
+        vs.push_back(V("norm3_f64", 5, double, 3, FN_OP_NORM, 256, 6, 256, 0, 2));
+        vs.push_back(V("norm3_f64", 5, double, 3, FN_OP_NORM, 512, 4, 256, 0, 2));
+        vs.push_back(V("norm3_f64", 5, double, 3, FN_OP_NORM, 512, 3, 512, 0, 2));
+        vs.push_back(V("norm3_f64", 5, double, 3, FN_OP_NORM, 256, 8, 256, 0, 2));
+        vs.push_back(V("norm2_f64", 2, double, 2, FN_OP_NORM, 512, 4, 256, 0, 2));
+        vs.push_back(V("norm2_f64", 2, double, 2, FN_OP_NORM, 512, 4, 256, 0, 3));
+        vs.push_back(V("norm4_f64", 3, double, 4, FN_OP_NORM, 256, 3, 256, 0, 2));
+        vs.push_back(V("norm4_f64", 3, double, 4, FN_OP_NORM, 256, 4, 256, 0, 3));
+        vs.push_back(V("normalize4_f64", 3, double, 4, FN_OP_NORMALIZE, 256, 3, 256, 0, 2));
+        vs.push_back(V("normalize4_f64", 3, double, 4, FN_OP_NORMALIZE, 128, 4, 128, 0, 4));
+        vs.push_back(V("normalize4_f64", 3, double, 4, FN_OP_NORMALIZE, 256, 2, 256, 0, 3));
+        vs.push_back(V("normalize3_f32", 4, float, 3, FN_OP_NORMALIZE, 512, 4, 256, 0, 2));
+        vs.push_back(V("normalize2_f32", 4, float, 2, FN_OP_NORMALIZE, 512, 4, 256, 0, 2));
+        vs.push_back(V("normalize2_f32", 4, float, 2, FN_OP_NORMALIZE, 1024, 4, 256, 0, 2));
+        vs.push_back(V("normalize4_f32", 4, float, 4, FN_OP_NORMALIZE, 512, 3, 256, 0, 2));
+        vs.push_back(V("normalize4_f32", 4, float, 4, FN_OP_NORMALIZE, 256, 4, 256, 0, 2));
+    }
     if (which == "all" || which == "rot") {
         vs.push_back(V("rotation_unit_f64", 3, double, 4, FN_OP_ROT_UNIT, 256, 3, 256, 0, 2));
         vs.push_back(V("rotation_general_f64", 3, double, 4, FN_OP_ROT_GENERAL, 256, 3, 256, 0, 2));
