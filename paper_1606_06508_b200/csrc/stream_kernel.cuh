@@ -242,17 +242,23 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
 // 2 CTAs x 4 stages x 6 KiB reaches the cudaMemcpy bandwidth.  L2 policy hints measured
 // neutral (within noise) -> off.  The division-bound comparison variants (naive,
 // quotient) are FP64-issue bound instead and prefer full occupancy (kCtasPerSm below).
+constexpr int pow2_floor(int v) { return v >= 2 ? 2 * pow2_floor(v / 2) : 1; }
+
 template <typename T, int N> struct Tile {
-    static constexpr int kRows = (N * (int)sizeof(T) <= 16) ? 512 : 256;
+    // largest power of two with at most 8 KiB of input per stage
+    static constexpr int kRows = pow2_floor(8192 / (N * (int)sizeof(T)));
     static constexpr int kStageBytes = kRows * N * (int)sizeof(T);
     static constexpr int kStages = kStageBytes <= 6144 ? 4 : 3;
     static constexpr int kThreads = 256;
     static constexpr int kHints = 0;
 };
 
+// norm writes 8 B per row against 16-32 B read: read-dominated traffic wants more
+// loads in flight (4 CTAs: 7090 vs 5963 GB/s at 2, profiles/r01i_tune_norm.csv).
 template <int OP> struct CtasPerSm {
     static constexpr int value =
-        (OP == FN_OP_NAIVE || OP == FN_OP_QUOTIENT || OP == FN_OP_QUOTIENT3_FAST) ? 8 : 2;
+        (OP == FN_OP_NAIVE || OP == FN_OP_QUOTIENT || OP == FN_OP_QUOTIENT3_FAST) ? 8
+        : (OP == FN_OP_NORM ? 4 : 2);
 };
 
 template <typename T, int N, int OP, int TR_, int S_> struct TileLayout {
