@@ -248,7 +248,9 @@ template <typename T, int N> struct Tile {
     // largest power of two with at most 8 KiB of input per stage
     static constexpr int kRows = pow2_floor(8192 / (N * (int)sizeof(T)));
     static constexpr int kStageBytes = kRows * N * (int)sizeof(T);
-    static constexpr int kStages = kStageBytes <= 6144 ? 4 : 3;
+    // measured (profiles/r01j_tune_all.csv): 4 stages for n = 2, 3; 3 for quaternions,
+    // whose wider output staging already keeps more bytes in flight per CTA.
+    static constexpr int kStages = N == 4 ? 3 : 4;
     static constexpr int kThreads = 256;
     static constexpr int kHints = 0;
 };
