@@ -114,6 +114,21 @@ static bool force_direct() {
     return g_force_direct == 1;
 }
 
+// CTAs per SM: the measured streaming optimum (CtasPerSm), overridable for experiments
+// with FASTNORM_B200_CTAS_PER_SM; small batches (few tiles per CTA) fill the machine
+// with the occupancy maximum instead, to shorten the pipeline fill / drain.
+static int g_cps_override = -2;
+template <int OP>
+static int ctas_per_sm_for(int64_t ntiles, int sms) {
+    if (g_cps_override == -2) {
+        const char* e = getenv("FASTNORM_B200_CTAS_PER_SM");
+        g_cps_override = e ? atoi(e) : -1;
+    }
+    if (g_cps_override > 0) return g_cps_override;
+    const int64_t tiles_per_cta = ntiles / ((int64_t)CtasPerSm<OP>::value * sms);
+    return tiles_per_cta < 32 ? 64 : CtasPerSm<OP>::value;
+}
+
 template <typename T, int N, int OP>
 static int launch(const void* xv, int64_t n, void* hv, void* bv, void* qv, const KArgs<T>& ka,
                   cudaStream_t stream) {
@@ -133,7 +148,7 @@ static int launch(const void* xv, int64_t n, void* hv, void* bv, void* qv, const
                          (Op::W2 == 0 || aligned16(extra));
     if (aligned && !force_direct() && n >= (int64_t)L::TR) {
         const int64_t ntiles = n / L::TR;
-        const int64_t per_sm = std::min<int64_t>(TL::blocks_per_sm(dev), CtasPerSm<OP>::value);
+        const int64_t per_sm = std::min<int64_t>(TL::blocks_per_sm(dev), ctas_per_sm_for<OP>(ntiles, sms));
         const int64_t resident = per_sm * sms;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, resident));
         tma_stream_kernel<T, N, OP>

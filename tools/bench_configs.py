@@ -2,7 +2,7 @@
 
 For each config: generate the rows in HBM, run the config's kernel families through the
 public batched API, time every launch with CUDA events on the launching stream (L2
-flushed before each timed launch by writing a 512 MiB buffer, so even the 56 MB config-1
+flushed before each timed launch by reading a 512 MiB buffer, so even the 56 MB config-1
 batch is read from HBM), and report vectors/s, GB/s and the fraction of the measured
 copy peak.  Config 1 additionally reports CUDA-graph replay (launch overhead removed)
 and the L2-resident rate (no flush; informational only).
@@ -52,7 +52,10 @@ def timed(fnc, reps, flush):
     s = torch.cuda.current_stream()
     for _ in range(reps):
         if flush is not None:
-            flush.fill_(1)  # evicts L2 and keeps the GPU busy while the host enqueues
+            # read (not write) 512 MiB: evicts the batch from L2 with clean lines, so no
+            # write-back of flush data competes with the timed kernel; it also keeps the
+            # GPU busy while the host enqueues the timed launch
+            flush.sum(dtype=torch.int32)
         else:
             torch.cuda._sleep(400_000)  # ~0.2 ms of GPU work hides the host enqueue latency
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
