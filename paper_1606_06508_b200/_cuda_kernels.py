@@ -18,6 +18,7 @@ computes on the GPU through the C ABI:
 from __future__ import annotations
 
 import functools
+import inspect
 
 import numpy as np
 
@@ -105,6 +106,10 @@ def _make_scalar(base: str, suffix: str):
         return tuple(vals)
 
     kernel.__name__ = f"{base}_{suffix}"
+    names = (["tau_min", "tau_max", "sigma_min", "sigma_max", "inv_min", "inv_max"] if takes_ka else []) + \
+        [f"x{k + 1}" for k in range(dim)]
+    kernel.__signature__ = inspect.Signature(
+        [inspect.Parameter(nm, inspect.Parameter.POSITIONAL_OR_KEYWORD) for nm in names])
     return kernel
 
 
