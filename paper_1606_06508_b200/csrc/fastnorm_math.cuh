@@ -174,6 +174,10 @@ struct MarksteinDivider {
 #endif
 
 #if !FNB_F64_DIV_MARKSTEIN
+// Plain IEEE division per numerator.  Measured alternatives (profiles/r01d_div_*.csv,
+// r01l_div_zero_shortcut.csv): the Markstein shared reciprocal, and skipping the
+// division for provably-zero quotients, both lose 5-30 % on unit-range rows (configs
+// 1, 3) for at most +9 % on wide-range rows (config 2).
 template <> struct Divider<double> {
     double b;
     __device__ __forceinline__ explicit Divider(double b_) : b(b_) {}
