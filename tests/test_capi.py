@@ -118,3 +118,24 @@ def test_host_run_multi_argument_errors():
                                ka.ctypes.data, None, 0) == -1
     assert L.fn_host_run_multi(1, 3, 1, x.ctypes.data, 0, h.ctypes.data, b.ctypes.data, None,
                                ka.ctypes.data, devs.ctypes.data, 1) == 0
+
+
+def test_c_example_builds():
+    """A plain C program compiles and links against the C ABI (examples/normalize_host.c)."""
+    import subprocess
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run(["make", "-s", "-B", "-C", os.path.join(repo, "examples")], check=True)
+    assert os.path.exists(os.path.join(repo, "examples", "normalize_host"))
+
+
+@pytest.mark.gpu
+def test_c_example_runs():
+    import subprocess
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run(["make", "-s", "-C", os.path.join(repo, "examples")], check=True)
+    out = subprocess.run([os.path.join(repo, "examples", "normalize_host"), "1000000"],
+                         capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "r = 1.2203" in out.stdout or "r = " in out.stdout
