@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <condition_variable>
 #include <mutex>
 #include <thread>
 #include <string>
@@ -282,10 +283,101 @@ struct Staging {
     static constexpr int kMaxPipes = 8;
     int pipes = 3;
     cudaStream_t streams[kMaxPipes] = {};
-    void* buf[kMaxPipes] = {};
-    size_t bytes = 0;
+    cudaEvent_t done[kMaxPipes] = {};
+    void* buf[kMaxPipes] = {};   // device staging
+    void* hbuf[kMaxPipes] = {};  // page-locked host staging (pageable callers only)
+    size_t bytes = 0, hbytes = 0;
     bool init = false;
 };
+
+// ---------------------------------------------------------------------------------
+// Parallel host memcpy for pageable callers: a small persistent worker pool copies the
+// slices of one job; jobs are serialised (host memory bandwidth is shared anyway).
+// FASTNORM_B200_COPY_THREADS (default min(16, 3/4 of the cores): 0.26 -> 0.68 Gvec/s for
+// pageable 3-D f64 rows on the 16-core B200 host, profiles/r01n_pageable.txt).
+// ---------------------------------------------------------------------------------
+class CopyPool {
+  public:
+    CopyPool() {
+        const int hw = (int)std::thread::hardware_concurrency();
+        const char* e = getenv("FASTNORM_B200_COPY_THREADS");
+        nthreads_ = e ? std::max(1, atoi(e)) : std::max(1, std::min(16, hw * 3 / 4));
+        for (int k = 1; k < nthreads_; ++k) workers_.emplace_back([this, k] { work(k); });
+    }
+    ~CopyPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : workers_) t.join();
+    }
+    void copy(void* dst, const void* src, size_t bytes) {
+        if (bytes < ((size_t)4 << 20) || nthreads_ == 1) {
+            memcpy(dst, src, bytes);
+            return;
+        }
+        std::lock_guard<std::mutex> job(job_mu_);
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            dst_ = static_cast<char*>(dst);
+            src_ = static_cast<const char*>(src);
+            bytes_ = bytes;
+            pending_ = nthreads_ - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        slice(0);
+        std::unique_lock<std::mutex> lk(mu_);
+        done_cv_.wait(lk, [this] { return pending_ == 0; });
+    }
+
+  private:
+    void slice(int k) {
+        const size_t per = (bytes_ / nthreads_ + 63) & ~(size_t)63;
+        const size_t lo = std::min(bytes_, per * k), hi = std::min(bytes_, per * (k + 1));
+        if (hi > lo) memcpy(dst_ + lo, src_ + lo, hi - lo);
+    }
+    void work(int k) {
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+            }
+            slice(k);
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--pending_ == 0) done_cv_.notify_one();
+        }
+    }
+    int nthreads_ = 1;
+    std::vector<std::thread> workers_;
+    std::mutex mu_, job_mu_;
+    std::condition_variable cv_, done_cv_;
+    char* dst_ = nullptr;
+    const char* src_ = nullptr;
+    size_t bytes_ = 0;
+    int pending_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+
+static CopyPool& copy_pool() {
+    static CopyPool pool;
+    return pool;
+}
+
+static bool is_page_locked(const void* p) {
+    if (!p) return true;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
 
 // Host-path pipeline shape: FASTNORM_B200_HOST_PIPES (2..8, default 3) streams and
 // FASTNORM_B200_HOST_CHUNK_MB (default 48) MiB of input per chunk.
@@ -323,6 +415,8 @@ static int staging_get(int dev, size_t bytes_per_pipe, Staging** out) {
         for (int p = 0; p < st.pipes; ++p) {
             e = cudaStreamCreateWithFlags(&st.streams[p], cudaStreamNonBlocking);
             if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
+            e = cudaEventCreateWithFlags(&st.done[p], cudaEventDisableTiming);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
         }
         st.init = true;
     }
@@ -344,6 +438,24 @@ static int staging_get(int dev, size_t bytes_per_pipe, Staging** out) {
 
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
+// Page-locked host staging of bytes_per_pipe per pipe (caller holds device_mutex(dev)).
+static int host_staging_get(Staging* st, size_t bytes_per_pipe) {
+    if (st->hbytes >= bytes_per_pipe) return FN_OK;
+    for (int p = 0; p < st->pipes; ++p) {
+        if (st->hbuf[p]) cudaFreeHost(st->hbuf[p]);
+        st->hbuf[p] = nullptr;
+    }
+    st->hbytes = 0;
+    for (int p = 0; p < st->pipes; ++p) {
+        if (cudaHostAlloc(&st->hbuf[p], bytes_per_pipe, cudaHostAllocDefault) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(FN_ENOMEM, "cudaHostAlloc staging buffer failed");
+        }
+    }
+    st->hbytes = bytes_per_pipe;
+    return FN_OK;
+}
+
 int host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* body,
              void* sq, const double* ka) {
     int rc = check_args(op, dim, dtype, x, n, head, body, sq);
@@ -363,30 +475,70 @@ int host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, v
     Staging* st = nullptr;
     rc = staging_get(dev, bx + b0 + b1 + b2, &st);
     if (rc != FN_OK) return rc;
+    // Pageable caller memory cannot be DMA'd asynchronously: such sides go through
+    // page-locked staging filled / drained by the parallel host copier, overlapped with
+    // the transfers and kernels of the other pipes.
+    const bool stage_in = !is_page_locked(x);
+    const bool stage_out = !is_page_locked(head) || (wd.w1 && !is_page_locked(body)) ||
+                           (wd.w2 && !is_page_locked(sq));
+    if (stage_in || stage_out) {
+        rc = host_staging_get(st, bx + b0 + b1 + b2);
+        if (rc != FN_OK) return rc;
+    }
+    struct Pending {
+        bool live = false;
+        int64_t r0 = 0, m = 0;
+    } pending[Staging::kMaxPipes];
+    char* const outs[3] = {static_cast<char*>(head), static_cast<char*>(body), static_cast<char*>(sq)};
+    const int ws[3] = {wd.w0, wd.w1, wd.w2};
+    const size_t offs[3] = {bx, bx + b0, bx + b0 + b1};
+    auto drain = [&](int p) -> int {
+        if (!pending[p].live) return FN_OK;
+        cudaError_t ee = cudaEventSynchronize(st->done[p]);
+        if (ee != cudaSuccess) return cuda_fail(ee, "cudaEventSynchronize");
+        if (stage_out) {
+            const char* hb = static_cast<const char*>(st->hbuf[p]);
+            for (int k = 0; k < 3; ++k)
+                if (ws[k])
+                    copy_pool().copy(outs[k] + pending[p].r0 * ws[k] * w, hb + offs[k],
+                                     pending[p].m * ws[k] * w);
+        }
+        pending[p].live = false;
+        return FN_OK;
+    };
     int64_t chunk = 0;
     for (int64_t r0 = 0; r0 < n; r0 += rows, ++chunk) {
         const int p = (int)(chunk % st->pipes);
         const int64_t m = std::min<int64_t>(rows, n - r0);
         cudaStream_t s = st->streams[p];
-        char* base = static_cast<char*>(st->buf[p]);
-        void* dx = base;
-        void* d0 = base + bx;
-        void* d1 = wd.w1 ? base + bx + b0 : nullptr;
-        void* d2 = wd.w2 ? base + bx + b0 + b1 : nullptr;
-        e = cudaMemcpyAsync(dx, static_cast<const char*>(x) + r0 * dim * w, m * dim * w,
-                            cudaMemcpyHostToDevice, s);
-        if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync H2D");
-        rc = run(op, dim, dtype, dx, m, d0, d1, d2, ka, s);
+        rc = drain(p);  // staging of pipe p is free again (its previous chunk completed)
         if (rc != FN_OK) return rc;
-        e = cudaMemcpyAsync(static_cast<char*>(head) + r0 * wd.w0 * w, d0, m * wd.w0 * w,
-                            cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess && wd.w1)
-            e = cudaMemcpyAsync(static_cast<char*>(body) + r0 * wd.w1 * w, d1, m * wd.w1 * w,
-                                cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess && wd.w2)
-            e = cudaMemcpyAsync(static_cast<char*>(sq) + r0 * wd.w2 * w, d2, m * wd.w2 * w,
-                                cudaMemcpyDeviceToHost, s);
+        char* base = static_cast<char*>(st->buf[p]);
+        char* hbase = static_cast<char*>(st->hbuf[p]);
+        void* dx = base;
+        void* dptr[3] = {base + offs[0], wd.w1 ? base + offs[1] : nullptr, wd.w2 ? base + offs[2] : nullptr};
+        const char* src = static_cast<const char*>(x) + r0 * dim * w;
+        if (stage_in) {
+            copy_pool().copy(hbase, src, m * dim * w);
+            src = hbase;
+        }
+        e = cudaMemcpyAsync(dx, src, m * dim * w, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync H2D");
+        rc = run(op, dim, dtype, dx, m, dptr[0], dptr[1], dptr[2], ka, s);
+        if (rc != FN_OK) return rc;
+        for (int k = 0; k < 3 && e == cudaSuccess; ++k) {
+            if (!ws[k]) continue;
+            char* dst = stage_out ? hbase + offs[k] : outs[k] + r0 * ws[k] * w;
+            e = cudaMemcpyAsync(dst, dptr[k], m * ws[k] * w, cudaMemcpyDeviceToHost, s);
+        }
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync D2H");
+        e = cudaEventRecord(st->done[p], s);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+        pending[p] = {true, r0, m};
+    }
+    for (int64_t c = std::max<int64_t>(0, chunk - st->pipes); c < chunk; ++c) {
+        rc = drain((int)(c % st->pipes));
+        if (rc != FN_OK) return rc;
     }
     for (int p = 0; p < st->pipes; ++p) {
         e = cudaStreamSynchronize(st->streams[p]);

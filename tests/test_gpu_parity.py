@@ -256,3 +256,18 @@ def test_host_run_multi_device_sharding(cuda_dev):
     assert oracle.same(got.length, ref.length).all() and oracle.same(got.unit, ref.unit).all()
     qr = fn.quotient2(x[:, :2].copy())
     assert oracle.same(q.unit, qr.unit).all()
+
+
+@pytest.mark.parametrize("x_pinned,out_pinned", [(False, False), (True, False), (False, True), (True, True)])
+def test_host_path_pageable_and_pinned(cuda_dev, x_pinned, out_pinned):
+    """Host path across several 48 MiB chunks with every pinned / pageable combination
+    (pageable sides go through the page-locked staging + parallel copier)."""
+    p = fn.preset("double")
+    n = 5_000_003  # 120 MB of input -> 3 chunks, ragged last chunk
+    xn = _random_rows(n, 3, False, seed=123)
+    x = torch.from_numpy(xn).pin_memory().numpy() if x_pinned else xn
+    r = torch.empty(n, dtype=torch.float64, pin_memory=out_pinned).numpy()
+    u = torch.empty((n, 3), dtype=torch.float64, pin_memory=out_pinned).numpy()
+    fn.normalize3(p, x, out=(r, u))
+    h, b, _ = oracle.run(_lib.OP_NORMALIZE, xn, np.array(fn.kernel_args(p)), threads=8)
+    assert oracle.same(r, h).all() and oracle.same(u, b).all()

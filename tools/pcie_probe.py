@@ -57,5 +57,25 @@ def main():
           f"pipes={os.environ.get('FASTNORM_B200_HOST_PIPES', 'default')})")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--pageable" not in sys.argv:
     main()
+
+
+def pageable():
+    """The host path with ordinary (pageable) numpy arrays, as most callers pass them."""
+    import numpy as np
+
+    import paper_1606_06508_b200 as fn
+    p = fn.preset("double")
+    rows = 1 << 27
+    x = np.random.default_rng(0).uniform(-1, 1, (rows, 3))
+    r = np.empty(rows)
+    u = np.empty((rows, 3))
+    fn.normalize3(p, x[:1000], out=(r[:1000], u[:1000]))
+    t = timed(lambda: fn.normalize3(p, x, out=(r, u)))
+    print(f"fn_host_run normalize3 f64 2^27 rows PAGEABLE: {rows / t / 1e9:.3f} Gvec/s "
+          f"({rows * 56 / t / 1e9:.1f} GB/s over PCIe)")
+
+
+if __name__ == "__main__" and "--pageable" in sys.argv:
+    pageable()
