@@ -337,8 +337,7 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
         T* t0 = reinterpret_cast<T*>(s_out + ob * L::kOutBytes);
         T* t1 = t0 + TR * W0;
         T* t2 = t1 + TR * W1;
-#pragma unroll
-        for (int j = threadIdx.x; j < TR; j += NT) {
+        auto row = [&](int j) {
             T xr[N], o0[Slot<W0>::value], o1[Slot<W1>::value], o2[Slot<W2>::value];
 #pragma unroll
             for (int c = 0; c < N; ++c) xr[c] = tin[j * N + c];
@@ -349,6 +348,13 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
             for (int c = 0; c < W1; ++c) t1[j * W1 + c] = o1[c];
 #pragma unroll
             for (int c = 0; c < W2; ++c) t2[j * W2 + c] = o2[c];
+        };
+        if constexpr (TR >= NT) {
+            static_assert(TR % NT == 0, "a tile is a whole number of rows per thread");
+#pragma unroll
+            for (int it = 0; it < TR / NT; ++it) row((int)threadIdx.x + it * NT);  // no guard
+        } else {
+            if ((int)threadIdx.x < TR) row((int)threadIdx.x);
         }
         fence_proxy_async_smem();  // generic-proxy smem traffic -> visible to bulk copies
         __syncthreads();
