@@ -74,6 +74,15 @@ __global__ void selftest_f64(uint64_t seed, int64_t n, unsigned long long* out) 
                 const double fa = fabs(a), fb = fabs(b);
                 if (fa > fb) { const double t = a; a = b; b = t; }
             }
+        } else if (cat == 14 && ((w3 >> 24) & 1)) {  // quotients at / next to subnormal midpoints
+            // a / b ~= (2k+1) 2^-1075, a half-integer multiple of the least subnormal
+            const double m_odd = (double)(2 * ((w0 >> 20) % (1ull << 40)) + 1);
+            b = __longlong_as_double((long long)(((uint64_t)(1123 + (w2 >> 59)) << 52) |
+                                                 (w2 & 0x000FFFFFFFFFFFFFull)));  // ~2^100..2^131
+            a = __dmul_rn(__dmul_rn(__dmul_rn(m_odd, b), 0x1p-600), 0x1p-475);     // normal, exact scalings
+            const int nudge = (int)((w3 >> 26) % 3) - 1;
+            a = __longlong_as_double(__double_as_longlong(a) + nudge);
+            if ((w3 >> 28) & 1) a = -a;
         } else if (cat < 14) {  // exponent difference pinned near the path boundaries
             const int targets[8] = {-1078, -1076, -1075, -1074, -1023, -968, -967, 1021};
             const int d = targets[(w3 >> 8) % 8] + (int)((w3 >> 16) % 5) - 2;
@@ -89,10 +98,13 @@ __global__ void selftest_f64(uint64_t seed, int64_t n, unsigned long long* out) 
             a = (w3 >> 8) & 1 ? special_f64(w0) : __longlong_as_double((long long)make_f64(w0, w1, 0));
             b = (w3 >> 9) & 1 ? special_f64(w2) : __longlong_as_double((long long)make_f64(w2, w1, 0));
         }
-        const double got = fnb::MarksteinDivider(b)(a);
         const double want = __ddiv_rn(a, b);
-        const bool ok = (__double_as_longlong(got) == __double_as_longlong(want)) ||
-                        (isnan(got) && isnan(want));
+        const double got = fnb::MarksteinDivider(b)(a);
+        const double got2 = fnb::Divider<double>(b)(a);  // tiny-result path of the kernels
+        const bool ok = ((__double_as_longlong(got) == __double_as_longlong(want)) ||
+                         (isnan(got) && isnan(want))) &&
+                        ((__double_as_longlong(got2) == __double_as_longlong(want)) ||
+                         (isnan(got2) && isnan(want)));
         if (!ok) {
             ++bad;
             if (atomicCAS(out + 1, 0ull, (unsigned long long)__double_as_longlong(a)) == 0ull)
