@@ -174,46 +174,17 @@ struct MarksteinDivider {
 #endif
 
 #if !FNB_F64_DIV_MARKSTEIN
-// Quotients that round into the subnormal range (or to zero) are exactly where the
-// library division __ddiv_rn leaves its fast path, and wide-range rows (configs 2, 5)
-// hit that case in most warps.  div_tiny_result() computes them directly: the
-// numerator is scaled by 2^600 (exact), divided on the fast path (normal result),
-// and the scaled quotient q rounded once onto the subnormal grid by the multiply with
-// 2^-600.  That second rounding can differ from a single rounding of the exact
-// quotient only when q sits exactly on a grid midpoint while q != a/b; the exact
-// remainder r = a' - b q (one fma, exact since q is correctly rounded and a' >= 2^-474)
-// tells on which side the exact quotient lies and the result moves one grid step.
-// A quotient provably below 2^-1075 (or a zero numerator) is the signed zero.
-// Kept out of line so the common path keeps its registers.
-static __device__ __noinline__ double div_tiny_result(double a, double b) {
-    const int ea = biased_exp(a), eb = biased_exp(b);
-    if (a == 0.0 || (ea >= 1 && ea - eb <= -1076) || (ea == 0 && eb >= 1076))
-        return signed_zero_of_quotient(a, b);
-    const double as = __dmul_rn(a, 0x1p600);          // exact: only scales up
-    const double q = __ddiv_rn(as, b);                  // normal, in [2^-476, 2^-420]
-    const double r = __fma_rn(-b, q, as);               // exact remainder
-    double t = __dmul_rn(q, 0x1p-600);                  // one rounding onto the 2^-1074 grid
-    const double d = __dadd_rn(q, -__dmul_rn(t, 0x1p600));  // q - t*2^600, exact
-    if (fabs(d) == 0x1p-475 && r != 0.0 &&
-        (signbit(r) != signbit(b)) == signbit(d))       // exact quotient beyond the midpoint
-        t = __dadd_rn(t, copysign(0x1p-1074, d));
-    return t;
-}
-
+// Plain IEEE division per numerator (__ddiv_rn).  Measured alternatives, all exact and
+// checked by fn_selftest_div, all slower on unit-range rows (configs 1, 3):
+//   * Markstein shared reciprocal (MarksteinDivider below): profiles/r01d_div_*.csv;
+//   * skipping provably-zero quotients in a branch: profiles/r01l_div_zero_shortcut.csv;
+//   * branch-free tiny-result path (numerator scaled by 2^600, one rounding onto the
+//     subnormal grid, midpoint fix from the exact remainder): +20 % on config 2 and +6 %
+//     on config 5 quotient rows, but -40 % on configs 1 and 3 (profiles/r01s_div.csv).
 template <> struct Divider<double> {
     double b;
-    int eb;
-    bool bnormal;
-    __device__ __forceinline__ explicit Divider(double b_) : b(b_) {
-        eb = biased_exp(b_);
-        bnormal = eb >= 1 && eb <= 2046;
-    }
-    __device__ __forceinline__ double operator()(double a) const {
-        const int ea = biased_exp(a);
-        // |a/b| < 2^(ea - eb + 1): below 2^-1021 the result may be subnormal or zero
-        if (bnormal && ea <= 2046 && ea - eb <= -1022) return div_tiny_result(a, b);
-        return __ddiv_rn(a, b);
-    }
+    __device__ __forceinline__ explicit Divider(double b_) : b(b_) {}
+    __device__ __forceinline__ double operator()(double a) const { return __ddiv_rn(a, b); }
 };
 #else
 template <> struct Divider<double> : MarksteinDivider {
