@@ -105,27 +105,32 @@ template <typename T, int N, int OP> struct TmaLaunch {
 
 static inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
-static int g_force_direct = -1;  // FASTNORM_B200_PATH=direct forces the per-row kernel
-
+// Launch-shape overrides read once from the environment (function-local statics:
+// thread-safe initialisation):
+//   FASTNORM_B200_PATH=direct       force the per-row kernel (diagnostics)
+//   FASTNORM_B200_CTAS_PER_SM=<k>   CTAs per SM for the streaming kernel (experiments)
 static bool force_direct() {
-    if (g_force_direct < 0) {
+    static const bool v = [] {
         const char* e = getenv("FASTNORM_B200_PATH");
-        g_force_direct = (e && strcmp(e, "direct") == 0) ? 1 : 0;
-    }
-    return g_force_direct == 1;
+        return e && strcmp(e, "direct") == 0;
+    }();
+    return v;
 }
 
-// CTAs per SM: the measured streaming optimum (CtasPerSm), overridable for experiments
-// with FASTNORM_B200_CTAS_PER_SM; small batches (few tiles per CTA) fill the machine
-// with the occupancy maximum instead, to shorten the pipeline fill / drain.
-static int g_cps_override = -2;
+static int cps_override() {
+    static const int v = [] {
+        const char* e = getenv("FASTNORM_B200_CTAS_PER_SM");
+        return e ? atoi(e) : -1;
+    }();
+    return v;
+}
+
+// CTAs per SM: the measured streaming optimum (CtasPerSm); small batches (few tiles per
+// CTA) fill the machine with the occupancy maximum instead, to shorten the pipeline
+// fill / drain.
 template <int OP>
 static int ctas_per_sm_for(int64_t ntiles, int sms) {
-    if (g_cps_override == -2) {
-        const char* e = getenv("FASTNORM_B200_CTAS_PER_SM");
-        g_cps_override = e ? atoi(e) : -1;
-    }
-    if (g_cps_override > 0) return g_cps_override;
+    if (cps_override() > 0) return cps_override();
     const int64_t tiles_per_cta = ntiles / ((int64_t)CtasPerSm<OP>::value * sms);
     return tiles_per_cta < 32 ? 64 : CtasPerSm<OP>::value;
 }

@@ -22,7 +22,8 @@ def main():
     ap.add_argument("--log2-rows", type=int, default=26)
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--op", default="normalize",
-                    choices=["normalize", "normalize_sq", "norm", "quotient", "quotient3_fast", "naive", "scale"])
+                    choices=["normalize", "normalize_sq", "norm", "quotient", "quotient3_fast", "naive", "scale",
+                             "normalize4_rotation"])
     a = ap.parse_args()
     c = workloads.CONFIGS[a.cfg]
     dt = torch.float64 if c.dtype == "float64" else torch.float32
@@ -42,6 +43,8 @@ def main():
             getattr(fn, f"scale{d}")(p, x)
         elif a.op == "quotient":
             {2: fn.quotient2, 3: fn.quotient3_robust, 4: fn.quotient4}[d](x)
+        elif a.op == "normalize4_rotation":
+            fn.normalize4_rotation(p, x)
         elif a.op == "quotient3_fast":
             fn.quotient3_fast(x)
         else:
