@@ -187,6 +187,23 @@ static int make_kargs(const double* ka, bool needed, KArgs<T>& out) {
         return fail(FN_EINVAL, "tau_min/tau_max must be non-negative and not NaN");
     memcpy(&out.tau_min_bits, &out.tau_min, sizeof(T));
     memcpy(&out.tau_max_bits, &out.tau_max, sizeof(T));
+    // Exponent insertion needs sigma = 2^k and inv = 2^-k exactly (validate_conditions
+    // requires powers of two, and kernel_args passes exact inverses); otherwise the
+    // kernels multiply, as the reference does for any parameter set.
+    auto log2_exact = [](T v, int* k) {
+        if (!(v > (T)0) || !std::isfinite(v)) return false;
+        int e = 0;
+        const T f = std::frexp(v, &e);
+        *k = e - 1;
+        return f == (T)0.5;
+    };
+    int kmin = 0, kmax = 0, kimin = 0, kimax = 0;
+    out.pow2 = log2_exact(out.sigma_min, &kmin) && log2_exact(out.sigma_max, &kmax) &&
+               log2_exact(out.inv_min, &kimin) && log2_exact(out.inv_max, &kimax) &&
+               kimin == -kmin && kimax == -kmax && out.inv_min != out.inv_max &&
+               out.inv_min != (T)1 && out.inv_max != (T)1;
+    out.k_min = out.pow2 ? kmin : 0;
+    out.k_max = out.pow2 ? kmax : 0;
     return FN_OK;
 }
 

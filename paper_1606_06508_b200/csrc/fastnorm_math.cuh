@@ -44,6 +44,11 @@ template <> struct Fp<double> {
         // p = 2^k (normal): k from the biased exponent field.
         return (int)((bits(p) >> 52) & 0x7ff) - 1023;
     }
+    static constexpr int kShift = 52, kExpMax = 2046;
+    __device__ __forceinline__ static double from_bits(Bits b) { return __longlong_as_double((long long)b); }
+    __device__ __forceinline__ static int biased_exponent(double x) {
+        return (int)(((unsigned)__double2hiint(x) >> 20) & 0x7ffu);
+    }
 };
 
 template <> struct Fp<float> {
@@ -62,13 +67,54 @@ template <> struct Fp<float> {
     __device__ __forceinline__ static int exponent_of_pow2(float p) {
         return (int)((bits(p) >> 23) & 0xff) - 127;
     }
+    static constexpr int kShift = 23, kExpMax = 254;
+    __device__ __forceinline__ static float from_bits(Bits b) { return __uint_as_float(b); }
+    __device__ __forceinline__ static int biased_exponent(float x) {
+        return (int)((__float_as_uint(x) >> 23) & 0xffu);
+    }
 };
+
+// Power-of-two scaling by exponent insertion: x * 2^k computed as an integer add on the
+// exponent field when both x and the result are normal -- exactly the bits of the IEEE
+// product there -- and by the IEEE multiply otherwise (zero, subnormal input or result,
+// overflow, inf, NaN), which rounds exactly as the reference's `sigma * x`.
+//
+// FNB_EXPONENT_INSERTION = 1 builds the scaling kernels with it (bit-identical: the
+// full GPU parity suite passes, profiles/r01u_insertion.txt); the default 0 multiplies
+// by the exact power of two instead, because the integer path measured 7 % slower on
+// the bench workload (9.93 vs 9.21 ms per 2^30 rows: the per-row instruction count,
+// not the FP64 pipe at 19 %, paces the tile loop).
+#ifndef FNB_EXPONENT_INSERTION
+#define FNB_EXPONENT_INSERTION 0
+#endif
+template <typename T>
+__device__ __forceinline__ bool pow2_insertable(T x, int k) {
+    const int e = Fp<T>::biased_exponent(x);
+    return e >= 1 && e <= Fp<T>::kExpMax && e + k >= 1 && e + k <= Fp<T>::kExpMax;
+}
+template <typename T>
+__device__ __forceinline__ T pow2_insert(T x, int k) {
+    using B = typename Fp<T>::Bits;
+    return Fp<T>::from_bits(Fp<T>::bits(x) + (B)((long long)k << Fp<T>::kShift));
+}
+template <typename T>
+__device__ __forceinline__ T pow2_scale(T x, int k, T factor, bool insert_ok) {
+#if FNB_EXPONENT_INSERTION
+    return (insert_ok && pow2_insertable(x, k)) ? pow2_insert(x, k) : Fp<T>::mul(factor, x);
+#else
+    (void)k;
+    (void)insert_ok;
+    return Fp<T>::mul(factor, x);  // factor = 2^k exactly: same bits as the insertion
+#endif
+}
 
 // The six kernel arguments (scale.py:26-30), already rounded to T, plus the bit
 // patterns of the two band thresholds for the integer band test.
 template <typename T> struct KArgs {
     T tau_min, tau_max, sigma_min, sigma_max, inv_min, inv_max;
     typename Fp<T>::Bits tau_min_bits, tau_max_bits;
+    int k_min, k_max;   // log2(sigma_min), log2(sigma_max) when pow2 (validated sets)
+    bool pow2;          // sigma_min, sigma_max and their inverses are powers of two
     unsigned long long* invalid;  // rows rejected by the rotations (may be NULL)
 };
 
@@ -92,9 +138,17 @@ __device__ __forceinline__ bool scale_classified(const T (&x)[N], const KArgs<T>
     const bool small = m < ka.tau_min_bits;
     const T sigma = big ? ka.sigma_max : (small ? ka.sigma_min : T(1));
     inv = big ? ka.inv_max : (small ? ka.inv_min : T(1));
+    // s_k = sigma * x_k by exponent insertion (k = log2 sigma) where exact, else IEEE mul
+    const int k = big ? ka.k_max : (small ? ka.k_min : 0);
 #pragma unroll
-    for (int k = 0; k < N; ++k) s[k] = F::mul(sigma, x[k]);  // 1*x == x bit for bit
+    for (int c = 0; c < N; ++c) s[c] = pow2_scale(x[c], k, sigma, ka.pow2);
     return m != 0;
+}
+
+template <typename T>
+__device__ __forceinline__ int inv_exponent(const KArgs<T>& ka, T inv) {
+    // inv = 2^-k of the selected branch (1, 1/sigma_max, 1/sigma_min)
+    return inv == ka.inv_max ? -ka.k_max : (inv == ka.inv_min ? -ka.k_min : 0);
 }
 
 // ---------------------------------------------------------------------------------
@@ -231,12 +285,18 @@ __device__ __forceinline__ void normalize_row(const T (&x)[N], const KArgs<T>& k
     const T ss = sum_squares<T, N>(s);
     const T rt = F::sqrt(ss);
     const T h = F::rcp(rt);
-    r = nonzero ? F::mul(inv, rt) : T(0);
+    const int ki = inv_exponent(ka, inv);
+    // r = inv * rt: exponent insertion while the length stays normal, IEEE mul otherwise
+    // (warranted overflow to inf, rounding into subnormals)
+    r = nonzero ? pow2_scale(rt, ki, inv, ka.pow2) : T(0);
 #pragma unroll
     for (int k = 0; k < N; ++k) u[k] = nonzero ? F::mul(h, s[k]) : T(0);
     if (N == 4) u[N - 1] = nonzero ? u[N - 1] : T(1);
     if (kSq) {
-        sq = nonzero ? F::ldexp_(ss, 2 * F::exponent_of_pow2(inv)) : T(0);
+        // sq = ss * inv^2 = ldexp(ss, 2 ki), one correct rounding
+        const int ks = ka.pow2 ? ki : F::exponent_of_pow2(inv);
+        const bool ins = FNB_EXPONENT_INSERTION && ka.pow2 && pow2_insertable(ss, 2 * ks);
+        sq = nonzero ? (ins ? pow2_insert(ss, 2 * ks) : F::ldexp_(ss, 2 * ks)) : T(0);
     }
 }
 
@@ -246,7 +306,7 @@ __device__ __forceinline__ T norm_row(const T (&x)[N], const KArgs<T>& ka) {
     using F = Fp<T>;
     T inv, s[N];
     const bool nonzero = scale_classified<T, N>(x, ka, inv, s);
-    const T r = F::mul(inv, F::sqrt(sum_squares<T, N>(s)));
+    const T r = pow2_scale(F::sqrt(sum_squares<T, N>(s)), inv_exponent(ka, inv), inv, ka.pow2);
     return nonzero ? r : T(0);
 }
 
