@@ -269,11 +269,14 @@ def run_ours(args):
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    # under torchrun (RANK set) the NCCL group is created even for a single rank, so the
+    # same barrier / max-reduce / counter-reduce code runs at every N
+    distributed = "RANK" in os.environ and "MASTER_ADDR" in os.environ
+    if distributed:
         dist.init_process_group("nccl", device_id=dev)
 
     def barrier():
-        if world > 1:
+        if distributed:
             dist.barrier()
 
     def max_over_ranks(v: float) -> float:
@@ -337,7 +340,7 @@ def run_ours(args):
     chunk_rows = (48 << 20) // (DIM * 8)
     e2e_launches = e2e_steps * ((n + chunk_rows - 1) // chunk_rows)
 
-    if world > 1:
+    if distributed:
         dist.destroy_process_group()
     if rank != 0:
         return 0
@@ -394,7 +397,8 @@ def run_ours(args):
         "validation": {
             "row_classes": dict(zip(multigpu.COUNTER_NAMES, counts_h)),
             "rows_counted": int(sum(counts_h)),
-            "reduce": "NCCL all_reduce(sum) of 6 counters" if world > 1 else "single rank",
+            "reduce": f"NCCL all_reduce(sum) of 6 counters over {world} rank(s)" if distributed
+                      else "single process",
         },
     }
     if world == 1 and not args.no_cpu_baseline:

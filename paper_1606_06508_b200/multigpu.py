@@ -31,11 +31,11 @@ def shard_range(n_total: int, rank: int, world: int) -> tuple[int, int]:
 
 
 def max_over_ranks(value: float, device=None) -> float:
-    """MAX of a per-rank scalar over the default process group (identity if single rank)."""
+    """MAX of a per-rank scalar over the default process group (identity without one)."""
     import torch
     import torch.distributed as dist
 
-    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+    if not (dist.is_available() and dist.is_initialized()):
         return float(value)
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -46,7 +46,7 @@ def reduce_counts(counts):
     """In-place SUM all-reduce of an int64 counter tensor; returns it as a list of ints."""
     import torch.distributed as dist
 
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+    if dist.is_available() and dist.is_initialized():
         dist.all_reduce(counts)
     return [int(v) for v in counts.cpu().tolist()]
 
