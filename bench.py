@@ -405,11 +405,12 @@ def run_ours(args):
         from paper_1606_06508_b200 import workloads as wl
 
         xs = wl.host_rows(CFG, 0, CPU_SAMPLE_ROWS)
-        rate, threads, kind, best = cpu_reference_rate(xs, ka, reps=3)
+        rate, threads, kind, best = cpu_reference_rate(xs, ka, reps=12)
         line["cpu_baseline"] = {
             "value": rate, "unit": UNIT, "cores": threads, "kind": kind,
             "sample": (f"cfg5 rows [0, {CPU_SAMPLE_ROWS}): reference loop_scaling3_f64 "
-                       f"(checksum only) on {threads} threads, best of 3 passes ({best:.3f} s)"),
+                       f"(checksum only) on {threads} threads, best of 12 passes ({best:.3f} s each; "
+                       f"~{12 * best * threads:.0f} CPU-s in total)"),
         }
     print(json.dumps(line), flush=True)
     return 0
