@@ -90,6 +90,13 @@ int fn_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, voi
            void* sq, const double* ka, void* stream);
 int fn_host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head,
                 void* body, void* sq, const double* ka);
+/* One row with the reference's scalar semantics, low latency: x[dim] as doubles (the f32
+ * families round them to binary32 like the reference's <float> casts), results written
+ * to out as doubles in the order head, body..., extra... (e.g. r, u1..un; inv, s1..sn;
+ * r, u1..un, sq).  Uses a per-thread page-locked buffer mapped into the device; one
+ * kernel launch and one stream synchronisation per call. */
+int fn_scalar(int op, int dim, int dtype, const double* x, double* out, const double* ka);
+
 /* fn_host_run over several devices of one process: rows are split into ndev contiguous
  * balanced shards, one host thread per device runs the pipelined host path on its
  * shard (no inter-device traffic; each device brings its own PCIe link). */

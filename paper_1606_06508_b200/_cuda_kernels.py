@@ -6,8 +6,9 @@ signatures (_kernels.pyx:419-634) and timing-loop signatures (:792-1008), plus
 ``BACKEND_NAME`` / ``BUILD_FLAGS`` (tests/test_backends.py:145-149).  Every one of them
 computes on the GPU through the C ABI:
 
-* scalar ``{base}_{f32,f64}(...)`` -- one row through ``fn_host_run`` (a kernel launch
-  per call: correct and drop-in, but use the batched overloads for throughput);
+* scalar ``{base}_{f32,f64}(...)`` -- one row through ``fn_scalar`` (one kernel launch
+  on a mapped page-locked row per call: correct and drop-in, but use the batched
+  overloads for throughput);
 * ``loop_*`` -- the rows the loop touches are normalised on the GPU in one launch and
   the checksum is accumulated on the host in the reference loop's exact order
   (``acc += <double>r + <double>u1 + ...``, _kernels.pyx:652-657), so it equals the
@@ -17,8 +18,10 @@ computes on the GPU through the C ABI:
 
 from __future__ import annotations
 
+import ctypes
 import functools
 import inspect
+import threading
 
 import numpy as np
 
@@ -84,26 +87,45 @@ def batch_kernel(base: str, suffix: str):
     return run
 
 
+_tls = threading.local()
+
+
+def _scalar_buffers():
+    b = getattr(_tls, "bufs", None)
+    if b is None:
+        b = _tls.bufs = ((ctypes.c_double * 8)(), (ctypes.c_double * 16)(), (ctypes.c_double * 6)())
+    return b
+
+
 def _make_scalar(base: str, suffix: str):
+    """Reference scalar signature -> fn_scalar (one launch on a mapped page-locked row)."""
     op, dim = parse_base(base)
     takes_ka = op in (_lib.OP_SCALE, _lib.OP_NORMALIZE, _lib.OP_NORMALIZE_SQ, _lib.OP_NORM)
-    dt = _np_dtype(suffix)
+    dcode = _lib.F64 if suffix == "f64" else _lib.F32
     nargs = dim + (6 if takes_ka else 0)
+    nout = sum(batch.widths(op, dim))
+    sq_first = op == _lib.OP_NORMALIZE_SQ
 
     def kernel(*args):
         if len(args) != nargs:
             raise TypeError(f"{base}_{suffix} takes {nargs} arguments ({len(args)} given)")
-        ka = _ka_array(args[:6]) if takes_ka else None
-        with np.errstate(over="ignore"):  # the reference's <float> cast overflows to inf too
-            row = np.array([args[-dim:]], dtype=np.float64).astype(dt)
-        res = batch.run(op, dim, row, ka)
-        head = float(res.head[0])
-        if res.body is None:
-            return head
-        vals = [head] + [float(v) for v in res.body[0]]
-        if res.sq is not None:
-            vals = [float(res.sq[0])] + vals
-        return tuple(vals)
+        xb, ob, kb = _scalar_buffers()
+        if takes_ka:
+            for i in range(6):
+                kb[i] = args[i]
+            for i in range(dim):
+                xb[i] = args[6 + i]
+        else:
+            for i in range(dim):
+                xb[i] = args[i]
+        rc = _lib.lib().fn_scalar(op, dim, dcode, ctypes.addressof(xb), ctypes.addressof(ob),
+                                  ctypes.addressof(kb) if takes_ka else None)
+        if rc:
+            _lib.check(rc, f"{base}_{suffix}")
+        if nout == 1:
+            return ob[0]
+        vals = ob[:nout]
+        return tuple([vals[-1]] + vals[:-1]) if sq_first else tuple(vals)
 
     kernel.__name__ = f"{base}_{suffix}"
     names = (["tau_min", "tau_max", "sigma_min", "sigma_max", "inv_min", "inv_max"] if takes_ka else []) + \

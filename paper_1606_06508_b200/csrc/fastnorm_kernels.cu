@@ -569,6 +569,66 @@ int host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, v
     return FN_OK;
 }
 
+// ---------------------------------------------------------------------------------
+// One row, low latency (the reference's scalar signatures): the row and its results
+// live in a per-thread, per-device page-locked buffer that is mapped into the device
+// address space; one direct-kernel launch reads and writes it over PCIe and one stream
+// synchronisation returns -- no staging copies, no allocation after the first call.
+// ---------------------------------------------------------------------------------
+struct ScalarCtx {
+    int dev = -1;
+    cudaStream_t stream = nullptr;
+    char* host = nullptr;   // 256 B page-locked, mapped
+    char* dptr = nullptr;   // its device alias
+};
+
+int scalar_run(int op, int dim, int dtype, const double* xin, double* out, const double* ka) {
+    static thread_local std::vector<ScalarCtx> ctxs;
+    if (!xin || !out) return fail(FN_EINVAL, "xin and out must not be NULL");
+    if (op < FN_OP_SCALE || op > FN_OP_NORMALIZE_ROT || dim < 2 || dim > 4)
+        return fail(FN_EINVAL, "unknown op or dim");
+    {
+        const Widths v = op_widths(op, dim);
+        const int rc0 = check_args(op, dim, dtype, xin, 1, out, v.w1 ? out : nullptr, v.w2 ? out : nullptr);
+        if (rc0 != FN_OK) return rc0;
+    }
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if ((int)ctxs.size() <= dev) ctxs.resize(dev + 1);
+    ScalarCtx& c = ctxs[dev];
+    if (c.dev < 0) {
+        e = cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
+        e = cudaHostAlloc(reinterpret_cast<void**>(&c.host), 256, cudaHostAllocMapped);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaHostAlloc");
+        e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c.dptr), c.host, 0);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaHostGetDevicePointer");
+        c.dev = dev;
+    }
+    const Widths wd = op_widths(op, dim);
+    const size_t w = dtype == FN_F64 ? 8 : 4;
+    // layout: x at 0, head at 64, body at 128, extra at 192 (bytes)
+    for (int k = 0; k < dim; ++k) {
+        if (dtype == FN_F64) reinterpret_cast<double*>(c.host)[k] = xin[k];
+        else reinterpret_cast<float*>(c.host)[k] = (float)xin[k];  // the reference's <float> cast
+    }
+    int rc = run(op, dim, dtype, c.dptr, 1, c.dptr + 64, wd.w1 ? c.dptr + 128 : nullptr,
+                 wd.w2 ? c.dptr + 192 : nullptr, ka, c.stream);
+    if (rc != FN_OK) return rc;
+    e = cudaStreamSynchronize(c.stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+    const int offs[3] = {64, 128, 192};
+    const int ws[3] = {wd.w0, wd.w1, wd.w2};
+    int o = 0;
+    for (int a = 0; a < 3; ++a)
+        for (int k = 0; k < ws[a]; ++k, ++o)
+            out[o] = dtype == FN_F64 ? reinterpret_cast<const double*>(c.host + offs[a])[k]
+                                     : (double)reinterpret_cast<const float*>(c.host + offs[a])[k];
+    (void)w;
+    return FN_OK;
+}
+
 // Row shards over several devices, one host thread per device, each running the
 // chunked host pipeline above on its own streams and staging buffers.  No data moves
 // between devices (rows are independent, _kernels.pyx:167-412).
@@ -638,6 +698,10 @@ int fn_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, voi
 int fn_host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* body,
                 void* sq, const double* ka) {
     return fnb::host_run(op, dim, dtype, x, n, head, body, sq, ka);
+}
+
+int fn_scalar(int op, int dim, int dtype, const double* x, double* out, const double* ka) {
+    return fnb::scalar_run(op, dim, dtype, x, out, ka);
 }
 
 int fn_host_run_multi(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* body,
