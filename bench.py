@@ -255,6 +255,59 @@ def run_reference_arm(args):
 
 
 # --------------------------------------------------------------------------------------
+# the other BASELINE configs (informational, measured after the timed region)
+# --------------------------------------------------------------------------------------
+OTHER_CONFIGS = {  # config -> [(public API call, algorithmic bytes per row)]
+    1: [("normalize3", 56)],
+    2: [("normalize2", 40), ("quotient2", 40)],
+    3: [("normalize4_sq", 80), ("normalize4_rotation", 144)],
+    4: [("normalize3", 28), ("quotient3_robust", 28)],
+}
+
+
+def measure_other_configs(dev, reps: int = 5):
+    """Each BASELINE config's kernels through the public API: rows generated in HBM, L2
+    evicted (a 512 MiB read) before every timed launch, CUDA events on the launching
+    stream, median of `reps`."""
+    import torch
+
+    import paper_1606_06508_b200 as fn
+    from paper_1606_06508_b200 import workloads
+
+    peak, _ = _peaks()
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    out = []
+    for cfg, calls in OTHER_CONFIGS.items():
+        c = workloads.CONFIGS[cfg]
+        dt = torch.float64 if c.dtype == "float64" else torch.float32
+        p = fn.preset("double" if dt == torch.float64 else "single")
+        x = torch.empty((c.rows, c.dim), dtype=dt, device=dev)
+        workloads.generate_device(cfg, x)
+        for name, bpr in calls:
+            f = getattr(fn, name)
+            call = (lambda: f(x)) if name.startswith("quotient") else (lambda: f(p, x))
+            for _ in range(3):
+                call()
+            times = []
+            for _ in range(reps):
+                flush.sum(dtype=torch.int32)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                call()
+                e1.record(stream)
+                torch.cuda.synchronize(dev)
+                times.append(e0.elapsed_time(e1) / 1e3)
+            t = statistics.median(times)
+            out.append({"config": cfg, "kernel": name, "rows": c.rows, "dtype": c.dtype,
+                        "vectors_per_s": c.rows / t, "GB_per_s": c.rows * bpr / t / 1e9,
+                        "frac": c.rows * bpr / t / 1e9 / peak, "ms": t * 1e3})
+        del x
+        torch.cuda.empty_cache()
+    return out
+
+
+# --------------------------------------------------------------------------------------
 # our arm
 # --------------------------------------------------------------------------------------
 def run_ours(args):
@@ -401,6 +454,8 @@ def run_ours(args):
                       else "single process",
         },
     }
+    if world == 1 and not args.no_configs:
+        line["other_configs"] = measure_other_configs(dev)
     if world == 1 and not args.no_cpu_baseline:
         from paper_1606_06508_b200 import workloads as wl
 
@@ -424,6 +479,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the informational per-config measurements (configs 1-4)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("note: --warmup raised to 3 (timing rule)", file=sys.stderr)

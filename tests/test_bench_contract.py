@@ -49,3 +49,5 @@ def test_our_arm_line(cuda_dev):
     assert d["value"] > 50e9 and e["value"] > 0.5e9
     assert d["validation"]["rows_counted"] == 1 << 30
     assert d["clocks"]["samples"] >= 1 and d["clocks"]["sm_max_mhz"]
+    oc = d["other_configs"]
+    assert {c["config"] for c in oc} == {1, 2, 3, 4} and all(c["frac"] > 0.2 for c in oc)
