@@ -607,7 +607,6 @@ int scalar_run(int op, int dim, int dtype, const double* xin, double* out, const
         c.dev = dev;
     }
     const Widths wd = op_widths(op, dim);
-    const size_t w = dtype == FN_F64 ? 8 : 4;
     // layout: x at 0, head at 64, body at 128, extra at 192 (bytes)
     for (int k = 0; k < dim; ++k) {
         if (dtype == FN_F64) reinterpret_cast<double*>(c.host)[k] = xin[k];
@@ -625,7 +624,6 @@ int scalar_run(int op, int dim, int dtype, const double* xin, double* out, const
         for (int k = 0; k < ws[a]; ++k, ++o)
             out[o] = dtype == FN_F64 ? reinterpret_cast<const double*>(c.host + offs[a])[k]
                                      : (double)reinterpret_cast<const float*>(c.host + offs[a])[k];
-    (void)w;
     return FN_OK;
 }
 

@@ -5,7 +5,6 @@ double metrics agree with exact rational arithmetic, and violations are detected
 import math
 from fractions import Fraction
 
-import numpy as np
 import pytest
 
 import paper_1606_06508_b200 as fn

@@ -11,7 +11,7 @@ equals the oracle (and, where built, the reference's own compiled loop).
 import numpy as np
 import pytest
 
-from gpu_helpers import THREADS, compare_chunked, to_np
+from gpu_helpers import compare_chunked, to_np
 
 import oracle
 import paper_1606_06508_b200 as fn
