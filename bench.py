@@ -395,6 +395,8 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
         e2e_rows = int(t.item())
     e2e_error = None
+    numa = multigpu.numa_local(local)  # pin + copy from the GPU's own socket
+    numa.__enter__()
     try:
         xh = torch.empty((e2e_rows, DIM), dtype=torch.float64, pin_memory=True)
         xh.copy_(x[:e2e_rows])
@@ -422,6 +424,7 @@ def run_ours(args):
         barrier()
         t_e2e = max_over_ranks(t1 - t0)
         del xh, rh, uh, xn, rn, un
+    numa.__exit__(None, None, None)
     e2e_value = e2e_rows * world * e2e_steps / t_e2e if e2e_error is None else None
     chunk_rows = (48 << 20) // (DIM * 8)
     e2e_launches = e2e_steps * ((e2e_rows + chunk_rows - 1) // chunk_rows)
@@ -481,6 +484,7 @@ def run_ours(args):
             "error": e2e_error,
             "api": "paper_1606_06508_b200.normalize3(p, pinned numpy [N,3], out=(r, unit)) -> fn_host_run",
             "gpu_launches": e2e_launches,
+            "host_cpus": "NUMA-local to the GPU" if numa.cpus else "all (topology unknown)",
         },
         "validation": {
             "row_classes": dict(zip(multigpu.COUNTER_NAMES, counts_h)),

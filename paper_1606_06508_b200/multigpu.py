@@ -60,3 +60,54 @@ def shard_counts_device(x, ka):
     counts = torch.zeros(6, dtype=torch.int64, device=x.device)
     workloads.row_stats_device(x, ka, counts.view(torch.uint64))
     return counts
+
+
+def gpu_local_cpus(device_index: int) -> set[int] | None:
+    """CPUs of the NUMA node the GPU's PCIe link hangs off (sysfs), or None if unknown."""
+    import os
+
+    import torch
+
+    try:
+        prop = torch.cuda.get_device_properties(device_index)
+        bus = f"{prop.pci_domain_id:04x}:{prop.pci_bus_id:02x}:{prop.pci_device_id:02x}.0"
+        with open(f"/sys/bus/pci/devices/{bus}/numa_node") as f:
+            node = int(f.read().strip())
+        if node < 0:
+            return None
+        with open(f"/sys/devices/system/node/node{node}/cpulist") as f:
+            spec = f.read().strip()
+    except Exception:
+        return None
+    cpus: set[int] = set()
+    for part in spec.split(","):
+        lo, _, hi = part.partition("-")
+        cpus.update(range(int(lo), int(hi or lo) + 1))
+    allowed = os.sched_getaffinity(0)
+    return (cpus & allowed) or None
+
+
+class numa_local:
+    """Context manager: run (and first-touch page-locked host buffers) on the CPUs local
+    to the GPU, so host <-> device copies do not cross the socket interconnect; the
+    previous affinity is restored on exit.  A no-op where the topology is unknown."""
+
+    def __init__(self, device_index: int):
+        self.device_index = device_index
+        self.saved = None
+        self.cpus = None
+
+    def __enter__(self):
+        import os
+
+        self.cpus = gpu_local_cpus(self.device_index)
+        if self.cpus:
+            self.saved = os.sched_getaffinity(0)
+            os.sched_setaffinity(0, self.cpus)
+        return self
+
+    def __exit__(self, *exc):
+        import os
+
+        if self.saved is not None:
+            os.sched_setaffinity(0, self.saved)
