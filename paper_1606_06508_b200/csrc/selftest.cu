@@ -128,6 +128,12 @@ __global__ void selftest_f32(uint64_t seed, int64_t n, unsigned long long* out) 
         if (cat == 5) {                                           // quotient shaped
             if ((ua & 0x7fffffffu) > (ub & 0x7fffffffu)) { unsigned t = ua; ua = ub; ub = t; }
         }
+        if (cat == 7) {                                           // IEEE special operands
+            const unsigned sp[6] = {0x00000000u, 0x80000000u, 0x7f800000u, 0xff800000u,
+                                    0x7fc00000u, 0x3f800000u};
+            if ((w1 >> 8) & 1) ua = sp[(w1 >> 9) % 6];
+            if ((w1 >> 12) & 1) ub = sp[(w1 >> 13) % 6];
+        }
         float a = __uint_as_float(ua), b = __uint_as_float(ub);
         if (cat == 6) a = (w1 >> 8) & 1 ? 0.0f : -0.0f;
         const float got = fnb::Divider<float>(b)(a);
