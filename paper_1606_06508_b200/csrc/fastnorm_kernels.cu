@@ -125,6 +125,34 @@ static int cps_override() {
     return v;
 }
 
+// Programmatic dependent launch for the streaming kernels (FASTNORM_B200_PDL=0 turns it
+// off).  Back-to-back launches on a stream overlap one kernel's drain with the next one's
+// launch and prologue; each kernel still waits (griddepcontrol.wait) for its
+// predecessor before touching global memory, so stream order semantics are unchanged.
+static bool pdl_enabled() {
+    static const bool v = [] {
+        const char* e = getenv("FASTNORM_B200_PDL");
+        return !(e && strcmp(e, "0") == 0);
+    }();
+    return v;
+}
+
+template <typename... Params, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(Params...), int grid, int block, size_t smem,
+                              cudaStream_t stream, Args... args) {
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 // CTAs per SM: the measured streaming optimum (CtasPerSm); small batches (few tiles per
 // CTA) fill the machine with the occupancy maximum instead, to shorten the pipeline
 // fill / drain.
@@ -157,13 +185,14 @@ static int launch(const void* xv, int64_t n, void* hv, void* bv, void* qv, const
         const int64_t per_sm = std::min<int64_t>(TL::blocks_per_sm(dev), ctas_per_sm_for<OP>(ntiles, sms));
         const int64_t resident = per_sm * sms;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, resident));
-        tma_stream_kernel<T, N, OP>
-            <<<grid, Tile<T, N>::kThreads, L::kSmemBytes, stream>>>(x, n, head, body, extra, ka);
+        e = launch_pdl(tma_stream_kernel<T, N, OP>, grid, Tile<T, N>::kThreads, L::kSmemBytes,
+                       stream, x, n, head, body, extra, ka);
     } else {
         const int64_t want = (n + 255) / 256;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 8));
-        direct_kernel<T, N, OP><<<grid, 256, 0, stream>>>(x, n, head, body, extra, ka);
+        e = launch_pdl(direct_kernel<T, N, OP>, grid, 256, 0, stream, x, n, head, body, extra, ka);
     }
+    if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
     return FN_OK;

@@ -139,10 +139,25 @@ __device__ __forceinline__ void count_invalid(unsigned long long* counter, unsig
     if ((threadIdx.x & 31) == 0 && bad) atomicAdd(counter, bad);
 }
 
+// Programmatic dependent launch (PDL).  The host launches the streaming kernels with
+// programmatic stream serialization allowed, so a kernel may become resident while its
+// predecessor on the stream drains.  griddepcontrol.wait (a no-op for a normal launch)
+// blocks until every predecessor grid has completed and its memory is visible, so it
+// runs before the first global load or store; launch_dependents then lets the next
+// PDL launch on the stream start its own prologue early.
+__device__ __forceinline__ void grid_dependency_wait() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void grid_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 template <typename T, int N, int OP>
 __global__ void __launch_bounds__(256) direct_kernel(const T* __restrict__ x, int64_t nrows,
                                                      T* __restrict__ head, T* __restrict__ body,
                                                      T* __restrict__ extra, KArgs<T> ka) {
+    grid_dependency_wait();
+    grid_launch_dependents();
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     unsigned long long bad = 0;
     const int64_t start = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -315,6 +330,8 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
         fence_barrier_init();
     }
     __syncthreads();
+    grid_dependency_wait();
+    grid_launch_dependents();
     if (leader) {
         for (int64_t k = 0; k < my_tiles && k < S; ++k) {
             const int64_t tile = (int64_t)blockIdx.x + k * gridDim.x;

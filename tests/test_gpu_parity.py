@@ -271,3 +271,51 @@ def test_host_path_pageable_and_pinned(cuda_dev, x_pinned, out_pinned):
     fn.normalize3(p, x, out=(r, u))
     h, b, _ = oracle.run(_lib.OP_NORMALIZE, xn, np.array(fn.kernel_args(p)), threads=8)
     assert oracle.same(r, h).all() and oracle.same(u, b).all()
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_back_to_back_launch_ordering(cuda_dev, graph):
+    """The streaming kernels are launched with programmatic dependent launch.  Stream
+    order must still hold for read-after-write (launch k+1 consumes launch k's unit
+    vectors) and write-after-read (launch k+1 overwrites launch k's input), eagerly and
+    inside a CUDA graph.  Buffers start as NaN so a stale read cannot pass."""
+    n, chain = 1 << 21, 12
+    x0 = torch.from_numpy(_random_rows(n, 3, False, seed=77)).to(cuda_dev)
+    p = fn.preset("double")
+    want = [x0]
+    for _ in range(chain):
+        want.append(fn.normalize3(p, want[-1]).unit)
+    torch.cuda.synchronize()
+    bufs = [x0.clone()] + [torch.full_like(x0, float("nan")) for _ in range(chain)]
+    lens = [torch.full((n,), float("nan"), dtype=torch.float64, device=cuda_dev) for _ in range(chain)]
+    spare = torch.full_like(x0, float("nan"))
+
+    def run():
+        for k in range(chain):
+            fn.normalize3(p, bufs[k], out=(lens[k], bufs[k + 1]))
+        # write-after-read: the next launch overwrites the input of the one before it
+        fn.normalize3(p, bufs[chain - 1], out=(lens[0], spare))
+        fn.normalize3(p, bufs[chain], out=(lens[1], bufs[chain - 1]))
+
+    if graph:
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(device=cuda_dev)
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                run()
+        torch.cuda.synchronize()
+        for b in bufs[1:] + [spare]:
+            b.fill_(float("nan"))
+        bufs[0].copy_(x0)
+        torch.cuda.synchronize()
+        g.replay()
+    else:
+        run()
+    torch.cuda.synchronize()
+    bits = lambda t: t.view(torch.int64)  # noqa: E731
+    for k in range(1, chain - 1):
+        assert torch.equal(bits(bufs[k]), bits(want[k])), k
+    assert torch.equal(bits(bufs[chain]), bits(want[chain]))
+    assert torch.equal(bits(spare), bits(want[chain]))  # read before the overwrite
+    assert torch.equal(bits(bufs[chain - 1]), bits(fn.normalize3(p, want[chain]).unit))
