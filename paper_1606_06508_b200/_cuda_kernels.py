@@ -90,38 +90,62 @@ def batch_kernel(base: str, suffix: str):
 _tls = threading.local()
 
 
-def _scalar_buffers():
-    b = getattr(_tls, "bufs", None)
-    if b is None:
-        b = _tls.bufs = ((ctypes.c_double * 8)(), (ctypes.c_double * 16)(), (ctypes.c_double * 6)())
-    return b
+def _scalar_state():
+    """Per-thread argument buffers for fn_scalar and their addresses."""
+    st = getattr(_tls, "state", None)
+    if st is None:
+        xb, ob, kb = (ctypes.c_double * 8)(), (ctypes.c_double * 16)(), (ctypes.c_double * 6)()
+        st = _tls.state = (xb, ob, kb, ctypes.addressof(xb), ctypes.addressof(ob), ctypes.addressof(kb))
+    return st
+
+
+_ext_state: list = []
+
+
+def _scalar_entry():
+    """The CPython fast path (csrc/scalar_ext.c) bound to the loaded library's
+    fn_scalar, or None when that module was not built (the ctypes call is used then;
+    both launch the same kernel)."""
+    if not _ext_state:
+        try:
+            from paper_1606_06508_b200 import _scalar
+        except ImportError:
+            _ext_state.append(None)
+        else:
+            _scalar.bind(ctypes.cast(_lib.lib().fn_scalar, ctypes.c_void_p).value)
+            _ext_state.append(_scalar.scalar)
+    return _ext_state[0]
 
 
 def _make_scalar(base: str, suffix: str):
-    """Reference scalar signature -> fn_scalar (one launch on a mapped page-locked row)."""
+    """Reference scalar signature -> fn_scalar (one launch; the row rides in the kernel
+    parameters, the results come back through mapped page-locked memory)."""
     op, dim = parse_base(base)
     takes_ka = op in (_lib.OP_SCALE, _lib.OP_NORMALIZE, _lib.OP_NORMALIZE_SQ, _lib.OP_NORM)
     dcode = _lib.F64 if suffix == "f64" else _lib.F32
     nargs = dim + (6 if takes_ka else 0)
     nout = sum(batch.widths(op, dim))
     sq_first = op == _lib.OP_NORMALIZE_SQ
+    name = f"{base}_{suffix}"
 
     def kernel(*args):
         if len(args) != nargs:
-            raise TypeError(f"{base}_{suffix} takes {nargs} arguments ({len(args)} given)")
-        xb, ob, kb = _scalar_buffers()
+            raise TypeError(f"{name} takes {nargs} arguments ({len(args)} given)")
+        fast = _scalar_entry()
+        if fast is not None:
+            res = fast(op, dim, dcode, nout, sq_first, args)
+            if type(res) is int:
+                _lib.check(res, name)
+            return res
+        xb, ob, kb, xa, oa, kaddr = _scalar_state()
         if takes_ka:
-            for i in range(6):
-                kb[i] = args[i]
-            for i in range(dim):
-                xb[i] = args[6 + i]
+            kb[:] = args[:6]
+            xb[:dim] = args[6:]
         else:
-            for i in range(dim):
-                xb[i] = args[i]
-        rc = _lib.lib().fn_scalar(op, dim, dcode, ctypes.addressof(xb), ctypes.addressof(ob),
-                                  ctypes.addressof(kb) if takes_ka else None)
+            xb[:dim] = args
+        rc = _lib.lib().fn_scalar(op, dim, dcode, xa, oa, kaddr if takes_ka else None)
         if rc:
-            _lib.check(rc, f"{base}_{suffix}")
+            _lib.check(rc, name)
         if nout == 1:
             return ob[0]
         vals = ob[:nout]

@@ -13,6 +13,7 @@
 #include <mutex>
 #include <thread>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "stream_kernel.cuh"
@@ -599,17 +600,99 @@ int host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, v
 }
 
 // ---------------------------------------------------------------------------------
-// One row, low latency (the reference's scalar signatures): the row and its results
-// live in a per-thread, per-device page-locked buffer that is mapped into the device
-// address space; one direct-kernel launch reads and writes it over PCIe and one stream
-// synchronisation returns -- no staging copies, no allocation after the first call.
+// One row, low latency (the reference's scalar signatures).  The row travels inside the
+// kernel's parameter block (no device read of host memory); one thread computes it with
+// the same RowOp as the batched kernels, stores the results into a per-thread,
+// per-device page-locked buffer mapped into the device address space, fences at system
+// scope and publishes a sequence number there.  The host spins on that word instead
+// of synchronising the stream (cudaStreamQuery every few thousand spins catches a
+// failed launch).  No staging copies, no allocation after the first call.
 // ---------------------------------------------------------------------------------
+template <typename T, int N> struct RowArg {
+    T v[N];
+};
+
+constexpr int kScalarFlagOffset = 128;  // bytes; outputs (at most 14 values) sit below
+
+template <typename T, int N, int OP>
+__global__ void __launch_bounds__(32) scalar_kernel(RowArg<T, N> x, KArgs<T> ka, T* out,
+                                                    unsigned* flag, unsigned seq) {
+    using Op = RowOp<T, N, OP>;
+    if (threadIdx.x != 0) return;
+    T xr[N], o0[Slot<Op::W0>::value], o1[Slot<Op::W1>::value], o2[Slot<Op::W2>::value];
+#pragma unroll
+    for (int c = 0; c < N; ++c) xr[c] = x.v[c];
+    (void)Op::apply(xr, ka, o0, o1, o2);
+    int k = 0;
+#pragma unroll
+    for (int c = 0; c < Op::W0; ++c) out[k++] = o0[c];
+#pragma unroll
+    for (int c = 0; c < Op::W1; ++c) out[k++] = o1[c];
+#pragma unroll
+    for (int c = 0; c < Op::W2; ++c) out[k++] = o2[c];
+    __threadfence_system();
+    *reinterpret_cast<volatile unsigned*>(flag) = seq;
+}
+
 struct ScalarCtx {
     int dev = -1;
     cudaStream_t stream = nullptr;
     char* host = nullptr;   // 256 B page-locked, mapped
     char* dptr = nullptr;   // its device alias
+    unsigned seq = 0;
 };
+
+template <typename T, int N, int OP>
+static cudaError_t scalar_launch(const double* xin, const KArgs<T>& ka, const ScalarCtx& c) {
+    RowArg<T, N> x;
+    for (int k = 0; k < N; ++k) x.v[k] = (T)xin[k];  // f32: the reference's <float> cast
+    scalar_kernel<T, N, OP><<<1, 32, 0, c.stream>>>(
+        x, ka, reinterpret_cast<T*>(c.dptr), reinterpret_cast<unsigned*>(c.dptr + kScalarFlagOffset), c.seq);
+    return cudaGetLastError();
+}
+
+template <typename T, int OP>
+static cudaError_t scalar_dim(int dim, const double* xin, const KArgs<T>& ka, const ScalarCtx& c) {
+    switch (dim) {
+        case 2: return scalar_launch<T, 2, OP>(xin, ka, c);
+        case 3: return scalar_launch<T, 3, OP>(xin, ka, c);
+        default: return scalar_launch<T, 4, OP>(xin, ka, c);
+    }
+}
+
+template <typename T>
+static int scalar_dispatch(int op, int dim, const double* xin, const double* kad, const ScalarCtx& c) {
+    KArgs<T> ka;
+    int rc = make_kargs<T>(kad, needs_ka(op), ka);
+    if (rc != FN_OK) return rc;
+    cudaError_t e;
+    switch (op) {
+        case FN_OP_SCALE: e = scalar_dim<T, FN_OP_SCALE>(dim, xin, ka, c); break;
+        case FN_OP_NORMALIZE: e = scalar_dim<T, FN_OP_NORMALIZE>(dim, xin, ka, c); break;
+        case FN_OP_NORMALIZE_SQ: e = scalar_dim<T, FN_OP_NORMALIZE_SQ>(dim, xin, ka, c); break;
+        case FN_OP_NORM: e = scalar_dim<T, FN_OP_NORM>(dim, xin, ka, c); break;
+        case FN_OP_NAIVE: e = scalar_dim<T, FN_OP_NAIVE>(dim, xin, ka, c); break;
+        case FN_OP_QUOTIENT: e = scalar_dim<T, FN_OP_QUOTIENT>(dim, xin, ka, c); break;
+        case FN_OP_QUOTIENT3_FAST:
+            if (dim != 3) return fail(FN_EINVAL, "quotient3_fast is defined for dim 3 only");
+            e = scalar_launch<T, 3, FN_OP_QUOTIENT3_FAST>(xin, ka, c);
+            break;
+        default:
+            if constexpr (std::is_same<T, double>::value) {
+                if (op == FN_OP_ROT_UNIT) { e = scalar_launch<double, 4, FN_OP_ROT_UNIT>(xin, ka, c); break; }
+                if (op == FN_OP_ROT_GENERAL) { e = scalar_launch<double, 4, FN_OP_ROT_GENERAL>(xin, ka, c); break; }
+                if (op == FN_OP_NORMALIZE_ROT) { e = scalar_launch<double, 4, FN_OP_NORMALIZE_ROT>(xin, ka, c); break; }
+            }
+            return fail(FN_EINVAL, "unknown op");
+    }
+    return e == cudaSuccess ? FN_OK : cuda_fail(e, "scalar kernel launch");
+}
+
+static inline void cpu_relax() {
+#if defined(__x86_64__) || defined(__i386__)
+    __builtin_ia32_pause();
+#endif
+}
 
 int scalar_run(int op, int dim, int dtype, const double* xin, double* out, const double* ka) {
     static thread_local std::vector<ScalarCtx> ctxs;
@@ -631,28 +714,33 @@ int scalar_run(int op, int dim, int dtype, const double* xin, double* out, const
         if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
         e = cudaHostAlloc(reinterpret_cast<void**>(&c.host), 256, cudaHostAllocMapped);
         if (e != cudaSuccess) return cuda_fail(e, "cudaHostAlloc");
+        memset(c.host, 0, 256);
         e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c.dptr), c.host, 0);
         if (e != cudaSuccess) return cuda_fail(e, "cudaHostGetDevicePointer");
         c.dev = dev;
     }
-    const Widths wd = op_widths(op, dim);
-    // layout: x at 0, head at 64, body at 128, extra at 192 (bytes)
-    for (int k = 0; k < dim; ++k) {
-        if (dtype == FN_F64) reinterpret_cast<double*>(c.host)[k] = xin[k];
-        else reinterpret_cast<float*>(c.host)[k] = (float)xin[k];  // the reference's <float> cast
-    }
-    int rc = run(op, dim, dtype, c.dptr, 1, c.dptr + 64, wd.w1 ? c.dptr + 128 : nullptr,
-                 wd.w2 ? c.dptr + 192 : nullptr, ka, c.stream);
+    if (++c.seq == 0) c.seq = 1;  // 0 is the initial flag value
+    const int rc = dtype == FN_F64 ? scalar_dispatch<double>(op, dim, xin, ka, c)
+                                   : scalar_dispatch<float>(op, dim, xin, ka, c);
     if (rc != FN_OK) return rc;
-    e = cudaStreamSynchronize(c.stream);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
-    const int offs[3] = {64, 128, 192};
-    const int ws[3] = {wd.w0, wd.w1, wd.w2};
-    int o = 0;
-    for (int a = 0; a < 3; ++a)
-        for (int k = 0; k < ws[a]; ++k, ++o)
-            out[o] = dtype == FN_F64 ? reinterpret_cast<const double*>(c.host + offs[a])[k]
-                                     : (double)reinterpret_cast<const float*>(c.host + offs[a])[k];
+    unsigned* flag = reinterpret_cast<unsigned*>(c.host + kScalarFlagOffset);
+    for (unsigned spin = 1;; ++spin) {
+        if (__atomic_load_n(flag, __ATOMIC_ACQUIRE) == c.seq) break;
+        if ((spin & 4095u) == 0) {
+            e = cudaStreamQuery(c.stream);
+            if (e == cudaSuccess) {
+                if (__atomic_load_n(flag, __ATOMIC_ACQUIRE) == c.seq) break;
+                return fail(FN_ECUDA, "scalar kernel finished without publishing its result");
+            }
+            if (e != cudaErrorNotReady) return cuda_fail(e, "scalar kernel");
+        }
+        cpu_relax();
+    }
+    const Widths wd = op_widths(op, dim);
+    const int total = wd.w0 + wd.w1 + wd.w2;
+    for (int o = 0; o < total; ++o)
+        out[o] = dtype == FN_F64 ? reinterpret_cast<const double*>(c.host)[o]
+                                 : (double)reinterpret_cast<const float*>(c.host)[o];
     return FN_OK;
 }
 

@@ -139,3 +139,16 @@ def test_c_example_runs():
                          capture_output=True, text=True)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "r = 1.2203" in out.stdout or "r = " in out.stdout
+
+
+def test_scalar_extension_binds_fn_scalar():
+    """The CPython fast path for the scalar signatures is built in-tree and binds the
+    loaded library's fn_scalar; without a GPU its calls fail loudly like the ABI."""
+    from paper_1606_06508_b200 import _cuda_kernels, _scalar
+
+    assert _cuda_kernels._scalar_entry() is _scalar.scalar
+    if _lib.device_count() == 0:
+        with pytest.raises(_lib.CudaLibraryError):
+            _cuda_kernels.normalize3_f64(*[1.0] * 6, 3.0, 4.0, 12.0)
+    with pytest.raises(TypeError):
+        _scalar.scalar(1, 3, 1, 4, False, [3.0, 4.0, 12.0])

@@ -319,3 +319,29 @@ def test_back_to_back_launch_ordering(cuda_dev, graph):
     assert torch.equal(bits(bufs[chain]), bits(want[chain]))
     assert torch.equal(bits(spare), bits(want[chain]))  # read before the overwrite
     assert torch.equal(bits(bufs[chain - 1]), bits(fn.normalize3(p, want[chain]).unit))
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_scalar_path_equals_batched_on_every_golden_row(golden, cuda_dev, prec):
+    """Every golden row (random, special-value products, KATs) through the scalar
+    signatures (CPython fast path -> fn_scalar, row in the kernel parameters) equals the
+    batched kernels bit for bit, for every family incl. normalize{n}_sq (squared length
+    first in the scalar tuple)."""
+    ka = tuple(float(v) for v in golden[f"{prec}_ka"])
+    for dim in (2, 3, 4):
+        x = _golden_rows(golden, prec, dim)
+        xd = torch.from_numpy(x).to(cuda_dev)
+        for base in [_base(f, dim) for f in FAMILIES[dim]] + [f"normalize{dim}_sq"]:
+            scaling = base.startswith(("scale", "normalize", "norm"))
+            res = _cuda_kernels.batch_kernel(base, prec)(xd, np.array(ka) if scaling else None)
+            torch.cuda.synchronize()
+            table = _as_table(res)
+            if base.endswith("_sq"):
+                table = np.concatenate([res.sq.cpu().numpy().astype(np.float64)[:, None], table], axis=1)
+            k = getattr(_cuda_kernels, f"{base}_{prec}")
+            for i in range(len(x)):
+                row = [float(v) for v in x[i]]
+                out = k(*ka, *row) if scaling else k(*row)
+                out = out if isinstance(out, tuple) else (out,)
+                assert len(out) == table.shape[1]
+                assert all(same_scalar(a, b) for a, b in zip(out, table[i])), (base, row, out, table[i])
