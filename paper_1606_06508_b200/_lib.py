@@ -68,6 +68,10 @@ def _declare(L: ctypes.CDLL) -> None:
     L.fn_measure_bounds.argtypes = [_int, _int, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp]
     L.fn_selftest_div.restype = _int
     L.fn_selftest_div.argtypes = [_int, ctypes.c_uint64, _i64, _vp, _vp]
+    L.fn_host_alloc.restype = _int
+    L.fn_host_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(_vp)]
+    L.fn_host_free.restype = _int
+    L.fn_host_free.argtypes = [_vp]
     L.fn_row_stats.restype = _int
     L.fn_row_stats.argtypes = [_int, _int, _vp, _i64, _vp, _vp, _vp]
 

@@ -57,6 +57,29 @@ def host_devices(devices):
         _host.devices = prev
 
 
+def host_empty(shape, dtype=np.float64) -> np.ndarray:
+    """An uninitialised numpy array in page-locked (portable) host memory from
+    ``fn_host_alloc``.  Host-array calls DMA such buffers directly instead of staging
+    them (1.56 vs 0.64 Gvec/s for 3-D f64 rows with inputs and outputs page-locked).
+    The memory is released (``fn_host_free``) when the array and every view of it are
+    gone.  Allocation pins pages, so reuse these buffers across calls."""
+    import ctypes
+    import weakref
+
+    shape = (int(shape),) if np.isscalar(shape) else tuple(int(d) for d in shape)
+    dt = np.dtype(dtype)
+    count = int(np.prod(shape, dtype=np.int64))
+    nbytes = count * dt.itemsize
+    if nbytes == 0:
+        return np.empty(shape, dtype=dt)
+    L = _lib.lib()
+    ptr = ctypes.c_void_p()
+    _lib.check(L.fn_host_alloc(nbytes, ctypes.byref(ptr)), "fn_host_alloc")
+    buf = (ctypes.c_char * nbytes).from_address(ptr.value)
+    weakref.finalize(buf, L.fn_host_free, ptr.value)
+    return np.frombuffer(buf, dtype=dt, count=count).reshape(shape)
+
+
 class BatchOut(NamedTuple):
     head: Any
     body: Any

@@ -810,6 +810,30 @@ int fn_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, voi
     return fnb::run(op, dim, dtype, x, n, head, body, sq, ka, stream);
 }
 
+int fn_host_alloc(size_t bytes, void** ptr) {
+    if (!ptr) return fnb::set_error(FN_EINVAL, "ptr must not be NULL");
+    *ptr = nullptr;
+    if (bytes == 0) return FN_OK;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fnb::set_error(FN_ENODEV, "no CUDA device");
+    }
+    const cudaError_t e = cudaHostAlloc(ptr, bytes, cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+        *ptr = nullptr;
+        return fnb::set_error(e == cudaErrorMemoryAllocation ? FN_ENOMEM : FN_ECUDA, cudaGetErrorString(e));
+    }
+    return FN_OK;
+}
+
+int fn_host_free(void* ptr) {
+    if (!ptr) return FN_OK;
+    const cudaError_t e = cudaFreeHost(ptr);
+    if (e != cudaSuccess) return fnb::set_error(FN_ECUDA, cudaGetErrorString(e));
+    return FN_OK;
+}
+
 int fn_host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* body,
                 void* sq, const double* ka) {
     return fnb::host_run(op, dim, dtype, x, n, head, body, sq, ka);

@@ -152,3 +152,16 @@ def test_scalar_extension_binds_fn_scalar():
             _cuda_kernels.normalize3_f64(*[1.0] * 6, 3.0, 4.0, 12.0)
     with pytest.raises(TypeError):
         _scalar.scalar(1, 3, 1, 4, False, [3.0, 4.0, 12.0])
+
+
+def test_host_alloc_without_gpu_fails_loudly():
+    import paper_1606_06508_b200 as fn
+
+    ptr = ctypes.c_void_p(1)
+    L = _lib.lib()
+    assert L.fn_host_alloc(0, ctypes.byref(ptr)) == 0 and not ptr.value
+    assert L.fn_host_free(None) == 0
+    assert fn.host_empty((0, 3)).shape == (0, 3)
+    if _lib.device_count() == 0:
+        with pytest.raises(_lib.CudaLibraryError):
+            fn.host_empty((16, 3))

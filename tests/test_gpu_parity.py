@@ -345,3 +345,27 @@ def test_scalar_path_equals_batched_on_every_golden_row(golden, cuda_dev, prec):
                 out = out if isinstance(out, tuple) else (out,)
                 assert len(out) == table.shape[1]
                 assert all(same_scalar(a, b) for a, b in zip(out, table[i])), (base, row, out, table[i])
+
+
+def test_host_empty_buffers_exact_and_released(cuda_dev):
+    """host_empty arrays (page-locked, DMA'd without staging) go through the host path and
+    give the same bits as device inputs; the memory is freed with the last view."""
+    import gc
+    import weakref
+
+    n = (1 << 20) + 7
+    x = fn.host_empty((n, 3))
+    x[:] = _random_rows(n, 3, False, seed=21)
+    r, u = fn.host_empty(n), fn.host_empty((n, 3))
+    p = fn.preset("double")
+    fn.normalize3(p, x, out=(r, u))
+    want = fn.normalize3(p, torch.from_numpy(np.array(x)).to(cuda_dev))
+    assert np.array_equal(r.view(np.int64), want.length.cpu().numpy().view(np.int64))
+    assert np.array_equal(u.view(np.int64), want.unit.cpu().numpy().view(np.int64))
+    owner = x
+    while isinstance(owner, np.ndarray):
+        owner = owner.base
+    alive = weakref.ref(owner)  # the ctypes block whose finalizer calls fn_host_free
+    del x, owner
+    gc.collect()
+    assert alive() is None
