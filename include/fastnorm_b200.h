@@ -69,8 +69,12 @@ typedef enum {
      * general form) get NaN matrices and are counted into *invalid (fn_run_rot). */
     FN_OP_ROT_UNIT = 7,       /* rotation_unit(q)                      rotation.py:87-111 */
     FN_OP_ROT_GENERAL = 8,    /* rotation_general(q) via scale4        rotation.py:53-84  */
-    FN_OP_NORMALIZE_ROT = 9   /* normalize4 fused with rotation_unit of its unit output:
+    FN_OP_NORMALIZE_ROT = 9,  /* normalize4 fused with rotation_unit of its unit output:
                                  head = r[N], body = unit[N,4], sq slot = R[N,3,3]       */
+    /* RotationMatrix.apply (rotation.py:39-41) over a batch of vectors: x = v[N,3]
+     * (dim 3, FN_F64), head = R v [N,3]; the ka argument points to the 9 entries of R,
+     * row-major.  out_i = ((R_i0 v_0 + R_i1 v_1) + R_i2 v_2), each operation rounded. */
+    FN_OP_ROT_APPLY = 10
 } fn_op;
 
 typedef enum { FN_F32 = 0, FN_F64 = 1 } fn_dtype;
@@ -112,6 +116,10 @@ int fn_host_run_multi(int op, int dim, int dtype, const void* x, int64_t n, void
  * of rows the reference would reject. */
 int fn_run_rot(int op, const double* q, int64_t n, double* head, double* body, double* extra,
                const double* ka, uint64_t* invalid, void* stream);
+
+/* RotationMatrix.apply (rotation.py:39-41) for a batch: out[N,3] = R v[N,3], R[9]
+ * row-major (same as fn_run(FN_OP_ROT_APPLY, 3, FN_F64, v, n, out, NULL, NULL, R, s)). */
+int fn_rotate_apply_f64(const double R[9], const double* v, int64_t n, double* out, void* stream);
 
 /* ---- named entry points: one per reference export --------------------------------- */
 /* scale{n}_{f64,f32}      replaces _kernels.pyx:419-439 / :523-546 */

@@ -79,6 +79,9 @@ def lib() -> ctypes.CDLL:
             L.orc_rotation.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64,
                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                        ctypes.c_void_p]
+            L.orc_rotate_apply.restype = None
+            L.orc_rotate_apply.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                           ctypes.c_void_p]
             L.orc_loop.restype = ctypes.c_double
             L.orc_loop.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
                                    ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p]
@@ -151,6 +154,19 @@ def rotation(op: int, q: np.ndarray, ka=None):
     R = np.empty((n, 3, 3))
     bad = lib().orc_rotation(op, q.ctypes.data, n, R.ctypes.data, None, None, kptr)
     return R, int(bad)
+
+
+OP_ROT_APPLY = 10
+
+
+def rotate_apply(R, v: np.ndarray) -> np.ndarray:
+    """Oracle RotationMatrix.apply (rotation.py:39-41) of one matrix R (9 entries,
+    row-major) over float64 vectors v[N, 3]."""
+    Rm = np.ascontiguousarray(np.asarray(R, dtype=np.float64).reshape(9))
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    out = np.empty_like(v)
+    lib().orc_rotate_apply(Rm.ctypes.data, v.ctypes.data, v.shape[0], out.ctypes.data)
+    return out
 
 
 def loop(algo: int, buf: np.ndarray, iters: int, mask: int, ka=None) -> float:

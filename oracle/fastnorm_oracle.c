@@ -339,4 +339,14 @@ int64_t orc_rotation(int op, const double* q, int64_t n, double* head, double* b
     return bad;
 }
 
+/* RotationMatrix.apply (rotation.py:39-41) with one matrix over v[N,3]:
+ * out_i = r[0]*v[0] + r[1]*v[1] + r[2]*v[2], evaluated left to right (Python floats). */
+void orc_rotate_apply(const double* R, const double* v, int64_t n, double* out) {
+    for (int64_t i = 0; i < n; ++i) {
+        const double* x = v + 3 * i;
+        for (int k = 0; k < 3; ++k)
+            out[3 * i + k] = R[3 * k] * x[0] + R[3 * k + 1] * x[1] + R[3 * k + 2] * x[2];
+    }
+}
+
 const char* orc_build_flags(void) { return "gcc -O3 -ffp-contract=off"; }

@@ -26,6 +26,7 @@ OP_NORMALIZE_SQ = 6
 OP_ROT_UNIT = 7
 OP_ROT_GENERAL = 8
 OP_NORMALIZE_ROT = 9
+OP_ROT_APPLY = 10
 F32 = 0
 F64 = 1
 
@@ -72,6 +73,8 @@ def _declare(L: ctypes.CDLL) -> None:
     L.fn_host_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(_vp)]
     L.fn_host_free.restype = _int
     L.fn_host_free.argtypes = [_vp]
+    L.fn_rotate_apply_f64.restype = _int
+    L.fn_rotate_apply_f64.argtypes = [_vp, _vp, _i64, _vp, _vp]
     L.fn_row_stats.restype = _int
     L.fn_row_stats.argtypes = [_int, _int, _vp, _i64, _vp, _vp, _vp]
 

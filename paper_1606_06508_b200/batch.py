@@ -32,6 +32,8 @@ def widths(op: int, dim: int) -> tuple[int, int, int]:
         return 9, 0, 0
     if op == _lib.OP_NORMALIZE_ROT:
         return 1, 4, 9
+    if op == _lib.OP_ROT_APPLY:
+        return 3, 0, 0
     return 1, dim, 0
 
 

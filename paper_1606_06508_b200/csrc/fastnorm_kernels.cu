@@ -75,11 +75,13 @@ static Widths op_widths(int op, int dim) {
         case FN_OP_ROT_UNIT:
         case FN_OP_ROT_GENERAL: return {9, 0, 0};
         case FN_OP_NORMALIZE_ROT: return {1, 4, 9};
+        case FN_OP_ROT_APPLY: return {3, 0, 0};
         default: return {1, dim, 0};
     }
 }
 static bool is_rotation(int op) {
-    return op == FN_OP_ROT_UNIT || op == FN_OP_ROT_GENERAL || op == FN_OP_NORMALIZE_ROT;
+    return op == FN_OP_ROT_UNIT || op == FN_OP_ROT_GENERAL || op == FN_OP_NORMALIZE_ROT ||
+           op == FN_OP_ROT_APPLY;
 }
 
 // Per-instantiation occupancy (computed once per process and device).
@@ -237,6 +239,17 @@ static int make_kargs(const double* ka, bool needed, KArgs<T>& out) {
     return FN_OK;
 }
 
+// Kernel arguments of an op: the six scaling constants, or for FN_OP_ROT_APPLY the nine
+// matrix entries (the ka pointer of the ABI carries R there).
+template <typename T>
+static int make_kargs_op(int op, const double* ka, bool needed, KArgs<T>& out) {
+    if (op != FN_OP_ROT_APPLY) return make_kargs<T>(ka, needed, out);
+    memset(&out, 0, sizeof(out));
+    if (!ka) return fail(FN_EINVAL, "FN_OP_ROT_APPLY needs the 9 matrix entries in ka");
+    for (int k = 0; k < 9; ++k) out.rot[k] = (T)ka[k];
+    return FN_OK;
+}
+
 template <typename T, int OP>
 static int dispatch_dim(int dim, const void* x, int64_t n, void* h, void* b, void* q,
                         const KArgs<T>& ka, cudaStream_t s) {
@@ -279,23 +292,26 @@ static int dispatch(int op, int dim, const void* x, int64_t n, void* h, void* b,
 static int dispatch_rot(int op, const void* x, int64_t n, void* h, void* b, void* q,
                         const double* kad, unsigned long long* invalid, cudaStream_t s) {
     KArgs<double> ka;
-    int rc = make_kargs<double>(kad, needs_ka(op), ka);
+    int rc = make_kargs_op<double>(op, kad, needs_ka(op), ka);
     if (rc != FN_OK) return rc;
     ka.invalid = invalid;
     switch (op) {
         case FN_OP_ROT_UNIT: return launch<double, 4, FN_OP_ROT_UNIT>(x, n, h, b, q, ka, s);
         case FN_OP_ROT_GENERAL: return launch<double, 4, FN_OP_ROT_GENERAL>(x, n, h, b, q, ka, s);
         case FN_OP_NORMALIZE_ROT: return launch<double, 4, FN_OP_NORMALIZE_ROT>(x, n, h, b, q, ka, s);
+        case FN_OP_ROT_APPLY: return launch<double, 3, FN_OP_ROT_APPLY>(x, n, h, b, q, ka, s);
         default: return fail(FN_EINVAL, "unknown rotation op");
     }
 }
 
 int check_args(int op, int dim, int dtype, const void* x, int64_t n, const void* head,
                const void* body, const void* sq) {
-    if (op < FN_OP_SCALE || op > FN_OP_NORMALIZE_ROT) return fail(FN_EINVAL, "unknown op");
+    if (op < FN_OP_SCALE || op > FN_OP_ROT_APPLY) return fail(FN_EINVAL, "unknown op");
     if (dim < 2 || dim > 4) return fail(FN_EINVAL, "dim must be 2, 3 or 4");
     if (dtype != FN_F32 && dtype != FN_F64) return fail(FN_EINVAL, "dtype must be FN_F32/FN_F64");
-    if (is_rotation(op) && (dim != 4 || dtype != FN_F64))
+    if (op == FN_OP_ROT_APPLY && (dim != 3 || dtype != FN_F64))
+        return fail(FN_EINVAL, "FN_OP_ROT_APPLY takes float64 3-vectors (dim 3, FN_F64)");
+    if (is_rotation(op) && op != FN_OP_ROT_APPLY && (dim != 4 || dtype != FN_F64))
         return fail(FN_EINVAL, "rotations take float64 quaternions (dim 4, FN_F64)");
     if (n < 0) return fail(FN_EINVAL, "n must be >= 0");
     if (n == 0) return FN_OK;
@@ -663,7 +679,7 @@ static cudaError_t scalar_dim(int dim, const double* xin, const KArgs<T>& ka, co
 template <typename T>
 static int scalar_dispatch(int op, int dim, const double* xin, const double* kad, const ScalarCtx& c) {
     KArgs<T> ka;
-    int rc = make_kargs<T>(kad, needs_ka(op), ka);
+    int rc = make_kargs_op<T>(op, kad, needs_ka(op), ka);
     if (rc != FN_OK) return rc;
     cudaError_t e;
     switch (op) {
@@ -682,6 +698,7 @@ static int scalar_dispatch(int op, int dim, const double* xin, const double* kad
                 if (op == FN_OP_ROT_UNIT) { e = scalar_launch<double, 4, FN_OP_ROT_UNIT>(xin, ka, c); break; }
                 if (op == FN_OP_ROT_GENERAL) { e = scalar_launch<double, 4, FN_OP_ROT_GENERAL>(xin, ka, c); break; }
                 if (op == FN_OP_NORMALIZE_ROT) { e = scalar_launch<double, 4, FN_OP_NORMALIZE_ROT>(xin, ka, c); break; }
+                if (op == FN_OP_ROT_APPLY) { e = scalar_launch<double, 3, FN_OP_ROT_APPLY>(xin, ka, c); break; }
             }
             return fail(FN_EINVAL, "unknown op");
     }
@@ -697,7 +714,7 @@ static inline void cpu_relax() {
 int scalar_run(int op, int dim, int dtype, const double* xin, double* out, const double* ka) {
     static thread_local std::vector<ScalarCtx> ctxs;
     if (!xin || !out) return fail(FN_EINVAL, "xin and out must not be NULL");
-    if (op < FN_OP_SCALE || op > FN_OP_NORMALIZE_ROT || dim < 2 || dim > 4)
+    if (op < FN_OP_SCALE || op > FN_OP_ROT_APPLY || dim < 2 || dim > 4)
         return fail(FN_EINVAL, "unknown op or dim");
     {
         const Widths v = op_widths(op, dim);
@@ -848,11 +865,14 @@ int fn_host_run_multi(int op, int dim, int dtype, const void* x, int64_t n, void
     return fnb::host_run_multi(op, dim, dtype, x, n, head, body, sq, ka, devices, ndev);
 }
 
+int fn_rotate_apply_f64(const double R[9], const double* v, int64_t n, double* out, void* stream) {
+    return fnb::run(FN_OP_ROT_APPLY, 3, FN_F64, v, n, out, nullptr, nullptr, R, stream);
+}
+
 int fn_run_rot(int op, const double* q, int64_t n, double* head, double* body, double* extra,
                const double* ka, uint64_t* invalid, void* stream) {
-    if (op != FN_OP_ROT_UNIT && op != FN_OP_ROT_GENERAL && op != FN_OP_NORMALIZE_ROT)
-        return fnb::set_error(FN_EINVAL, "fn_run_rot takes a rotation op");
-    return fnb::run_ex(op, 4, FN_F64, q, n, head, body, extra, ka,
+    if (!fnb::is_rotation(op)) return fnb::set_error(FN_EINVAL, "fn_run_rot takes a rotation op");
+    return fnb::run_ex(op, op == FN_OP_ROT_APPLY ? 3 : 4, FN_F64, q, n, head, body, extra, ka,
                        reinterpret_cast<unsigned long long*>(invalid), stream);
 }
 

@@ -116,6 +116,7 @@ template <typename T> struct KArgs {
     int k_min, k_max;   // log2(sigma_min), log2(sigma_max) when pow2 (validated sets)
     bool pow2;          // sigma_min, sigma_max and their inverses are powers of two
     unsigned long long* invalid;  // rows rejected by the rotations (may be NULL)
+    T rot[9];           // FN_OP_ROT_APPLY: the matrix, row-major
 };
 
 // ---------------------------------------------------------------------------------
@@ -522,6 +523,16 @@ __device__ __forceinline__ bool rotation_unit_row(const T (&q)[4], T* R) {
         for (int k = 0; k < 9; ++k) R[k] = T(NAN);
     }
     return ok;
+}
+
+// RotationMatrix.apply (rotation.py:39-41): out_i = ((R_i0 v_0 + R_i1 v_1) + R_i2 v_2)
+// with every product and sum rounded separately, as the reference's Python floats.
+template <typename T>
+__device__ __forceinline__ void rotation_apply_row(const T (&v)[3], const T (&R)[9], T* out) {
+    using F = Fp<T>;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+        out[i] = F::add(F::add(F::mul(R[3 * i], v[0]), F::mul(R[3 * i + 1], v[1])), F::mul(R[3 * i + 2], v[2]));
 }
 
 // rotation_general: scale4 (exact cascade, :61-62), ss = ((q1^2+q2^2)+q3^2)+q4^2 on the

@@ -111,6 +111,16 @@ template <typename T, int N> struct RowOp<T, N, FN_OP_NORMALIZE_ROT> {
     }
 };
 
+// R v for a batch of vectors with one matrix (in the kernel arguments).
+template <typename T, int N> struct RowOp<T, N, FN_OP_ROT_APPLY> {
+    static_assert(N == 3, "the rotation is applied to 3-vectors");
+    static constexpr int W0 = 3, W1 = 0, W2 = 0;
+    __device__ __forceinline__ static bool apply(const T (&x)[N], const KArgs<T>& ka, T* o0, T*, T*) {
+        rotation_apply_row(x, ka.rot, o0);
+        return true;
+    }
+};
+
 template <int W> struct Slot { static constexpr int value = W > 0 ? W : 1; };
 
 // One row through global memory (tails, unaligned arrays, tiny batches).

@@ -29,7 +29,7 @@ from paper_1606_06508_b200.params import FpParams, preset
 from paper_1606_06508_b200.scale import check_precision, kernel_args_array
 
 __all__ = ["RotationMatrix", "NormalizeRotationOutcome", "rotation_general", "rotation_unit",
-           "normalize4_rotation"]
+           "normalize4_rotation", "rotate_vectors"]
 
 Row = tuple[float, float, float]
 
@@ -46,8 +46,18 @@ class RotationMatrix:
     def flat(self) -> tuple[float, ...]:
         return self.rows[0] + self.rows[1] + self.rows[2]
 
-    def apply(self, v: tuple[float, float, float]) -> Row:
-        """Matrix-vector product R @ v."""
+    def apply(self, v, out=None):
+        """Matrix-vector product R @ v (rotation.py:39-41).
+
+        A 3-tuple is evaluated like the reference (its Python glue, not a kernel).  One
+        [N, 3] float64 array (CUDA tensor or host array) selects the batched kernel
+        (FN_OP_ROT_APPLY: 24 B in, 24 B out per vector, R in the kernel arguments),
+        bit-identical to applying the reference row by row."""
+        if batch.is_array(v) and v.ndim == 2:
+            if str(v.dtype).replace("torch.", "") != "float64":
+                raise TypeError("apply takes float64 vectors (the reference computes in double)")
+            R = np.array(self.flat(), dtype=np.float64)
+            return batch.run(_lib.OP_ROT_APPLY, 3, v, R, out=None if out is None else (out,)).head
         return tuple(r[0] * v[0] + r[1] * v[1] + r[2] * v[2] for r in self.rows)
 
 
@@ -95,12 +105,29 @@ def _batched(op: int, q, strict: bool, what: str, out=None):
     return res.head
 
 
+def _scalar_rotation(op: int, q) -> np.ndarray:
+    """One quaternion through fn_scalar (row in the kernel parameters): R[3, 3]."""
+    from paper_1606_06508_b200 import _cuda_kernels
+
+    row = _scalar_quaternion(q)
+    fast = _cuda_kernels._scalar_entry()
+    if fast is None:  # extension not built: the host-array path (also the GPU)
+        ka = kernel_args_array(preset("double")) if op == _lib.OP_ROT_GENERAL else None
+        return batch.run(op, 4, row, ka).head[0]
+    args = tuple(row[0].tolist())
+    if op == _lib.OP_ROT_GENERAL:
+        args = tuple(kernel_args_array(preset("double")).tolist()) + args
+    res = fast(op, 4, _lib.F64, 9, False, args)
+    if type(res) is int:
+        _lib.check(res, "rotation")
+    return np.array(res, dtype=np.float64).reshape(3, 3)
+
+
 def rotation_general(q, strict: bool = True, out=None):
     """Rotation matrix of an arbitrary nonzero quaternion (or [N, 4] quaternions)."""
     if batch.is_array(q) and q.ndim == 2:
         return _batched(_lib.OP_ROT_GENERAL, q, strict, "rotation_general", out)
-    row = _scalar_quaternion(q)
-    m = batch.run(_lib.OP_ROT_GENERAL, 4, row, kernel_args_array(preset("double"))).head[0]
+    m = _scalar_rotation(_lib.OP_ROT_GENERAL, q)
     if np.isnan(m[0, 0]):
         raise ValueError("zero quaternion has no rotation matrix")
     return _as_matrix(m)
@@ -110,8 +137,17 @@ def rotation_unit(q, strict: bool = True, out=None):
     """Rotation matrix of a unit quaternion (or [N, 4] unit quaternions); no norm taken."""
     if batch.is_array(q) and q.ndim == 2:
         return _batched(_lib.OP_ROT_UNIT, q, strict, "rotation_unit", out)
-    row = _scalar_quaternion(q)
-    return _as_matrix(batch.run(_lib.OP_ROT_UNIT, 4, row, None).head[0])
+    return _as_matrix(_scalar_rotation(_lib.OP_ROT_UNIT, q))
+
+
+def rotate_vectors(q, v, method: str = "unit", out=None):
+    """Rotate the vectors v[N, 3] (float64; CUDA tensor or host array) by one quaternion:
+    ``rotation_{method}(q).apply(v)`` -- one scalar launch for the matrix, then one
+    streaming pass over the vectors."""
+    if method not in ("unit", "general"):
+        raise ValueError(f"method must be 'unit' or 'general', got {method!r}")
+    m = rotation_unit(q) if method == "unit" else rotation_general(q)
+    return m.apply(v, out=out)
 
 
 def normalize4_rotation(p: FpParams, q, out=None) -> NormalizeRotationOutcome:

@@ -223,6 +223,17 @@ def main():
     out["rot_general"] = np.array(gen)
     out["rot_unit"] = np.array(uni)
     out["rot_unit_of_normalized"] = np.array(uni_n)
+    # RotationMatrix.apply (rotation.py:39-41): matrices from rotation_unit of the
+    # reference's normalized quaternions and from rotation_general of raw ones, each
+    # applied to vectors of every magnitude class and to special-value products.
+    mats = [rot.rotation_unit(tuple(u)) for u in units[:6].tolist()]
+    mats += [rot.rotation_general(tuple(row)) for row in q[600:604].tolist()]
+    mats.append(rot.rotation_unit((0.0, 0.0, 0.0, 1.0)))
+    vecs = np.concatenate([random_rows(rng, 400, 3, False), rng.standard_normal((200, 3)),
+                           np.array(list(itertools.product(SPECIALS["f64"][:8], repeat=3)))])
+    out["rot_apply_R"] = np.array([m.flat() for m in mats])
+    out["rot_apply_v"] = vecs
+    out["rot_apply_out"] = np.array([[m.apply(tuple(v)) for v in vecs.tolist()] for m in mats])
     path = os.path.join(HERE, "golden_vectors.npz")
     np.savez_compressed(path, **out)
     n = sum(v.size for v in out.values())

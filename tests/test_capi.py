@@ -73,6 +73,12 @@ def test_argument_errors_without_gpu():
     bad[0] = np.nan
     assert L.fn_run(1, 3, 1, x.ctypes.data, 4, h.ctypes.data, b.ctypes.data, None, bad.ctypes.data, None) == -1
     assert b"tau" in L.fn_last_error()
+    # FN_OP_ROT_APPLY: float64 3-vectors only, and ka carries the matrix
+    assert L.fn_run(10, 4, 1, x.ctypes.data, 4, h.ctypes.data, None, None, ka.ctypes.data, None) == -1
+    assert L.fn_run(10, 3, 0, x.ctypes.data, 4, h.ctypes.data, None, None, ka.ctypes.data, None) == -1
+    assert L.fn_run(10, 3, 1, x.ctypes.data, 4, b.ctypes.data, b.ctypes.data, None, ka.ctypes.data, None) == -1
+    assert L.fn_rotate_apply_f64(None, x.ctypes.data, 4, b.ctypes.data, None) == -1
+    assert b"matrix" in L.fn_last_error()
     # n == 0 is a no-op success
     assert L.fn_run(1, 3, 1, vp(0), 0, vp(0), vp(0), None, ka.ctypes.data, None) == 0
     assert L.fn_host_run(1, 3, 1, vp(0), 0, vp(0), vp(0), None, ka.ctypes.data) == 0

@@ -81,3 +81,44 @@ def test_rotations_cfg3_full(cuda_dev):
     U = fn.rotation_unit(res.unit)
     torch.cuda.synchronize()
     assert bool((U.view(torch.int64) == res.rotation.view(torch.int64)).all())
+
+
+@pytest.mark.parametrize("where", ["device", "device_unaligned", "host"])
+def test_rotate_apply_golden(golden, cuda_dev, where):
+    """RotationMatrix.apply over a batch (FN_OP_ROT_APPLY) == the reference's apply, row
+    by row, for every golden matrix and vector (special values included)."""
+    v = golden["rot_apply_v"]
+    if where == "device":
+        vd = torch.from_numpy(v).to(cuda_dev)
+    elif where == "device_unaligned":
+        vd = torch.from_numpy(np.concatenate([v[:1], v])).to(cuda_dev)[1:]
+    else:
+        vd = v
+    for Rf, want in zip(golden["rot_apply_R"], golden["rot_apply_out"]):
+        m = fn.RotationMatrix(tuple(tuple(Rf[3 * i:3 * i + 3].tolist()) for i in range(3)))
+        got = m.apply(vd)
+        got = to_np(got) if hasattr(got, "cpu") else got
+        assert oracle.same(got, want).all()
+        # the scalar form (the reference's own Python expression) agrees as well
+        for k in range(0, len(v), 97):
+            assert oracle.same(np.array(m.apply(tuple(v[k].tolist()))), want[k]).all()
+
+
+def test_rotate_vectors_full_size(cuda_dev):
+    """2^27 config-5-class vectors (wide exponent range, near-DBL_MAX and subnormal rows)
+    rotated by one quaternion, unit and general forms, vs the oracle; the scalar matrix
+    comes from the scalar rotation path."""
+    n = 1 << 27
+    v = torch.empty((n, 3), dtype=torch.float64, device=cuda_dev)
+    workloads.generate_device(5, v)
+    q = (0.3, -1.2, 2.5, 0.7)
+    for method in ("unit", "general"):
+        out = fn.rotate_vectors(q, v, method=method)
+        m = fn.rotation_unit(q) if method == "unit" else fn.rotation_general(q)
+        torch.cuda.synchronize()
+        chunk = 1 << 24
+        for lo in range(0, n, chunk):
+            vh = to_np(v[lo:lo + chunk])
+            assert oracle.same(to_np(out[lo:lo + chunk]), oracle.rotate_apply(m.flat(), vh)).all()
+    with pytest.raises(TypeError):
+        fn.rotation_unit(q).apply(v.float())

@@ -69,3 +69,12 @@ def test_oracle_rotations_match_reference_golden(golden, oracle_mod):
     assert oracle_mod.same(R.reshape(-1, 9), golden["rot_unit_of_normalized"]).all()
     h, b, _ = oracle_mod.run(oracle_mod.OP_NORMALIZE, q, ka)
     assert oracle_mod.same(r, h).all() and oracle_mod.same(u, b).all()
+
+
+def test_oracle_rotate_apply_matches_reference_golden(golden, oracle_mod):
+    """RotationMatrix.apply (rotation.py:39-41), evaluated by the reference module on
+    rotation_unit / rotation_general matrices over vectors of every magnitude class and
+    special-value products (inf, NaN, signed zeros)."""
+    v = golden["rot_apply_v"]
+    for R, want in zip(golden["rot_apply_R"], golden["rot_apply_out"]):
+        assert oracle_mod.same(oracle_mod.rotate_apply(R, v), want).all()

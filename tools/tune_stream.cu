@@ -50,6 +50,7 @@ struct Bufs {
 template <typename T>
 KArgs<T> make_ka() {
     KArgs<T> ka;
+    memset(&ka, 0, sizeof(ka));
     const bool f = sizeof(T) == 4;
     ka.tau_min = (T)(f ? 0x1p-49 : 0x1p-482);
     ka.tau_max = (T)(f ? 0x1p62 : 0x1p510);
@@ -59,6 +60,8 @@ KArgs<T> make_ka() {
     ka.inv_max = (T)(f ? 0x1p66 : 0x1p514);
     memcpy(&ka.tau_min_bits, &ka.tau_min, sizeof(T));
     memcpy(&ka.tau_max_bits, &ka.tau_max, sizeof(T));
+    const double rot[9] = {0.36, 0.48, -0.8, -0.8, 0.6, 0.0, 0.48, 0.64, 0.6};
+    for (int k = 0; k < 9; ++k) ka.rot[k] = (T)rot[k];
     return ka;
 }
 
@@ -216,6 +219,9 @@ int main(int argc, char** argv) {
         vs.push_back(V("rotation_general_f64", 3, double, 4, FN_OP_ROT_GENERAL, 256, 3, 256, 0, 4));
         vs.push_back(V("normalize4_rot_f64", 3, double, 4, FN_OP_NORMALIZE_ROT, 128, 3, 256, 0, 2));
         vs.push_back(V("normalize4_rot_f64", 3, double, 4, FN_OP_NORMALIZE_ROT, 128, 4, 128, 0, 3));
+        vs.push_back(V("rot_apply_f64", 5, double, 3, FN_OP_ROT_APPLY, 256, 4, 256, 0, 2));
+        vs.push_back(V("rot_apply_f64", 5, double, 3, FN_OP_ROT_APPLY, 256, 4, 256, 0, 3));
+        vs.push_back(V("rot_apply_f64", 5, double, 3, FN_OP_ROT_APPLY, 256, 4, 256, 0, 4));
     }
     if (which == "all" || which == "f64x2") {
         vs.push_back(V("normalize2_f64", 2, double, 2, FN_OP_NORMALIZE, 512, 4, 256, 0, 2));
