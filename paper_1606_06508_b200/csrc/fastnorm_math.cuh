@@ -541,9 +541,11 @@ template <typename T>
 __device__ __forceinline__ bool rotation_general_row(const T (&x)[4], const KArgs<T>& ka, T* R) {
     using F = Fp<T>;
     bool ok = isfinite(x[0]) && isfinite(x[1]) && isfinite(x[2]) && isfinite(x[3]);
+    // Rows that reach R are finite and nonzero; there the integer classification gives
+    // the cascade's (inv, s) exactly, without its divergent branches.
+    // Rejected rows (non-finite or zero) get NaN matrices below either way.
     T inv, q[4];
-    scale_row(x, ka, inv, q);
-    ok = ok && inv != T(0);
+    ok = scale_classified<T, 4>(x, ka, inv, q) && ok;
     const T q1 = q[0], q2 = q[1], q3 = q[2], q4 = q[3];
     const T a11 = F::mul(q1, q1), a22 = F::mul(q2, q2), a33 = F::mul(q3, q3), a44 = F::mul(q4, q4);
     const T ss = F::add(F::add(F::add(a11, a22), a33), a44);

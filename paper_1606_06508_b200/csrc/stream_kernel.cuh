@@ -288,11 +288,25 @@ template <int OP> struct CtasPerSm {
         : (OP == FN_OP_NORM ? 4 : 2);
 };
 
-template <typename T, int N, int OP, int TR_, int S_> struct TileLayout {
+// Output staging tiles: 3 (one bulk-store group reading behind the current one).  A
+// fourth tile for the write-heavy rotations measured +2 % in tools/tune_stream
+// (profiles/r01ax_rot.csv) but -5 % through the library (normalize4_rotation 6265 vs
+// 5950 GB/s, A/B of the two builds alternated on one box, profiles/r01az_ab.txt), so
+// FNB_ROT_OUT_TILES stays 3.
+#ifndef FNB_ROT_OUT_TILES
+#define FNB_ROT_OUT_TILES 3
+#endif
+template <int OP> struct OutTiles {
+    static constexpr int value =
+        (OP == FN_OP_ROT_UNIT || OP == FN_OP_ROT_GENERAL || OP == FN_OP_NORMALIZE_ROT) ? FNB_ROT_OUT_TILES : 3;
+};
+
+template <typename T, int N, int OP, int TR_, int S_, int OB_ = OutTiles<OP>::value> struct TileLayout {
     using Op = RowOp<T, N, OP>;
     static constexpr int TR = TR_;
     static constexpr int S = S_;
-    static constexpr int OB = 3;
+    static constexpr int OB = OB_;  // output staging tiles (bulk-store groups in flight)
+    static_assert(OB >= 3, "the store pipeline keeps OB - 2 groups reading behind the current one");
     static constexpr int kInBytes = TR * N * (int)sizeof(T);
     static constexpr int kB0 = TR * Op::W0 * (int)sizeof(T);
     static constexpr int kB1 = TR * Op::W1 * (int)sizeof(T);
@@ -313,11 +327,11 @@ template <typename T, int N, int OP> struct OpRows {
 // HINTS: bit 0 -> input loads carry an L2 evict-first policy (read once);
 //        bit 1 -> output bulk stores carry an L2 evict-first policy.
 template <typename T, int N, int OP, int TR_ = OpRows<T, N, OP>::value, int S_ = Tile<T, N>::kStages,
-          int NT = Tile<T, N>::kThreads, int HINTS = Tile<T, N>::kHints>
+          int NT = Tile<T, N>::kThreads, int HINTS = Tile<T, N>::kHints, int OB_ = OutTiles<OP>::value>
 __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x, int64_t nrows,
                                                         T* __restrict__ head, T* __restrict__ body,
                                                         T* __restrict__ extra, KArgs<T> ka) {
-    using L = TileLayout<T, N, OP, TR_, S_>;
+    using L = TileLayout<T, N, OP, TR_, S_, OB_>;
     using Op = typename L::Op;
     constexpr int TR = L::TR, S = L::S, OB = L::OB;
     constexpr int W0 = Op::W0, W1 = Op::W1, W2 = Op::W2;
@@ -405,8 +419,9 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
                 else
                     bulk_load_plain(s_in + s * L::kInBytes, x + nt * TR * N, L::kInBytes, &full[s]);
             }
-            // The staging tile written at iteration k+1 was last drained by group k-2.
-            bulk_wait_read<1>();
+            // Threads write staging tile (k+2) % OB after the next __syncthreads, so group
+            // k+2-OB must have been read out by then: at most OB-2 groups stay pending.
+            bulk_wait_read<OB - 2>();
         }
     }
 

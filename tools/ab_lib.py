@@ -1,59 +1,80 @@
-"""A/B timing of two builds of libfastnorm_b200.so on the bench workload (dev tool).
+"""A/B timing of two builds of libfastnorm_b200.so on a config workload (dev tool).
 
-python tools/ab_lib.py OLD.so NEW.so [--reps 20] [--rounds 5]
-Both libraries run fn_run(FN_OP_NORMALIZE, 3, FN_F64) over the same 2^30 config-5 rows,
-interleaved round by round, timed with CUDA events on one stream."""
+python tools/ab_lib.py OLD.so NEW.so [--op 1] [--dim 3] [--cfg 5] [--log2-rows 30]
+Both libraries run fn_run(op, dim, FN_F64) over the same config rows, alternating
+process by process (each .so carries its own static cudart, so one library per
+process), timed with CUDA events on one stream.  Defaults: the bench workload
+(normalize3 over 2^30 config-5 rows)."""
+import argparse
 import ctypes
 import statistics
+import subprocess
 import sys
 
-import torch
-
 sys.path.insert(0, ".")
-from paper_1606_06508_b200 import workloads  # noqa: E402
 
 
-def load(path):
-    L = ctypes.CDLL(path)
+def parse(argv):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("libs", nargs="+")
+    ap.add_argument("--op", type=int, default=1)
+    ap.add_argument("--dim", type=int, default=3)
+    ap.add_argument("--cfg", type=int, default=5)
+    ap.add_argument("--log2-rows", type=int, default=30)
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--rounds", type=int, default=3)
+    return ap.parse_args(argv)
+
+
+def run_one(a):
+    import numpy as np
+    import torch
+
+    from paper_1606_06508_b200 import batch, workloads
+
+    L = ctypes.CDLL(a.libs[0])
     L.fn_run.restype = ctypes.c_int
     L.fn_run.argtypes = [ctypes.c_int] * 3 + [ctypes.c_void_p, ctypes.c_int64] + [ctypes.c_void_p] * 5
-    return L
+    n = 1 << a.log2_rows
+    x = torch.empty((n, a.dim), dtype=torch.float64, device="cuda")
+    workloads.generate_device(a.cfg, x)
+    w0, w1, w2 = batch.widths(a.op, a.dim)
+    outs = [torch.empty((n, w), dtype=torch.float64, device="cuda") if w else None for w in (w0, w1, w2)]
+    ptr = [o.data_ptr() if o is not None else None for o in outs]
+    ka = np.array([2.0 ** -482, 2.0 ** 510, 2.0 ** 592, 2.0 ** -514, 2.0 ** -592, 2.0 ** 514])
+    s = torch.cuda.current_stream().cuda_stream
+    bytes_per_row = 8 * (a.dim + w0 + w1 + w2)
+
+    def launch():
+        rc = L.fn_run(a.op, a.dim, 1, x.data_ptr(), n, ptr[0], ptr[1], ptr[2], ka.ctypes.data, s)
+        assert rc == 0, rc
+
+    times = []
+    for _ in range(a.rounds):
+        for _ in range(3):
+            launch()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(a.reps):
+            launch()
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) / a.reps)
+    ms = statistics.median(times)
+    print(f"{a.libs[0]}: op={a.op} dim={a.dim} cfg={a.cfg} {ms:.4f} ms/launch, "
+          f"{n * bytes_per_row / ms / 1e6:.1f} GB/s, all={['%.3f' % v for v in times]}", flush=True)
 
 
 def main():
-    # one library per process (each .so carries its own static cudart)
-    if len(sys.argv) > 2:
-        import subprocess
-        for rd in range(3):
-            for path in sys.argv[1:3]:
-                subprocess.run([sys.executable, __file__, path], check=True)
+    a = parse(sys.argv[1:])
+    if len(a.libs) > 1:
+        rest = [f"--op={a.op}", f"--dim={a.dim}", f"--cfg={a.cfg}", f"--log2-rows={a.log2_rows}",
+                f"--reps={a.reps}", f"--rounds={a.rounds}"]
+        for _ in range(3):
+            for path in a.libs:
+                subprocess.run([sys.executable, __file__, path] + rest, check=True)
         return
-    libs = [load(sys.argv[1])]
-    reps, rounds = 20, 3
-    n = 1 << 30
-    x = torch.empty((n, 3), dtype=torch.float64, device="cuda")
-    workloads.generate_device(5, x)
-    r = torch.empty(n, dtype=torch.float64, device="cuda")
-    u = torch.empty((n, 3), dtype=torch.float64, device="cuda")
-    import numpy as np
-    ka = np.array([2.0 ** -482, 2.0 ** 510, 2.0 ** 592, 2.0 ** -514, 2.0 ** -592, 2.0 ** 514])
-    s = torch.cuda.current_stream().cuda_stream
-    res = {0: []}
-    for rd in range(rounds):
-        for k, L in enumerate(libs):
-            for _ in range(3):
-                rc = L.fn_run(1, 3, 1, x.data_ptr(), n, r.data_ptr(), u.data_ptr(), None, ka.ctypes.data, s)
-                assert rc == 0, rc
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            for _ in range(reps):
-                L.fn_run(1, 3, 1, x.data_ptr(), n, r.data_ptr(), u.data_ptr(), None, ka.ctypes.data, s)
-            e1.record()
-            torch.cuda.synchronize()
-            res[k].append(e0.elapsed_time(e1) / reps)
-    for k in (0,):
-        ms = statistics.median(res[k])
-        print(f"{sys.argv[1 + k]}: {ms:.4f} ms/launch, {n * 56 / ms / 1e6:.1f} GB/s, all={['%.3f' % v for v in res[k]]}")
+    run_one(a)
 
 
 if __name__ == "__main__":

@@ -65,10 +65,10 @@ KArgs<T> make_ka() {
     return ka;
 }
 
-template <typename T, int N, int OP, int TR, int S, int NT, int H>
+template <typename T, int N, int OP, int TR, int S, int NT, int H, int OB = OutTiles<OP>::value>
 float time_variant(const Bufs& b, int cps, int reps, int sms, int* occ_out) {
-    using L = TileLayout<T, N, OP, TR, S>;
-    auto kern = tma_stream_kernel<T, N, OP, TR, S, NT, H>;
+    using L = TileLayout<T, N, OP, TR, S, OB>;
+    auto kern = tma_stream_kernel<T, N, OP, TR, S, NT, H, OB>;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemBytes));
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, L::kSmemBytes));
@@ -112,6 +112,10 @@ constexpr int row_bytes() {
 #define V(FAM, CFG, T, N, OP, TR, S, NT, H, CPS)                                         \
     Variant{FAM, CFG, TR, S, NT, H, CPS, row_bytes<T, N, OP>(),                          \
             &time_variant<T, N, OP, TR, S, NT, H>, {}, 0}
+// same with OB output staging tiles (reported in the HINTS column as 10*OB + HINTS)
+#define VO(FAM, CFG, T, N, OP, TR, S, NT, H, CPS, OB)                                    \
+    Variant{FAM, CFG, TR, S, NT, 10 * OB + H, CPS, row_bytes<T, N, OP>(),                \
+            &time_variant<T, N, OP, TR, S, NT, H, OB>, {}, 0}
 
 int main(int argc, char** argv) {
     const int lg = argc > 1 ? atoi(argv[1]) : 28;
@@ -219,6 +223,15 @@ int main(int argc, char** argv) {
         vs.push_back(V("rotation_general_f64", 3, double, 4, FN_OP_ROT_GENERAL, 256, 3, 256, 0, 4));
         vs.push_back(V("normalize4_rot_f64", 3, double, 4, FN_OP_NORMALIZE_ROT, 128, 3, 256, 0, 2));
         vs.push_back(V("normalize4_rot_f64", 3, double, 4, FN_OP_NORMALIZE_ROT, 128, 4, 128, 0, 3));
+        vs.push_back(VO("rotation_unit_f64", 3, double, 4, FN_OP_ROT_UNIT, 256, 3, 256, 0, 2, 4));
+        vs.push_back(VO("rotation_unit_f64", 3, double, 4, FN_OP_ROT_UNIT, 256, 3, 256, 0, 2, 5));
+        vs.push_back(VO("rotation_unit_f64", 3, double, 4, FN_OP_ROT_UNIT, 128, 3, 128, 0, 3, 4));
+        vs.push_back(VO("rotation_unit_f64", 3, double, 4, FN_OP_ROT_UNIT, 128, 3, 128, 0, 3, 6));
+        vs.push_back(VO("normalize4_rot_f64", 3, double, 4, FN_OP_NORMALIZE_ROT, 128, 3, 256, 0, 2, 4));
+        vs.push_back(VO("normalize4_rot_f64", 3, double, 4, FN_OP_NORMALIZE_ROT, 128, 3, 256, 0, 2, 5));
+        vs.push_back(VO("normalize3_f64", 5, double, 3, FN_OP_NORMALIZE, 256, 4, 256, 0, 2, 3));
+        vs.push_back(VO("normalize3_f64", 5, double, 3, FN_OP_NORMALIZE, 256, 4, 256, 0, 2, 4));
+        vs.push_back(VO("normalize3_f64", 5, double, 3, FN_OP_NORMALIZE, 256, 4, 256, 0, 2, 5));
         vs.push_back(V("rot_apply_f64", 5, double, 3, FN_OP_ROT_APPLY, 256, 4, 256, 0, 2));
         vs.push_back(V("rot_apply_f64", 5, double, 3, FN_OP_ROT_APPLY, 256, 4, 256, 0, 3));
         vs.push_back(V("rot_apply_f64", 5, double, 3, FN_OP_ROT_APPLY, 256, 4, 256, 0, 4));
