@@ -369,3 +369,45 @@ def test_host_empty_buffers_exact_and_released(cuda_dev):
     del x, owner
     gc.collect()
     assert alive() is None
+
+
+def test_concurrent_calls_from_threads(cuda_dev):
+    """The ABI is reentrant: host-path calls (per-device staging behind a mutex), scalar
+    calls (per-thread mapped buffers) and device-path calls on per-thread streams, all
+    from 6 Python threads at once, each checked against a serial run."""
+    import threading
+
+    p = fn.preset("double")
+    ka = fn.kernel_args(p)
+    rows = [_random_rows(200_003 + 17 * t, 3, False, seed=40 + t) for t in range(6)]
+    want = [fn.normalize3(p, torch.from_numpy(x).to(cuda_dev)) for x in rows]
+    want = [(w.length.cpu().numpy(), w.unit.cpu().numpy()) for w in want]
+    k = _backend.scalar_kernel("normalize3", "double")
+    errors = []
+
+    def work(t):
+        try:
+            x = rows[t]
+            for _ in range(3):
+                res = fn.normalize3(p, x)  # host path
+                assert np.array_equal(res.length.view(np.int64), want[t][0].view(np.int64))
+                assert np.array_equal(res.unit.view(np.int64), want[t][1].view(np.int64))
+                s = torch.cuda.Stream(device=cuda_dev)
+                with torch.cuda.stream(s):
+                    xd = torch.from_numpy(x).to(cuda_dev, non_blocking=False)
+                    rd = fn.normalize3(p, xd)
+                    s.synchronize()
+                assert np.array_equal(rd.unit.cpu().numpy().view(np.int64), want[t][1].view(np.int64))
+                for i in range(0, len(x), 20_011):
+                    out = k(*ka, *x[i].tolist())
+                    assert same_scalar(out[0], want[t][0][i])
+                    assert all(same_scalar(a, b) for a, b in zip(out[1:], want[t][1][i]))
+        except Exception as exc:  # noqa: BLE001 -- reported below
+            errors.append((t, repr(exc)))
+
+    threads = [threading.Thread(target=work, args=(t,)) for t in range(6)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
