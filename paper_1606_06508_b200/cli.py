@@ -181,6 +181,37 @@ def cmd_bench(a) -> int:
     return 0
 
 
+def cmd_ratios(a) -> int:
+    from paper_1606_06508_b200 import bench
+
+    cfg = bench.BenchConfig(experiments=a.experiments, rows=a.rows, reps=a.reps,
+                            dimensions=tuple(a.dims or (2, 3, 4)), precisions=tuple(a.precs or ("double",)),
+                            algorithms=tuple(a.algos or ALGOS), seed=a.seed, regime=a.regime)
+    try:
+        rep = bench.run_bench(cfg)
+    except bench.BenchConfigError as e:
+        print(f"error: {e}", file=sys.stderr)
+        return 2
+    env = rep.environment
+    print(f"# {env['device']} ({env['sm_count']} SMs), {env['library']}; timer: {env['timer']}")
+    print(f"# regime {cfg.regime}, {cfg.rows} vectors x {cfg.experiments} experiments x {cfg.reps} launches")
+    print(f"{'task':<14}{'prec':<8}{'algorithm':<16}{'ns/vector':>12}{'std':>10}{'Gvec/s':>10}")
+    for r in rep.rows:
+        print(f"{r.task:<14}{r.precision:<8}{r.algorithm:<16}{r.mean_ns_per_vector:>12.5f}"
+              f"{r.std_ns_per_vector:>10.5f}{r.vectors_per_s / 1e9:>10.2f}")
+    print(f"{'label':<7}{'task':<14}{'prec':<8}{'ratio':<28}{'mean':>8}{'std':>8}")
+    for r in rep.ratios:
+        print(f"{r.label:<7}{r.task:<14}{r.precision:<8}{r.numerator + '/' + r.denominator:<28}"
+              f"{r.mean:>8.2f}{r.std:>8.2f}")
+    if a.csv_path:
+        with open(a.csv_path, "w", encoding="utf-8") as fh:
+            fh.write(rep.to_csv())
+    if a.json_path:
+        with open(a.json_path, "w", encoding="utf-8") as fh:
+            fh.write(rep.to_json())
+    return 0
+
+
 def cmd_selftest(a) -> int:
     import torch
 
@@ -247,6 +278,20 @@ def build_parser() -> argparse.ArgumentParser:
     s.add_argument("--steps", type=int, default=20)
     s.add_argument("--warmup", type=int, default=3)
     s.set_defaults(fn=cmd_bench)
+
+    s = sub.add_parser("ratios", help="per-vector times and the T3/T4 ratio tables on the GPU "
+                                      "(the reference's `bench` protocol, batched)")
+    s.add_argument("--experiments", type=int, default=10)
+    s.add_argument("--rows", type=int, default=1 << 24, help="vectors per experiment (in HBM)")
+    s.add_argument("--reps", type=int, default=5, help="timed launches per algorithm and experiment")
+    s.add_argument("--dim", dest="dims", type=int, choices=(2, 3, 4), action="append")
+    s.add_argument("--prec", dest="precs", choices=("single", "double"), action="append")
+    s.add_argument("--algo", dest="algos", choices=ALGOS, action="append")
+    s.add_argument("--regime", choices=("normal", "subnormal", "huge", "mixed", "unit-ish"), default="normal")
+    s.add_argument("--seed", type=int, default=0)
+    s.add_argument("--csv", dest="csv_path", default=None)
+    s.add_argument("--json", dest="json_path", default=None)
+    s.set_defaults(fn=cmd_ratios)
 
     s = sub.add_parser("selftest", help="device self-test of the exact division paths")
     s.add_argument("--pairs", type=int, default=1 << 24)
