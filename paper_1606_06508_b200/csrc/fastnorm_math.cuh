@@ -257,15 +257,54 @@ __device__ __forceinline__ float special_quotient(float a, float b) {
     return nan ? __uint_as_float(0x7fc00000u) : __uint_as_float(sign | (inf ? 0x7f800000u : 0u));
 }
 
+// Binary32 Markstein division in binary32 arithmetic (same argument as div_markstein
+// above, p = 24): y = RN(1/b) (__frcp_rn), q1 faithful, r1 exact, q2 = RN(a/b).
+__device__ __forceinline__ float div_markstein32(float a, float b, float y) {
+    const float q0 = __fmul_rn(a, y);
+    const float r0 = __fmaf_rn(-b, q0, a);
+    const float q1 = __fmaf_rn(r0, y, q0);
+    const float r1 = __fmaf_rn(-b, q1, a);
+    return __fmaf_rn(r1, y, q1);
+}
+
+__device__ __forceinline__ int biased_exp32(float v) { return (int)((__float_as_uint(v) >> 23) & 0xffu); }
+
+// FNB_F32_DIV_NATIVE = 1 divides in-range binary32 operands natively (div_markstein32)
+// and keeps the binary64 path for the rest.  Exact (fn_selftest_div), but measured
+// slower everywhere (__frcp_rn plus the range test cost more than the binary64 Markstein
+// with its shared reciprocal): quotient3 f32 3780 -> 2440 GB/s on config 4 and
+// 3818 -> 3204 in band; quotient3_fast 5461 -> 3961 (profiles/r01bn_ab.txt).  Off.
+#ifndef FNB_F32_DIV_NATIVE
+#define FNB_F32_DIV_NATIVE 0
+#endif
+
 template <> struct Divider<float> {
     double b, y;
     float bf;
     bool bok;
+#if FNB_F32_DIV_NATIVE
+    float yf;
+    bool bfast;
+    int eb;
+#endif
     __device__ __forceinline__ explicit Divider(float b_) : b((double)b_), bf(b_) {
         bok = isfinite(b_) && b_ != 0.0f;
         y = __drcp_rn(bok ? b : 1.0);
+#if FNB_F32_DIV_NATIVE
+        eb = biased_exp32(b_);
+        bfast = eb >= 3 && eb <= 252;
+        yf = __frcp_rn(bfast ? b_ : 1.0f);
+#endif
     }
     __device__ __forceinline__ float operator()(float a) const {
+#if FNB_F32_DIV_NATIVE
+        // |a| >= 2^-100, 2^-124 <= |b| < 2^126, quotient exponent in [-100, 125] (the
+        // binary32 image of the binary64 bounds above): no intermediate under/overflow,
+        // r0 and r1 exact, so the Markstein result is RN(a/b).
+        const int ea = biased_exp32(a);
+        const int d = ea - eb;
+        if (bfast && ea >= 27 && ea <= 254 && d >= -100 && d <= 125) return div_markstein32(a, bf, yf);
+#endif
         // Finite operands: the binary64 quotient of two binary32 values rounded once to
         // binary32 (innocuous double rounding); a zero numerator gives the xor-signed zero.
         // The rest goes to special_quotient instead of the library division's slow path:

@@ -20,6 +20,8 @@ def parse(argv):
     ap.add_argument("--op", type=int, default=1)
     ap.add_argument("--dim", type=int, default=3)
     ap.add_argument("--cfg", type=int, default=5)
+    ap.add_argument("--regime", default=None, help="reference regime instead of a config")
+    ap.add_argument("--f32", action="store_true")
     ap.add_argument("--log2-rows", type=int, default=30)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--rounds", type=int, default=3)
@@ -36,17 +38,22 @@ def run_one(a):
     L.fn_run.restype = ctypes.c_int
     L.fn_run.argtypes = [ctypes.c_int] * 3 + [ctypes.c_void_p, ctypes.c_int64] + [ctypes.c_void_p] * 5
     n = 1 << a.log2_rows
-    x = torch.empty((n, a.dim), dtype=torch.float64, device="cuda")
-    workloads.generate_device(a.cfg, x)
+    dt = torch.float32 if a.f32 else torch.float64
+    x = torch.empty((n, a.dim), dtype=dt, device="cuda")
+    if a.regime:
+        workloads.generate_regime_device(a.regime, x)
+    else:
+        workloads.generate_device(a.cfg, x)
     w0, w1, w2 = batch.widths(a.op, a.dim)
-    outs = [torch.empty((n, w), dtype=torch.float64, device="cuda") if w else None for w in (w0, w1, w2)]
+    outs = [torch.empty((n, w), dtype=dt, device="cuda") if w else None for w in (w0, w1, w2)]
     ptr = [o.data_ptr() if o is not None else None for o in outs]
-    ka = np.array([2.0 ** -482, 2.0 ** 510, 2.0 ** 592, 2.0 ** -514, 2.0 ** -592, 2.0 ** 514])
+    ka = (np.array([2.0 ** -49, 2.0 ** 62, 2.0 ** 100, 2.0 ** -66, 2.0 ** -100, 2.0 ** 66]) if a.f32 else
+          np.array([2.0 ** -482, 2.0 ** 510, 2.0 ** 592, 2.0 ** -514, 2.0 ** -592, 2.0 ** 514]))
     s = torch.cuda.current_stream().cuda_stream
-    bytes_per_row = 8 * (a.dim + w0 + w1 + w2)
+    bytes_per_row = x.element_size() * (a.dim + w0 + w1 + w2)
 
     def launch():
-        rc = L.fn_run(a.op, a.dim, 1, x.data_ptr(), n, ptr[0], ptr[1], ptr[2], ka.ctypes.data, s)
+        rc = L.fn_run(a.op, a.dim, 0 if a.f32 else 1, x.data_ptr(), n, ptr[0], ptr[1], ptr[2], ka.ctypes.data, s)
         assert rc == 0, rc
 
     times = []
@@ -61,7 +68,8 @@ def run_one(a):
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1) / a.reps)
     ms = statistics.median(times)
-    print(f"{a.libs[0]}: op={a.op} dim={a.dim} cfg={a.cfg} {ms:.4f} ms/launch, "
+    src = f"regime={a.regime}" if a.regime else f"cfg={a.cfg}"
+    print(f"{a.libs[0]}: op={a.op} dim={a.dim} {src} {'f32' if a.f32 else 'f64'} {ms:.4f} ms/launch, "
           f"{n * bytes_per_row / ms / 1e6:.1f} GB/s, all={['%.3f' % v for v in times]}", flush=True)
 
 
@@ -69,7 +77,8 @@ def main():
     a = parse(sys.argv[1:])
     if len(a.libs) > 1:
         rest = [f"--op={a.op}", f"--dim={a.dim}", f"--cfg={a.cfg}", f"--log2-rows={a.log2_rows}",
-                f"--reps={a.reps}", f"--rounds={a.rounds}"]
+                f"--reps={a.reps}", f"--rounds={a.rounds}"] + (["--f32"] if a.f32 else []) + \
+            ([f"--regime={a.regime}"] if a.regime else [])
         for _ in range(3):
             for path in a.libs:
                 subprocess.run([sys.executable, __file__, path] + rest, check=True)
