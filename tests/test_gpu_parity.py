@@ -411,3 +411,41 @@ def test_concurrent_calls_from_threads(cuda_dev):
     for th in threads:
         th.join()
     assert not errors, errors
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_host_path_every_family_small_chunks(cuda_dev, pinned, monkeypatch):
+    """Every kernel family and both precisions through the host pipeline with 1 MiB
+    chunks (FASTNORM_B200_HOST_CHUNK_MB is read per call): many chunks, a ragged last
+    chunk, one to three output arrays of every width, page-locked or pageable buffers.
+    The device path (parity-tested above) is the reference."""
+    monkeypatch.setenv("FASTNORM_B200_HOST_CHUNK_MB", "1")
+
+    def host(a):
+        return torch.from_numpy(a).pin_memory().numpy() if pinned else a
+
+    for prec, single in (("f64", False), ("f32", True)):
+        for dim in (2, 3, 4):
+            x = host(_random_rows(3 * (1 << 20) // (dim * (4 if single else 8)) + 4099, dim, single, seed=dim))
+            xd = torch.from_numpy(np.array(x)).to(cuda_dev)
+            ka = np.array(fn.kernel_args(fn.preset("single" if single else "double")))
+            bases = [_base(f, dim) for f in FAMILIES[dim]] + [f"normalize{dim}_sq"]
+            for base in bases:
+                scaling = base.startswith(("scale", "normalize", "norm"))
+                k = _cuda_kernels.batch_kernel(base, prec)
+                got, want = k(x, ka if scaling else None), k(xd, ka if scaling else None)
+                torch.cuda.synchronize()
+                for g, w in zip(got, want):
+                    if g is None:
+                        continue
+                    assert oracle.same(np.asarray(g), w.cpu().numpy()).all(), (base, prec)
+    q = host(_random_rows(200_000, 4, False, seed=9))
+    qd = torch.from_numpy(np.array(q)).to(cuda_dev)
+    for f in (fn.rotation_unit, fn.rotation_general):
+        assert oracle.same(f(q, strict=False), f(qd, strict=False).cpu().numpy()).all()
+    res, resd = fn.normalize4_rotation(fn.preset("double"), q), fn.normalize4_rotation(fn.preset("double"), qd)
+    for g, w in zip(res, resd):
+        assert oracle.same(np.asarray(g), w.cpu().numpy()).all()
+    v = host(_random_rows(300_001, 3, False, seed=10))
+    m = fn.rotation_unit((0.1, 0.2, 0.3, 0.9))
+    assert oracle.same(m.apply(v), m.apply(torch.from_numpy(np.array(v)).to(cuda_dev)).cpu().numpy()).all()
