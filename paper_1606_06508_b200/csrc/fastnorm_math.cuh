@@ -228,6 +228,38 @@ struct MarksteinDivider {
 #define FNB_F64_DIV_MARKSTEIN 0
 #endif
 
+// Quotients that land on the subnormal grid (or flush to zero), computed exactly without
+// the library division's generic slow path.  Preconditions: a finite, b finite normal
+// (biased exponent 1..2046), and the normalised exponent gap ea - eb <= -1024, so
+// |a/b| < 2^-1023 and RN(a/b) = n 2^-1074 with n = RN_int(X), X = (fa / fb) 2^s,
+// fa, fb in [1, 2), s = ea - eb + 1074 <= 50:
+//   s <= -2 : X < 1/2, n = 0;
+//   s == -1 : X in (1/4, 1), n = [fa > fb] (X == 1/2 only if fa == fb: tie -> 0, even);
+//   s >=  0 : n0 = rint(RN(A / fb)), A = fa 2^s; |RN(A/fb) - X| <= 2^-3, so n0 is off by
+//             at most one; r = A - n0 fb is exact (a multiple of 2^-52 below 2 in
+//             magnitude) and decides: 2|r| > fb moves n0 one step towards X.  A tie
+//             (2|r| == fb) means X = n0 +- 1/2 is representable, hence RN(A/fb) = X and
+//             rint already chose the even neighbour.
+// The result bits are n itself (n <= 2^51) with the xor sign.
+__device__ __forceinline__ double tiny_quotient(double a, double b, int ea, unsigned long long ma, int eb) {
+    const unsigned long long kMant = 0x000FFFFFFFFFFFFFull, kOne = 1023ull << 52;
+    const unsigned long long sign = (__double_as_longlong(a) ^ __double_as_longlong(b)) & 0x8000000000000000ull;
+    const int s = ea - eb + 1074;
+    const double fa = __longlong_as_double((long long)(ma | kOne));
+    const double fb = __longlong_as_double((long long)((__double_as_longlong(b) & kMant) | kOne));
+    long long n = 0;
+    if (s == -1) {
+        n = fa > fb ? 1 : 0;
+    } else if (s >= 0) {
+        const double A = __longlong_as_double((long long)(ma | ((unsigned long long)(1023 + s) << 52)));
+        double n0 = rint(__ddiv_rn(A, fb));
+        const double r = __fma_rn(-n0, fb, A);
+        if (fabs(__dadd_rn(r, r)) > fb) n0 = __dadd_rn(n0, r > 0.0 ? 1.0 : -1.0);
+        n = __double2ll_rn(n0);
+    }
+    return __longlong_as_double((long long)((unsigned long long)n | sign));
+}
+
 #if !FNB_F64_DIV_MARKSTEIN
 // Plain IEEE division per numerator (__ddiv_rn).  Measured alternatives, all exact and
 // checked by fn_selftest_div, all slower on unit-range rows (configs 1, 3):
@@ -236,10 +268,39 @@ struct MarksteinDivider {
 //   * branch-free tiny-result path (numerator scaled by 2^600, one rounding onto the
 //     subnormal grid, midpoint fix from the exact remainder): +20 % on config 2 and +6 %
 //     on config 5 quotient rows, but -40 % on configs 1 and 3 (profiles/r01s_div.csv).
+// FNB_F64_TINY_QUOTIENT = 1 routes subnormal-grid quotients to tiny_quotient instead of
+// the library slow path.  Exact (fn_selftest_div, golden, full-size parity), but the
+// division-bound kernels are issue-bound and the per-division range test costs more
+// than it saves: quotient2 cfg 2 55.2 -> 50.9, quotient3 cfg 5 36.6 -> 30.1 and cfg 1
+// 101 -> 79 Gvec/s (profiles/r01bq_ab.txt).  Off.
+#ifndef FNB_F64_TINY_QUOTIENT
+#define FNB_F64_TINY_QUOTIENT 0
+#endif
 template <> struct Divider<double> {
     double b;
+#if FNB_F64_TINY_QUOTIENT
+    int eb;
+    __device__ __forceinline__ explicit Divider(double b_) : b(b_) { eb = biased_exp(b_); }
+#else
     __device__ __forceinline__ explicit Divider(double b_) : b(b_) {}
-    __device__ __forceinline__ double operator()(double a) const { return __ddiv_rn(a, b); }
+#endif
+    __device__ __forceinline__ double operator()(double a) const {
+#if FNB_F64_TINY_QUOTIENT
+        // Wide-range rows divide small components by large ones: results on the subnormal
+        // grid take tiny_quotient (normal or subnormal numerator, normal divisor).
+        const unsigned long long ba = (unsigned long long)__double_as_longlong(a) & 0x7FFFFFFFFFFFFFFFull;
+        int ea = (int)(ba >> 52);
+        unsigned long long ma = ba & 0x000FFFFFFFFFFFFFull;
+        if (ea == 0 && ma != 0) {  // subnormal numerator: normalise the significand
+            const int lz = __clzll((long long)ma) - 11;
+            ma = (ma << lz) & 0x000FFFFFFFFFFFFFull;
+            ea = 1 - lz;
+        }
+        if (ba != 0 && ea <= 2046 && eb >= 1 && eb <= 2046 && ea - eb <= -1024)
+            return tiny_quotient(a, b, ea, ma, eb);
+#endif
+        return __ddiv_rn(a, b);
+    }
 };
 #else
 template <> struct Divider<double> : MarksteinDivider {
