@@ -228,6 +228,80 @@ def cpu_reference_rate(x: np.ndarray, ka, reps: int = 3):
     return n / best, threads, kind, best
 
 
+def cpu_detail(ka64, ka32, sample_rows: int = 1 << 22):
+    """The CPU legs SURVEY §8(d) lists beside the T-thread reference loop (rank 0, N = 1):
+    the same reference loop on one thread; the oracle restatement *with output stores*
+    on all threads (a port, labelled so); and the reference loop on a sample of every
+    other BASELINE config, to pair each GPU config with its CPU rate."""
+    import oracle
+    from paper_1606_06508_b200 import workloads
+
+    ref = oracle.ref_module()
+    threads = len(os.sched_getaffinity(0))
+    out = {"cores_available": threads, "sample_rows": sample_rows}
+
+    def best_time(fn, reps=3):
+        best = None
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        return best
+
+    x5 = workloads.host_rows(CFG, 0, sample_rows)
+    if ref is not None:
+        flat = np.ascontiguousarray(x5.reshape(-1))
+        mask = (1 << (sample_rows - 1).bit_length()) - 1
+        t = best_time(lambda: ref.loop_scaling3_f64(flat, sample_rows, mask, *ka64))
+        out["reference_loop_1_thread"] = {"value": sample_rows / t, "unit": UNIT, "cores": 1,
+                                          "kind": "reference", "sample": f"cfg5 rows [0, {sample_rows})"}
+    t = best_time(lambda: oracle.run(oracle.OP_NORMALIZE, x5, np.array(ka64), threads=threads))
+    out["port_with_stores"] = {"value": sample_rows / t, "unit": UNIT, "cores": threads, "kind": "port",
+                               "sample": f"cfg5 rows [0, {sample_rows}), oracle normalize3 writing r and unit"}
+    per_cfg = {}
+    for cfg in (1, 2, 3, 4):
+        c = workloads.CONFIGS[cfg]
+        n = min(sample_rows, c.rows)
+        xc = workloads.host_rows(cfg, 0, n)
+        single = c.dtype == "float32"
+        rate, thr, kind, _ = cpu_loop_rate(xc, c.dim, single, ka32 if single else ka64, ref, threads)
+        per_cfg[str(cfg)] = {"value": rate, "unit": UNIT, "cores": thr, "kind": kind,
+                             "sample": f"cfg{cfg} rows [0, {n}), loop_scaling{c.dim}_{'f32' if single else 'f64'}"}
+    out["reference_loop_per_config"] = per_cfg
+    return out
+
+
+def cpu_loop_rate(x: np.ndarray, dim: int, single: bool, ka, ref, threads: int, reps: int = 3):
+    """Best-of-reps vectors/s of the reference's scaling loop of any config on all cores."""
+    import oracle
+
+    n = x.shape[0]
+    bounds = [shard_range(n, t, threads) for t in range(threads)]
+    flat = np.ascontiguousarray(x.reshape(-1))
+    loop = getattr(ref, f"loop_scaling{dim}_{'f32' if single else 'f64'}") if ref is not None else None
+
+    def work(lo, hi):
+        rows = hi - lo
+        mask = (1 << max(0, (rows - 1).bit_length())) - 1
+        if loop is not None:
+            loop(flat[lo * dim: hi * dim], rows, mask, *ka)
+        else:
+            oracle.loop(oracle.ALGO_SCALING, x[lo:hi], rows, mask, ka)
+
+    best = None
+    for _ in range(reps):
+        ts = [threading.Thread(target=work, args=b) for b in bounds]
+        t0 = time.perf_counter()
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return n / best, threads, "reference" if loop is not None else "port", best
+
+
 def run_reference_arm(args):
     rank, world, _ = _dist_env()
     if rank != 0:
@@ -558,6 +632,10 @@ def run_ours(args):
         except Exception as exc:  # never lose the headline line
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": None, "kind": None,
                                     "sample": f"failed: {exc}"}
+        try:
+            line["cpu_detail"] = cpu_detail(ka, fn.kernel_args(fn.preset("single")))
+        except Exception as exc:  # informational only
+            line["cpu_detail"] = {"error": str(exc)}
     print(json.dumps(line), flush=True)
     return 0
 
