@@ -449,3 +449,31 @@ def test_host_path_every_family_small_chunks(cuda_dev, pinned, monkeypatch):
     v = host(_random_rows(300_001, 3, False, seed=10))
     m = fn.rotation_unit((0.1, 0.2, 0.3, 0.9))
     assert oracle.same(m.apply(v), m.apply(torch.from_numpy(np.array(v)).to(cuda_dev)).cpu().numpy()).all()
+
+
+def test_in_place_outputs(cuda_dev):
+    """unit (or scaled) may alias the input rows: every row is read into the tile before
+    its own outputs are written, and rows belong to one tile only (device TMA path, the
+    unaligned per-row path and the host pipeline)."""
+    p = fn.preset("double")
+    for n in (1_000_003, 777):
+        xh = _random_rows(n, 3, False, seed=n)
+        want = fn.normalize3(p, torch.from_numpy(xh).to(cuda_dev))
+        x = torch.from_numpy(xh.copy()).to(cuda_dev)
+        r = torch.empty(n, dtype=torch.float64, device=cuda_dev)
+        fn.normalize3(p, x, out=(r, x))
+        assert torch.equal(x.view(torch.int64), want.unit.view(torch.int64))
+        assert torch.equal(r.view(torch.int64), want.length.view(torch.int64))
+        big = torch.from_numpy(np.concatenate([xh[:1], xh])).to(cuda_dev)
+        xu = big[1:]
+        fn.normalize3(p, xu, out=(r, xu))  # 8-byte aligned rows: per-row kernel
+        assert torch.equal(xu.view(torch.int64), want.unit.view(torch.int64))
+        hx = xh.copy()
+        hr = np.empty(n)
+        fn.normalize3(p, hx, out=(hr, hx))
+        assert np.array_equal(hx.view(np.int64), want.unit.cpu().numpy().view(np.int64))
+        s = torch.from_numpy(xh.copy()).to(cuda_dev)
+        inv = torch.empty(n, dtype=torch.float64, device=cuda_dev)
+        ws = fn.scale3(p, torch.from_numpy(xh).to(cuda_dev))
+        fn.scale3(p, s, out=(inv, s))
+        assert torch.equal(s.view(torch.int64), ws.scaled.view(torch.int64))
