@@ -164,8 +164,9 @@ def _loop_terms(op: int, dim: int, dt, buf, rows: int, ka) -> np.ndarray:
     x = np.ascontiguousarray(flat[: rows * dim].reshape(rows, dim))
     res = batch.run(op, dim, x, ka)
     term = res.head.astype(np.float64)
-    for k in range(dim):  # ((r + u1) + u2) + ... in double, left to right
-        term = term + res.body[:, k].astype(np.float64)
+    with np.errstate(invalid="ignore", over="ignore"):  # inf + -inf -> NaN, as in the C loop
+        for k in range(dim):  # ((r + u1) + u2) + ... in double, left to right
+            term = term + res.body[:, k].astype(np.float64)
     return term
 
 
