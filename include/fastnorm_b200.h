@@ -74,7 +74,15 @@ typedef enum {
     /* RotationMatrix.apply (rotation.py:39-41) over a batch of vectors: x = v[N,3]
      * (dim 3, FN_F64), head = R v [N,3]; the ka argument points to the 9 entries of R,
      * row-major.  out_i = ((R_i0 v_0 + R_i1 v_1) + R_i2 v_2), each operation rounded. */
-    FN_OP_ROT_APPLY = 10
+    FN_OP_ROT_APPLY = 10,
+    /* Two-input ops (fn_rotate_rows_f64 / fn_host_rotate_rows_f64 only), float64, one
+     * output record out[N,3] per row:
+     *  QUAT_ROTATE: a = q[N,4]; out_i = rotation_unit(normalize4(p, q_i).unit).apply(v_i)
+     *               (normalize.py:65 -> rotation.py:87-111 -> rotation.py:39-41); rows
+     *               with a non-finite quaternion give NaN and are counted (*invalid).
+     *  MAT_APPLY:   a = R[N,9] row-major; out_i = R_i.apply(v_i) (rotation.py:39-41). */
+    FN_OP_QUAT_ROTATE = 11,
+    FN_OP_MAT_APPLY = 12
 } fn_op;
 
 typedef enum { FN_F32 = 0, FN_F64 = 1 } fn_dtype;
@@ -120,6 +128,15 @@ int fn_run_rot(int op, const double* q, int64_t n, double* head, double* body, d
 /* RotationMatrix.apply (rotation.py:39-41) for a batch: out[N,3] = R v[N,3], R[9]
  * row-major (same as fn_run(FN_OP_ROT_APPLY, 3, FN_F64, v, n, out, NULL, NULL, R, s)). */
 int fn_rotate_apply_f64(const double R[9], const double* v, int64_t n, double* out, void* stream);
+
+/* Per-row rotation of vectors (two input arrays, see FN_OP_QUAT_ROTATE / FN_OP_MAT_APPLY):
+ * a, v, out on the device (async on stream), ka = the six double constants for
+ * QUAT_ROTATE (ignored, may be NULL, for MAT_APPLY), invalid = device uint64 counter or
+ * NULL.  The host variant takes host arrays and pipelines them like fn_host_run. */
+int fn_rotate_rows_f64(int op, const double* a, const double* v, int64_t n, double* out,
+                       const double* ka, uint64_t* invalid, void* stream);
+int fn_host_rotate_rows_f64(int op, const double* a, const double* v, int64_t n, double* out,
+                            const double* ka);
 
 /* ---- named entry points: one per reference export --------------------------------- */
 /* scale{n}_{f64,f32}      replaces _kernels.pyx:419-439 / :523-546 */

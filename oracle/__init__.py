@@ -82,6 +82,9 @@ def lib() -> ctypes.CDLL:
             L.orc_rotate_apply.restype = None
             L.orc_rotate_apply.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                            ctypes.c_void_p]
+            L.orc_rotate_rows.restype = ctypes.c_int64
+            L.orc_rotate_rows.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                          ctypes.c_void_p, ctypes.c_void_p]
             L.orc_loop.restype = ctypes.c_double
             L.orc_loop.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
                                    ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p]
@@ -167,6 +170,20 @@ def rotate_apply(R, v: np.ndarray) -> np.ndarray:
     out = np.empty_like(v)
     lib().orc_rotate_apply(Rm.ctypes.data, v.ctypes.data, v.shape[0], out.ctypes.data)
     return out
+
+
+OP_QUAT_ROTATE, OP_MAT_APPLY = 11, 12
+
+
+def rotate_rows(op: int, a: np.ndarray, v: np.ndarray, ka=None):
+    """Oracle per-row rotation: op 11 (q[N,4] normalised, rotation_unit, applied to
+    v[N,3]) or op 12 (R[N,3,3] applied to v[N,3]).  Returns (out[N,3], invalid rows)."""
+    a = np.ascontiguousarray(a, dtype=np.float64).reshape(len(v), -1)
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    out = np.empty_like(v)
+    karr, kptr = _ka_ptr(ka)
+    bad = lib().orc_rotate_rows(op, a.ctypes.data, v.ctypes.data, v.shape[0], out.ctypes.data, kptr)
+    return out, int(bad)
 
 
 def loop(algo: int, buf: np.ndarray, iters: int, mask: int, ka=None) -> float:

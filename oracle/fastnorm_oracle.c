@@ -349,4 +349,27 @@ void orc_rotate_apply(const double* R, const double* v, int64_t n, double* out) 
     }
 }
 
+/* Per-row rotation of vectors (two inputs):
+ * op 11: out_i = rotation_unit(normalize4(q_i).unit).apply(v_i)  (normalize.py:65,
+ *        rotation.py:87-111, :39-41); returns the rows whose unit quaternion is
+ *        non-finite (the reference's rotation_unit raises ValueError there; NaN here);
+ * op 12: out_i = R_i.apply(v_i) with R_i the row-major 3x3 a[9 i .. 9 i + 8]. */
+int64_t orc_rotate_rows(int op, const double* a, const double* v, int64_t n, double* out,
+                        const double* ka) {
+    int64_t bad = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        double R[9];
+        const double* M = R;
+        if (op == 11) {
+            double r, u[4];
+            normalize_d(4, ka, a + 4 * i, &r, u, 0);
+            bad += !rot_unit(u, R);
+        } else {
+            M = a + 9 * i;
+        }
+        orc_rotate_apply(M, v + 3 * i, 1, out + 3 * i);
+    }
+    return bad;
+}
+
 const char* orc_build_flags(void) { return "gcc -O3 -ffp-contract=off"; }

@@ -13,7 +13,8 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfastnorm_b200.so")
+# FASTNORM_B200_LIB points at another build of the library (A/B timing of variants).
+LIB_PATH = os.environ.get("FASTNORM_B200_LIB") or os.path.join(HERE, "libfastnorm_b200.so")
 
 # op codes / dtypes (include/fastnorm_b200.h)
 OP_SCALE = 0
@@ -27,6 +28,8 @@ OP_ROT_UNIT = 7
 OP_ROT_GENERAL = 8
 OP_NORMALIZE_ROT = 9
 OP_ROT_APPLY = 10
+OP_QUAT_ROTATE = 11
+OP_MAT_APPLY = 12
 F32 = 0
 F64 = 1
 
@@ -73,6 +76,10 @@ def _declare(L: ctypes.CDLL) -> None:
     L.fn_host_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(_vp)]
     L.fn_host_free.restype = _int
     L.fn_host_free.argtypes = [_vp]
+    L.fn_rotate_rows_f64.restype = _int
+    L.fn_rotate_rows_f64.argtypes = [_int, _vp, _vp, _i64, _vp, _vp, _vp, _vp]
+    L.fn_host_rotate_rows_f64.restype = _int
+    L.fn_host_rotate_rows_f64.argtypes = [_int, _vp, _vp, _i64, _vp, _vp]
     L.fn_rotate_apply_f64.restype = _int
     L.fn_rotate_apply_f64.argtypes = [_vp, _vp, _i64, _vp, _vp]
     L.fn_row_stats.restype = _int

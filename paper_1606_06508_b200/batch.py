@@ -204,3 +204,43 @@ def run(op: int, dim: int, x, ka_arr: np.ndarray | None, out=None, invalid=None)
         rc = L.fn_host_run(op, dim, dcode, x.ctypes.data, n, ptr(head), ptr(body), ptr(extra), kptr)
         _lib.check(rc, "fn_host_run")
     return BatchOut(head, body, extra)
+
+
+def run_rows2(op: int, a, v, ka_arr: np.ndarray | None, out=None, invalid=None):
+    """Two-input ops (per-row rotation of vectors): a = q[N, 4] (OP_QUAT_ROTATE) or
+    R[N, 9] (OP_MAT_APPLY), v[N, 3], both float64 and in the same home (CUDA tensors on
+    one device, or host arrays).  Returns out[N, 3] of the same kind.
+
+    ``invalid`` (device path): a CUDA int64 tensor the kernel adds rejected rows to."""
+    width = 4 if op == _lib.OP_QUAT_ROTATE else 9
+    n = int(v.shape[0])
+    if tuple(v.shape) != (n, 3):
+        raise ValueError(f"vectors must have shape [N, 3], got {tuple(v.shape)}")
+    if tuple(a.shape) != (n, width):
+        raise ValueError(f"expected [{n}, {width}] records for the rotations, got {tuple(a.shape)}")
+    for t, what in ((a, "rotations"), (v, "vectors")):
+        if str(t.dtype).replace("torch.", "") != "float64":
+            raise TypeError(f"{what} must be float64 (the reference computes in double)")
+    L = _lib.lib()
+    kptr = None if ka_arr is None else ka_arr.ctypes.data
+    if is_torch(a) and a.is_cuda:
+        torch = _torch()
+        if not (is_torch(v) and v.is_cuda and v.device == a.device):
+            raise ValueError("rotations and vectors must be CUDA tensors on the same device")
+        a, v = a.contiguous(), v.contiguous()
+        o = _check_out(out, (n, 3), v, "out") if out is not None else torch.empty((n, 3), dtype=v.dtype, device=v.device)
+        with torch.cuda.device(v.device):
+            rc = L.fn_rotate_rows_f64(op, a.data_ptr(), v.data_ptr(), n, o.data_ptr(), kptr,
+                                      None if invalid is None else invalid.data_ptr(),
+                                      torch.cuda.current_stream(v.device).cuda_stream)
+        _lib.check(rc, "fn_rotate_rows_f64")
+        return o
+    if is_torch(a) or is_torch(v):
+        res = run_rows2(op, np.asarray(a.numpy() if is_torch(a) else a), np.asarray(v.numpy() if is_torch(v) else v),
+                        ka_arr, None if out is None else np.asarray(out.numpy() if is_torch(out) else out))
+        return _torch().from_numpy(res) if is_torch(v) else res
+    a, v = np.ascontiguousarray(a), np.ascontiguousarray(v)
+    o = _check_out(out, (n, 3), v, "out") if out is not None else np.empty((n, 3), dtype=np.float64)
+    rc = L.fn_host_rotate_rows_f64(op, a.ctypes.data, v.ctypes.data, n, o.ctypes.data, kptr)
+    _lib.check(rc, "fn_host_rotate_rows_f64")
+    return o

@@ -75,7 +75,9 @@ static Widths op_widths(int op, int dim) {
         case FN_OP_ROT_UNIT:
         case FN_OP_ROT_GENERAL: return {9, 0, 0};
         case FN_OP_NORMALIZE_ROT: return {1, 4, 9};
-        case FN_OP_ROT_APPLY: return {3, 0, 0};
+        case FN_OP_ROT_APPLY:
+        case FN_OP_QUAT_ROTATE:
+        case FN_OP_MAT_APPLY: return {3, 0, 0};
         default: return {1, dim, 0};
     }
 }
@@ -167,8 +169,8 @@ static int ctas_per_sm_for(int64_t ntiles, int sms) {
 }
 
 template <typename T, int N, int OP>
-static int launch(const void* xv, int64_t n, void* hv, void* bv, void* qv, const KArgs<T>& ka,
-                  cudaStream_t stream) {
+static int launch(const void* xv, const void* x2v, int64_t n, void* hv, void* bv, void* qv,
+                  const KArgs<T>& ka, cudaStream_t stream) {
     using TL = TmaLaunch<T, N, OP>;
     using L = typename TL::L;
     using Op = typename L::Op;
@@ -176,24 +178,26 @@ static int launch(const void* xv, int64_t n, void* hv, void* bv, void* qv, const
     T* head = static_cast<T*>(hv);
     T* body = static_cast<T*>(bv);
     T* extra = static_cast<T*>(qv);
+    const T* x2 = static_cast<const T*>(x2v);
+    constexpr int N2 = InWidth2<Op>::value;
     if (n == 0) return FN_OK;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
     const int sms = device_sms(dev);
-    const bool aligned = aligned16(x) && aligned16(head) && (Op::W1 == 0 || aligned16(body)) &&
-                         (Op::W2 == 0 || aligned16(extra));
+    const bool aligned = aligned16(x) && (N2 == 0 || aligned16(x2)) && aligned16(head) &&
+                         (Op::W1 == 0 || aligned16(body)) && (Op::W2 == 0 || aligned16(extra));
     if (aligned && !force_direct() && n >= (int64_t)L::TR) {
         const int64_t ntiles = n / L::TR;
         const int64_t per_sm = std::min<int64_t>(TL::blocks_per_sm(dev), ctas_per_sm_for<OP>(ntiles, sms));
         const int64_t resident = per_sm * sms;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, resident));
         e = launch_pdl(tma_stream_kernel<T, N, OP>, grid, Tile<T, N>::kThreads, L::kSmemBytes,
-                       stream, x, n, head, body, extra, ka);
+                       stream, x, x2, n, head, body, extra, ka);
     } else {
         const int64_t want = (n + 255) / 256;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 8));
-        e = launch_pdl(direct_kernel<T, N, OP>, grid, 256, 0, stream, x, n, head, body, extra, ka);
+        e = launch_pdl(direct_kernel<T, N, OP>, grid, 256, 0, stream, x, x2, n, head, body, extra, ka);
     }
     if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
     e = cudaGetLastError();
@@ -254,9 +258,9 @@ template <typename T, int OP>
 static int dispatch_dim(int dim, const void* x, int64_t n, void* h, void* b, void* q,
                         const KArgs<T>& ka, cudaStream_t s) {
     switch (dim) {
-        case 2: return launch<T, 2, OP>(x, n, h, b, q, ka, s);
-        case 3: return launch<T, 3, OP>(x, n, h, b, q, ka, s);
-        case 4: return launch<T, 4, OP>(x, n, h, b, q, ka, s);
+        case 2: return launch<T, 2, OP>(x, nullptr, n, h, b, q, ka, s);
+        case 3: return launch<T, 3, OP>(x, nullptr, n, h, b, q, ka, s);
+        case 4: return launch<T, 4, OP>(x, nullptr, n, h, b, q, ka, s);
         default: return fail(FN_EINVAL, "dim must be 2, 3 or 4");
     }
 }
@@ -283,7 +287,7 @@ static int dispatch(int op, int dim, const void* x, int64_t n, void* h, void* b,
         case FN_OP_QUOTIENT: return dispatch_dim<T, FN_OP_QUOTIENT>(dim, x, n, h, b, q, ka, s);
         case FN_OP_QUOTIENT3_FAST:
             if (dim != 3) return fail(FN_EINVAL, "quotient3_fast is defined for dim 3 only");
-            return launch<T, 3, FN_OP_QUOTIENT3_FAST>(x, n, h, b, q, ka, s);
+            return launch<T, 3, FN_OP_QUOTIENT3_FAST>(x, nullptr, n, h, b, q, ka, s);
         default: return fail(FN_EINVAL, "unknown op");
     }
 }
@@ -296,10 +300,10 @@ static int dispatch_rot(int op, const void* x, int64_t n, void* h, void* b, void
     if (rc != FN_OK) return rc;
     ka.invalid = invalid;
     switch (op) {
-        case FN_OP_ROT_UNIT: return launch<double, 4, FN_OP_ROT_UNIT>(x, n, h, b, q, ka, s);
-        case FN_OP_ROT_GENERAL: return launch<double, 4, FN_OP_ROT_GENERAL>(x, n, h, b, q, ka, s);
-        case FN_OP_NORMALIZE_ROT: return launch<double, 4, FN_OP_NORMALIZE_ROT>(x, n, h, b, q, ka, s);
-        case FN_OP_ROT_APPLY: return launch<double, 3, FN_OP_ROT_APPLY>(x, n, h, b, q, ka, s);
+        case FN_OP_ROT_UNIT: return launch<double, 4, FN_OP_ROT_UNIT>(x, nullptr, n, h, b, q, ka, s);
+        case FN_OP_ROT_GENERAL: return launch<double, 4, FN_OP_ROT_GENERAL>(x, nullptr, n, h, b, q, ka, s);
+        case FN_OP_NORMALIZE_ROT: return launch<double, 4, FN_OP_NORMALIZE_ROT>(x, nullptr, n, h, b, q, ka, s);
+        case FN_OP_ROT_APPLY: return launch<double, 3, FN_OP_ROT_APPLY>(x, nullptr, n, h, b, q, ka, s);
         default: return fail(FN_EINVAL, "unknown rotation op");
     }
 }
@@ -339,6 +343,29 @@ int run_ex(int op, int dim, int dtype, const void* x, int64_t n, void* head, voi
 int run(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* body, void* sq,
         const double* ka, void* stream) {
     return run_ex(op, dim, dtype, x, n, head, body, sq, ka, nullptr, stream);
+}
+
+// Two-input ops: record width of the first input (q: 4, R: 9); the second is v[N,3].
+static int rows2_dim(int op) { return op == FN_OP_QUAT_ROTATE ? 4 : (op == FN_OP_MAT_APPLY ? 9 : 0); }
+
+static int check_rows2(int op, const void* a, const void* v, int64_t n, const void* out) {
+    if (!rows2_dim(op)) return fail(FN_EINVAL, "op must be FN_OP_QUAT_ROTATE or FN_OP_MAT_APPLY");
+    if (n < 0) return fail(FN_EINVAL, "n must be >= 0");
+    if (n > 0 && (!a || !v || !out)) return fail(FN_EINVAL, "a, v and out must not be NULL");
+    return FN_OK;
+}
+
+int run_rows2(int op, const void* a, const void* v, int64_t n, void* out, const double* kad,
+              unsigned long long* invalid, cudaStream_t s) {
+    int rc = check_rows2(op, a, v, n, out);
+    if (rc != FN_OK || n == 0) return rc;
+    KArgs<double> ka;
+    rc = make_kargs<double>(kad, op == FN_OP_QUAT_ROTATE, ka);
+    if (rc != FN_OK) return rc;
+    ka.invalid = invalid;
+    if (op == FN_OP_QUAT_ROTATE)
+        return launch<double, 4, FN_OP_QUAT_ROTATE>(a, v, n, out, nullptr, nullptr, ka, s);
+    return launch<double, 9, FN_OP_MAT_APPLY>(a, v, n, out, nullptr, nullptr, ka, s);
 }
 
 // ---------------------------------------------------------------------------------
@@ -524,9 +551,10 @@ static int host_staging_get(Staging* st, size_t bytes_per_pipe) {
     return FN_OK;
 }
 
-int host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* body,
-             void* sq, const double* ka) {
-    int rc = check_args(op, dim, dtype, x, n, head, body, sq);
+// x2 / dim2: the second input of the two-input ops (NULL / 0 otherwise).
+static int host_run_impl(int op, int dim, int dtype, const void* x, const void* x2, int dim2, int64_t n,
+                         void* head, void* body, void* sq, const double* ka) {
+    int rc = x2 ? check_rows2(op, x, x2, n, head) : check_args(op, dim, dtype, x, n, head, body, sq);
     if (rc != FN_OK || n == 0) return rc;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
@@ -535,22 +563,25 @@ int host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, v
     const Widths wd = op_widths(op, dim);
     // ~48 MiB of input per chunk: three chunks in flight, per-copy latency amortised.
     const int64_t chunk_mb = env_int("FASTNORM_B200_HOST_CHUNK_MB", 48, 1, 1024);
-    const int64_t chunk_rows = std::max<int64_t>(4096, (chunk_mb << 20) / (int64_t)(dim * w));
+    const int64_t chunk_rows = std::max<int64_t>(4096, (chunk_mb << 20) / (int64_t)((dim + dim2) * w));
     const int64_t rows = std::min<int64_t>(n, chunk_rows);
-    const size_t bx = align256(rows * dim * w), b0 = align256(rows * wd.w0 * w),
-                 b1 = align256(rows * wd.w1 * w), b2 = align256(rows * wd.w2 * w);
+    const size_t bx = align256(rows * dim * w), bx2 = align256(rows * dim2 * w),
+                 b0 = align256(rows * wd.w0 * w), b1 = align256(rows * wd.w1 * w),
+                 b2 = align256(rows * wd.w2 * w);
+    const size_t per_pipe = bx + bx2 + b0 + b1 + b2;
     std::lock_guard<std::mutex> lk(device_mutex(dev));
     Staging* st = nullptr;
-    rc = staging_get(dev, bx + b0 + b1 + b2, &st);
+    rc = staging_get(dev, per_pipe, &st);
     if (rc != FN_OK) return rc;
     // Pageable caller memory cannot be DMA'd asynchronously: such sides go through
     // page-locked staging filled / drained by the parallel host copier, overlapped with
     // the transfers and kernels of the other pipes.
     const bool stage_in = !is_page_locked(x);
+    const bool stage_in2 = x2 && !is_page_locked(x2);
     const bool stage_out = !is_page_locked(head) || (wd.w1 && !is_page_locked(body)) ||
                            (wd.w2 && !is_page_locked(sq));
-    if (stage_in || stage_out) {
-        rc = host_staging_get(st, bx + b0 + b1 + b2);
+    if (stage_in || stage_in2 || stage_out) {
+        rc = host_staging_get(st, per_pipe);
         if (rc != FN_OK) return rc;
     }
     struct Pending {
@@ -559,7 +590,7 @@ int host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, v
     } pending[Staging::kMaxPipes];
     char* const outs[3] = {static_cast<char*>(head), static_cast<char*>(body), static_cast<char*>(sq)};
     const int ws[3] = {wd.w0, wd.w1, wd.w2};
-    const size_t offs[3] = {bx, bx + b0, bx + b0 + b1};
+    const size_t offs[3] = {bx + bx2, bx + bx2 + b0, bx + bx2 + b0 + b1};
     auto drain = [&](int p) -> int {
         if (!pending[p].live) return FN_OK;
         cudaError_t ee = cudaEventSynchronize(st->done[p]);
@@ -592,7 +623,19 @@ int host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, v
         }
         e = cudaMemcpyAsync(dx, src, m * dim * w, cudaMemcpyHostToDevice, s);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync H2D");
-        rc = run(op, dim, dtype, dx, m, dptr[0], dptr[1], dptr[2], ka, s);
+        if (x2) {
+            void* dx2 = base + bx;
+            const char* src2 = static_cast<const char*>(x2) + r0 * dim2 * w;
+            if (stage_in2) {
+                copy_pool().copy(hbase + bx, src2, m * dim2 * w);
+                src2 = hbase + bx;
+            }
+            e = cudaMemcpyAsync(dx2, src2, m * dim2 * w, cudaMemcpyHostToDevice, s);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync H2D");
+            rc = run_rows2(op, dx, dx2, m, dptr[0], ka, nullptr, s);
+        } else {
+            rc = run(op, dim, dtype, dx, m, dptr[0], dptr[1], dptr[2], ka, s);
+        }
         if (rc != FN_OK) return rc;
         for (int k = 0; k < 3 && e == cudaSuccess; ++k) {
             if (!ws[k]) continue;
@@ -613,6 +656,11 @@ int host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, v
         if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
     }
     return FN_OK;
+}
+
+int host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* body,
+             void* sq, const double* ka) {
+    return host_run_impl(op, dim, dtype, x, nullptr, 0, n, head, body, sq, ka);
 }
 
 // ---------------------------------------------------------------------------------
@@ -863,6 +911,19 @@ int fn_scalar(int op, int dim, int dtype, const double* x, double* out, const do
 int fn_host_run_multi(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* body,
                       void* sq, const double* ka, const int* devices, int ndev) {
     return fnb::host_run_multi(op, dim, dtype, x, n, head, body, sq, ka, devices, ndev);
+}
+
+int fn_rotate_rows_f64(int op, const double* a, const double* v, int64_t n, double* out,
+                       const double* ka, uint64_t* invalid, void* stream) {
+    return fnb::run_rows2(op, a, v, n, out, ka, reinterpret_cast<unsigned long long*>(invalid),
+                          static_cast<cudaStream_t>(stream));
+}
+
+int fn_host_rotate_rows_f64(int op, const double* a, const double* v, int64_t n, double* out,
+                            const double* ka) {
+    const int rc = fnb::check_rows2(op, a, v, n, out);
+    if (rc != FN_OK || n == 0) return rc;
+    return fnb::host_run_impl(op, fnb::rows2_dim(op), FN_F64, a, v, 3, n, out, nullptr, nullptr, ka);
 }
 
 int fn_rotate_apply_f64(const double R[9], const double* v, int64_t n, double* out, void* stream) {

@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "fastnorm_math.cuh"
 #include "../../include/fastnorm_b200.h"
@@ -121,18 +122,64 @@ template <typename T, int N> struct RowOp<T, N, FN_OP_ROT_APPLY> {
     }
 };
 
+// Two-input ops (a second AoS record per row, N2 wide): per-row rotation of vectors.
+// normalize4 -> rotation_unit of its unit output -> apply to v: the reference
+// composition rotation_unit(normalize4(p, *q).unit).apply(v) (rotation.py:39-41, 87-111).
+template <typename T, int N> struct RowOp<T, N, FN_OP_QUAT_ROTATE> {
+    static_assert(N == 4, "quaternions");
+    static constexpr int W0 = 3, W1 = 0, W2 = 0, N2 = 3;
+    __device__ __forceinline__ static bool apply2(const T (&q)[N], const T (&v)[3], const KArgs<T>& ka,
+                                                  T* o0, T*, T*) {
+        T r, u[4], sq, R[9];
+        normalize_row<T, 4, false>(q, ka, r, u, sq);
+        const bool ok = rotation_unit_row(u, R);
+        rotation_apply_row(v, R, o0);
+        return ok;
+    }
+};
+// Per-row RotationMatrix.apply: R[N,9] (row-major) times v[N,3].
+template <typename T, int N> struct RowOp<T, N, FN_OP_MAT_APPLY> {
+    static_assert(N == 9, "row-major 3x3 matrices");
+    static constexpr int W0 = 3, W1 = 0, W2 = 0, N2 = 3;
+    __device__ __forceinline__ static bool apply2(const T (&R)[N], const T (&v)[3], const KArgs<T>&, T* o0,
+                                                  T*, T*) {
+        rotation_apply_row(v, R, o0);
+        return true;
+    }
+};
+
+// Width of an op's second input record (0: single-input op).
+template <typename Op, typename = void> struct InWidth2 {
+    static constexpr int value = 0;
+};
+template <typename Op> struct InWidth2<Op, std::void_t<decltype(Op::N2)>> {
+    static constexpr int value = Op::N2;
+};
+
 template <int W> struct Slot { static constexpr int value = W > 0 ? W : 1; };
+
+template <typename Op, typename T, int N, int N2S>
+__device__ __forceinline__ bool apply_op(const T (&x)[N], const T (&x2)[N2S], const KArgs<T>& ka, T* o0, T* o1,
+                                         T* o2) {
+    if constexpr (InWidth2<Op>::value > 0)
+        return Op::apply2(x, x2, ka, o0, o1, o2);
+    else
+        return Op::apply(x, ka, o0, o1, o2);
+}
 
 // One row through global memory (tails, unaligned arrays, tiny batches).
 template <typename T, int N, int OP>
-__device__ __forceinline__ bool row_global(const T* __restrict__ x, int64_t i, T* __restrict__ head,
-                                           T* __restrict__ body, T* __restrict__ extra,
-                                           const KArgs<T>& ka) {
+__device__ __forceinline__ bool row_global(const T* __restrict__ x, const T* __restrict__ x2, int64_t i,
+                                           T* __restrict__ head, T* __restrict__ body,
+                                           T* __restrict__ extra, const KArgs<T>& ka) {
     using Op = RowOp<T, N, OP>;
-    T xr[N], o0[Slot<Op::W0>::value], o1[Slot<Op::W1>::value], o2[Slot<Op::W2>::value];
+    constexpr int N2 = InWidth2<Op>::value;
+    T xr[N], x2r[Slot<N2>::value], o0[Slot<Op::W0>::value], o1[Slot<Op::W1>::value], o2[Slot<Op::W2>::value];
 #pragma unroll
     for (int c = 0; c < N; ++c) xr[c] = __ldg(x + i * N + c);
-    const bool ok = Op::apply(xr, ka, o0, o1, o2);
+#pragma unroll
+    for (int c = 0; c < N2; ++c) x2r[c] = __ldg(x2 + i * N2 + c);
+    const bool ok = apply_op<Op>(xr, x2r, ka, o0, o1, o2);
 #pragma unroll
     for (int c = 0; c < Op::W0; ++c) head[i * Op::W0 + c] = o0[c];
 #pragma unroll
@@ -163,9 +210,10 @@ __device__ __forceinline__ void grid_launch_dependents() {
 }
 
 template <typename T, int N, int OP>
-__global__ void __launch_bounds__(256) direct_kernel(const T* __restrict__ x, int64_t nrows,
-                                                     T* __restrict__ head, T* __restrict__ body,
-                                                     T* __restrict__ extra, KArgs<T> ka) {
+__global__ void __launch_bounds__(256) direct_kernel(const T* __restrict__ x, const T* __restrict__ x2,
+                                                     int64_t nrows, T* __restrict__ head,
+                                                     T* __restrict__ body, T* __restrict__ extra,
+                                                     KArgs<T> ka) {
     grid_dependency_wait();
     grid_launch_dependents();
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -174,7 +222,7 @@ __global__ void __launch_bounds__(256) direct_kernel(const T* __restrict__ x, in
     const int64_t trips = nrows > start ? (nrows - 1 - start) / stride + 1 : 0;
     // uniform trip count per warp so the shuffle-reduce below sees every lane
     for (int64_t t = 0, i = start; t < trips; ++t, i += stride)
-        bad += row_global<T, N, OP>(x, i, head, body, extra, ka) ? 0 : 1;
+        bad += row_global<T, N, OP>(x, x2, i, head, body, extra, ka) ? 0 : 1;
     count_invalid(ka.invalid, bad);
 }
 
@@ -308,12 +356,14 @@ template <typename T, int N, int OP, int TR_, int S_, int OB_ = OutTiles<OP>::va
     static constexpr int OB = OB_;  // output staging tiles (bulk-store groups in flight)
     static_assert(OB >= 3, "the store pipeline keeps OB - 2 groups reading behind the current one");
     static constexpr int kInBytes = TR * N * (int)sizeof(T);
+    static constexpr int kIn2Bytes = TR * InWidth2<Op>::value * (int)sizeof(T);  // second input
     static constexpr int kB0 = TR * Op::W0 * (int)sizeof(T);
     static constexpr int kB1 = TR * Op::W1 * (int)sizeof(T);
     static constexpr int kB2 = TR * Op::W2 * (int)sizeof(T);
     static constexpr int kOutBytes = kB0 + kB1 + kB2;
-    static constexpr int kSmemBytes = S * kInBytes + OB * kOutBytes + S * 8;
-    static_assert(kInBytes % 16 == 0 && kB0 % 16 == 0 && kB1 % 16 == 0 && kB2 % 16 == 0,
+    static constexpr int kSmemBytes = S * (kInBytes + kIn2Bytes) + OB * kOutBytes + S * 8;
+    static_assert(kInBytes % 16 == 0 && kIn2Bytes % 16 == 0 && kB0 % 16 == 0 && kB1 % 16 == 0 &&
+                      kB2 % 16 == 0,
                   "bulk copies need 16 B multiples");
 };
 
@@ -324,20 +374,43 @@ template <typename T, int N, int OP> struct OpRows {
     static constexpr int value = (3 * kOutRow * Tile<T, N>::kRows > 65536) ? Tile<T, N>::kRows / 2 : Tile<T, N>::kRows;
 };
 
+// Per-row matrices are 72 B records: the default 8 KiB stage would hold only 64 of them
+// (5840 GB/s).  256 rows x 3 stages (18 KiB of matrices + 6 KiB of vectors per stage)
+// reach 6900 GB/s, 1.05 of the measured copy peak (read-dominated traffic,
+// profiles/r01bw_mat.txt).
+#ifndef FNB_MAT_APPLY_ROWS
+#define FNB_MAT_APPLY_ROWS 256
+#endif
+#ifndef FNB_MAT_APPLY_STAGES
+#define FNB_MAT_APPLY_STAGES 3
+#endif
+template <typename T> struct OpRows<T, 9, FN_OP_MAT_APPLY> {
+    static constexpr int value = FNB_MAT_APPLY_ROWS;
+};
+template <typename T> struct Tile<T, 9> {
+    static constexpr int kRows = FNB_MAT_APPLY_ROWS;
+    static constexpr int kStages = FNB_MAT_APPLY_STAGES;
+    static constexpr int kThreads = 256;
+    static constexpr int kHints = 0;
+};
+
 // HINTS: bit 0 -> input loads carry an L2 evict-first policy (read once);
 //        bit 1 -> output bulk stores carry an L2 evict-first policy.
 template <typename T, int N, int OP, int TR_ = OpRows<T, N, OP>::value, int S_ = Tile<T, N>::kStages,
           int NT = Tile<T, N>::kThreads, int HINTS = Tile<T, N>::kHints, int OB_ = OutTiles<OP>::value>
-__global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x, int64_t nrows,
-                                                        T* __restrict__ head, T* __restrict__ body,
-                                                        T* __restrict__ extra, KArgs<T> ka) {
+__global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x, const T* __restrict__ x2,
+                                                        int64_t nrows, T* __restrict__ head,
+                                                        T* __restrict__ body, T* __restrict__ extra,
+                                                        KArgs<T> ka) {
     using L = TileLayout<T, N, OP, TR_, S_, OB_>;
     using Op = typename L::Op;
     constexpr int TR = L::TR, S = L::S, OB = L::OB;
     constexpr int W0 = Op::W0, W1 = Op::W1, W2 = Op::W2;
+    constexpr int N2 = InWidth2<Op>::value;
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned char* s_in = smem;
-    unsigned char* s_out = smem + S * L::kInBytes;
+    unsigned char* s_in2 = smem + S * L::kInBytes;  // second input ring (two-input ops)
+    unsigned char* s_out = s_in2 + S * L::kIn2Bytes;
     uint64_t* full = reinterpret_cast<uint64_t*>(s_out + OB * L::kOutBytes);
 
     const int64_t ntiles = nrows / TR;
@@ -356,15 +429,18 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
     __syncthreads();
     grid_dependency_wait();
     grid_launch_dependents();
+    // One stage = the tile's input records (and its second-input records), one mbarrier.
+    auto load_stage = [&](int st, int64_t tile) {
+        mbar_arrive_expect_tx(&full[st], L::kInBytes + L::kIn2Bytes);
+        if (HINTS & 1)
+            bulk_load(s_in + st * L::kInBytes, x + tile * TR * N, L::kInBytes, &full[st], policy);
+        else
+            bulk_load_plain(s_in + st * L::kInBytes, x + tile * TR * N, L::kInBytes, &full[st]);
+        if constexpr (N2 > 0)
+            bulk_load_plain(s_in2 + st * L::kIn2Bytes, x2 + tile * TR * N2, L::kIn2Bytes, &full[st]);
+    };
     if (leader) {
-        for (int64_t k = 0; k < my_tiles && k < S; ++k) {
-            const int64_t tile = (int64_t)blockIdx.x + k * gridDim.x;
-            mbar_arrive_expect_tx(&full[k], L::kInBytes);
-            if (HINTS & 1)
-                bulk_load(s_in + k * L::kInBytes, x + tile * TR * N, L::kInBytes, &full[k], policy);
-            else
-                bulk_load_plain(s_in + k * L::kInBytes, x + tile * TR * N, L::kInBytes, &full[k]);
-        }
+        for (int64_t k = 0; k < my_tiles && k < S; ++k) load_stage((int)k, (int64_t)blockIdx.x + k * gridDim.x);
     }
 
     for (int64_t k = 0; k < my_tiles; ++k) {
@@ -375,14 +451,17 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
         mbar_wait(&full[s], parity);
 
         const T* tin = reinterpret_cast<const T*>(s_in + s * L::kInBytes);
+        const T* tin2 = reinterpret_cast<const T*>(s_in2 + s * L::kIn2Bytes);
         T* t0 = reinterpret_cast<T*>(s_out + ob * L::kOutBytes);
         T* t1 = t0 + TR * W0;
         T* t2 = t1 + TR * W1;
         auto row = [&](int j) {
-            T xr[N], o0[Slot<W0>::value], o1[Slot<W1>::value], o2[Slot<W2>::value];
+            T xr[N], x2r[Slot<N2>::value], o0[Slot<W0>::value], o1[Slot<W1>::value], o2[Slot<W2>::value];
 #pragma unroll
             for (int c = 0; c < N; ++c) xr[c] = tin[j * N + c];
-            bad += Op::apply(xr, ka, o0, o1, o2) ? 0 : 1;
+#pragma unroll
+            for (int c = 0; c < N2; ++c) x2r[c] = tin2[j * N2 + c];
+            bad += apply_op<Op>(xr, x2r, ka, o0, o1, o2) ? 0 : 1;
 #pragma unroll
             for (int c = 0; c < W0; ++c) t0[j * W0 + c] = o0[c];
 #pragma unroll
@@ -411,14 +490,7 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
                 if (W2) bulk_store(extra + row0 * W2, t2, L::kB2);
             }
             bulk_commit();
-            if (k + S < my_tiles) {
-                const int64_t nt = tile + (int64_t)S * gridDim.x;
-                mbar_arrive_expect_tx(&full[s], L::kInBytes);
-                if (HINTS & 1)
-                    bulk_load(s_in + s * L::kInBytes, x + nt * TR * N, L::kInBytes, &full[s], policy);
-                else
-                    bulk_load_plain(s_in + s * L::kInBytes, x + nt * TR * N, L::kInBytes, &full[s]);
-            }
+            if (k + S < my_tiles) load_stage(s, tile + (int64_t)S * gridDim.x);
             // Threads write staging tile (k+2) % OB after the next __syncthreads, so group
             // k+2-OB must have been read out by then: at most OB-2 groups stay pending.
             bulk_wait_read<OB - 2>();
@@ -431,7 +503,7 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
         const int64_t tail = nrows - ntiles * TR;
         for (int64_t j = threadIdx.x & ~31; j < tail; j += NT) {
             const int64_t i = ntiles * TR + j + (threadIdx.x & 31);
-            if (i < nrows) bad += row_global<T, N, OP>(x, i, head, body, extra, ka) ? 0 : 1;
+            if (i < nrows) bad += row_global<T, N, OP>(x, x2, i, head, body, extra, ka) ? 0 : 1;
         }
     }
     count_invalid(ka.invalid, bad);

@@ -29,7 +29,7 @@ from paper_1606_06508_b200.params import FpParams, preset
 from paper_1606_06508_b200.scale import check_precision, kernel_args_array
 
 __all__ = ["RotationMatrix", "NormalizeRotationOutcome", "rotation_general", "rotation_unit",
-           "normalize4_rotation", "rotate_vectors"]
+           "normalize4_rotation", "rotate_vectors", "normalize4_rotate", "apply_rotations"]
 
 Row = tuple[float, float, float]
 
@@ -161,3 +161,41 @@ def normalize4_rotation(p: FpParams, q, out=None) -> NormalizeRotationOutcome:
         raise TypeError("normalize4_rotation computes in double precision")
     res = batch.run(_lib.OP_NORMALIZE_ROT, 4, q, kernel_args_array(p), out=out)
     return NormalizeRotationOutcome(res.head, res.body, res.sq)
+
+
+def normalize4_rotate(p: FpParams, q, v, out=None, strict: bool = True):
+    """Rotate every vector v[i] by its own quaternion q[i] in one pass:
+    ``rotation_unit(normalize4(p, *q[i]).unit).apply(v[i])`` bit for bit
+    (normalize.py:65, rotation.py:87-111, :39-41), without materialising the unit
+    quaternions or the matrices (56 B in, 24 B out per row).
+
+    ``q``: [N, 4], ``v``: [N, 3], float64, both CUDA tensors on one device or both host
+    arrays.  Rows with a non-finite quaternion -- where the reference's rotation_unit
+    raises ValueError -- come back as NaN and, with ``strict`` (default), make the call
+    raise ValueError after the kernel ran."""
+    check_precision(p, q)
+    if p.precision != "double":
+        raise TypeError("normalize4_rotate computes in double precision")
+    ka = kernel_args_array(p)
+    if batch.is_torch(q) and q.is_cuda:
+        import torch
+
+        invalid = torch.zeros(1, dtype=torch.int64, device=q.device)
+        res = batch.run_rows2(_lib.OP_QUAT_ROTATE, q, v, ka, out=out, invalid=invalid)
+        bad = int(invalid.item()) if strict else 0
+    else:
+        res = batch.run_rows2(_lib.OP_QUAT_ROTATE, q, v, ka, out=out)
+        qa = q.numpy() if batch.is_torch(q) else np.asarray(q)
+        bad = int((~np.isfinite(qa).all(axis=1)).sum()) if strict else 0
+    if bad:
+        raise ValueError(f"normalize4_rotate: {bad} quaternion(s) are non-finite")
+    return res
+
+
+def apply_rotations(R, v, out=None):
+    """Per-row ``RotationMatrix.apply`` (rotation.py:39-41): out[i] = R[i] @ v[i] with the
+    reference's evaluation order.  ``R``: [N, 3, 3] or [N, 9] row-major, ``v``: [N, 3],
+    float64, same home (CUDA tensors on one device, or host arrays)."""
+    n = int(v.shape[0])
+    Rf = R.reshape(n, 9)
+    return batch.run_rows2(_lib.OP_MAT_APPLY, Rf, v, None, out=out)

@@ -234,6 +234,25 @@ def main():
     out["rot_apply_R"] = np.array([m.flat() for m in mats])
     out["rot_apply_v"] = vecs
     out["rot_apply_out"] = np.array([[m.apply(tuple(v)) for v in vecs.tolist()] for m in mats])
+    # per-row rotation of vectors (two inputs): the reference composition
+    # rotation_unit(normalize4(q).unit).apply(v) per quaternion (ValueError -> NaN row), and
+    # RotationMatrix.apply of every rotation_general golden matrix to its own vector.
+    nq = len(q)
+    v_rows = np.concatenate([random_rows(rng, nq // 2, 3, False), rng.standard_normal((nq - nq // 2, 3))])
+    sp = SPECIALS["f64"]
+    for i in range(0, nq, 37):  # special values sprinkled over the vectors
+        v_rows[i, i % 3] = sp[(i // 37) % len(sp)]
+    qrot = []
+    for urow, vrow in zip(units.tolist(), v_rows.tolist()):
+        try:
+            qrot.append(rot.rotation_unit(urow).apply(tuple(vrow)))
+        except ValueError:
+            qrot.append((math.nan,) * 3)
+    out["rot_rows_v"] = v_rows
+    out["rot_rows_quat_out"] = np.array(qrot)
+    mats = [tuple(tuple(m[3 * k:3 * k + 3]) for k in range(3)) for m in out["rot_general"].tolist()]
+    out["rot_rows_mat_out"] = np.array([rot.RotationMatrix(m).apply(tuple(vrow))
+                                        for m, vrow in zip(mats, v_rows.tolist())])
     path = os.path.join(HERE, "golden_vectors.npz")
     np.savez_compressed(path, **out)
     n = sum(v.size for v in out.values())

@@ -79,6 +79,13 @@ def test_argument_errors_without_gpu():
     assert L.fn_run(10, 3, 1, x.ctypes.data, 4, b.ctypes.data, b.ctypes.data, None, ka.ctypes.data, None) == -1
     assert L.fn_rotate_apply_f64(None, x.ctypes.data, 4, b.ctypes.data, None) == -1
     assert b"matrix" in L.fn_last_error()
+    # two-input rotations: op, n and pointers are checked before any device work
+    assert L.fn_rotate_rows_f64(1, x.ctypes.data, x.ctypes.data, 4, b.ctypes.data, ka.ctypes.data, None, None) == -1
+    assert L.fn_rotate_rows_f64(11, x.ctypes.data, x.ctypes.data, -1, b.ctypes.data, ka.ctypes.data, None, None) == -1
+    assert L.fn_rotate_rows_f64(12, None, x.ctypes.data, 4, b.ctypes.data, None, None, None) == -1
+    assert L.fn_rotate_rows_f64(11, vp(0), vp(0), 0, vp(0), None, None, None) == 0
+    assert L.fn_host_rotate_rows_f64(13, x.ctypes.data, x.ctypes.data, 4, b.ctypes.data, None) == -1
+    assert L.fn_host_rotate_rows_f64(12, x.ctypes.data, x.ctypes.data, 4, None, None) == -1
     # n == 0 is a no-op success
     assert L.fn_run(1, 3, 1, vp(0), 0, vp(0), vp(0), None, ka.ctypes.data, None) == 0
     assert L.fn_host_run(1, 3, 1, vp(0), 0, vp(0), vp(0), None, ka.ctypes.data) == 0

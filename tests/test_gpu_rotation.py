@@ -122,3 +122,53 @@ def test_rotate_vectors_full_size(cuda_dev):
             assert oracle.same(to_np(out[lo:lo + chunk]), oracle.rotate_apply(m.flat(), vh)).all()
     with pytest.raises(TypeError):
         fn.rotation_unit(q).apply(v.float())
+
+
+@pytest.mark.parametrize("where", ["device", "device_unaligned", "host", "host_pinned"])
+def test_rotate_rows_golden(golden, cuda_dev, where):
+    """Per-row rotation of vectors (two-input kernels) == the reference composition on every
+    golden row: normalize4 -> rotation_unit -> apply, and per-row RotationMatrix.apply."""
+    q, v, Rg = golden["rot_q"], golden["rot_rows_v"], golden["rot_general"]
+    p = fn.preset("double")
+
+    def home(a):
+        if where == "device":
+            return torch.from_numpy(a).to(cuda_dev)
+        if where == "device_unaligned":
+            return torch.from_numpy(np.concatenate([a[:1], a])).to(cuda_dev)[1:]
+        if where == "host_pinned":
+            return torch.from_numpy(a).pin_memory().numpy()
+        return a
+
+    got = fn.normalize4_rotate(p, home(q), home(v), strict=False)
+    assert oracle.same(to_np(got) if hasattr(got, "cpu") else got, golden["rot_rows_quat_out"]).all()
+    got = fn.apply_rotations(home(Rg), home(v))
+    assert oracle.same(to_np(got) if hasattr(got, "cpu") else got, golden["rot_rows_mat_out"]).all()
+    with pytest.raises(ValueError):
+        fn.normalize4_rotate(p, home(q), home(v))  # three non-finite quaternions
+
+
+def test_rotate_rows_full_size(cuda_dev):
+    """2^27 config-3 quaternions rotating 2^27 config-5-class vectors, vs the oracle, and
+    the per-row matrix form on the rotation_unit matrices of the same quaternions."""
+    n = workloads.CONFIGS[3].rows
+    p = fn.preset("double")
+    ka = np.array(fn.kernel_args(p))
+    q = torch.empty((n, 4), dtype=torch.float64, device=cuda_dev)
+    workloads.generate_device(3, q)
+    v = torch.empty((n, 3), dtype=torch.float64, device=cuda_dev)
+    workloads.generate_device(5, v)
+    out = fn.normalize4_rotate(p, q, v)
+    torch.cuda.synchronize()
+    chunk = 1 << 24
+    for lo in range(0, n, chunk):
+        want, bad = oracle.rotate_rows(oracle.OP_QUAT_ROTATE, to_np(q[lo:lo + chunk]), to_np(v[lo:lo + chunk]), ka)
+        assert bad == 0 and oracle.same(to_np(out[lo:lo + chunk]), want).all()
+    sub = 1 << 22
+    R = fn.rotation_unit(q[:sub])
+    out2 = fn.apply_rotations(R, v[:sub])
+    want2, _ = oracle.rotate_rows(oracle.OP_MAT_APPLY, to_np(R).reshape(sub, 9), to_np(v[:sub]))
+    assert oracle.same(to_np(out2), want2).all()
+    # the fused path equals the three-step composition on the device
+    u = fn.normalize4(p, q[:sub]).unit
+    assert oracle.same(to_np(out[:sub]), to_np(fn.apply_rotations(fn.rotation_unit(u), v[:sub]))).all()

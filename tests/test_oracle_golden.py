@@ -78,3 +78,14 @@ def test_oracle_rotate_apply_matches_reference_golden(golden, oracle_mod):
     v = golden["rot_apply_v"]
     for R, want in zip(golden["rot_apply_R"], golden["rot_apply_out"]):
         assert oracle_mod.same(oracle_mod.rotate_apply(R, v), want).all()
+
+
+def test_oracle_rotate_rows_match_reference_golden(golden, oracle_mod):
+    """Per-row rotation of vectors, as the reference composes it:
+    rotation_unit(normalize4(q).unit).apply(v) per row (ValueError rows stored as NaN) and
+    RotationMatrix.apply of each rotation_general matrix to its own vector."""
+    q, v, ka = golden["rot_q"], golden["rot_rows_v"], golden["f64_ka"]
+    out, bad = oracle_mod.rotate_rows(oracle_mod.OP_QUAT_ROTATE, q, v, ka)
+    assert oracle_mod.same(out, golden["rot_rows_quat_out"]).all() and bad == 3
+    out, bad = oracle_mod.rotate_rows(oracle_mod.OP_MAT_APPLY, golden["rot_general"], v)
+    assert oracle_mod.same(out, golden["rot_rows_mat_out"]).all() and bad == 0

@@ -82,9 +82,9 @@ float time_variant(const Bufs& b, int cps, int reps, int sms, int* occ_out) {
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
-    for (int i = 0; i < 2; ++i) kern<<<grid, NT, L::kSmemBytes>>>(x, b.n, h, bd, q, ka);
+    for (int i = 0; i < 2; ++i) kern<<<grid, NT, L::kSmemBytes>>>(x, (const T*)b.b, b.n, h, bd, q, ka);
     CK(cudaEventRecord(e0));
-    for (int i = 0; i < reps; ++i) kern<<<grid, NT, L::kSmemBytes>>>(x, b.n, h, bd, q, ka);
+    for (int i = 0; i < reps; ++i) kern<<<grid, NT, L::kSmemBytes>>>(x, (const T*)b.b, b.n, h, bd, q, ka);
     CK(cudaEventRecord(e1));
     CK(cudaEventSynchronize(e1));
     CK(cudaGetLastError());
