@@ -88,7 +88,7 @@ static bool is_rotation(int op) {
 
 // Per-instantiation occupancy (computed once per process and device).
 template <typename T, int N, int OP> struct TmaLaunch {
-    using L = TileLayout<T, N, OP, OpRows<T, N, OP>::value, Tile<T, N>::kStages>;
+    using L = TileLayout<T, N, OP, OpRows<T, N, OP>::value, OpStages<T, N, OP>::value>;
     static int blocks_per_sm(int dev) {
         static std::mutex mu;
         static int cache[64] = {0};

@@ -394,9 +394,27 @@ template <typename T> struct Tile<T, 9> {
     static constexpr int kHints = 0;
 };
 
+// Stages per op: the (T, N) default; the fused normalize4 -> rotation (144 B per row,
+// 112 B of it written) is tunable through FNB_NROT_ROWS / FNB_NROT_STAGES.  Through the
+// library (profiles/r01ca_nrot.txt): 128 x 3 (default) 6267 GB/s, 256 x 2 6308,
+// 128 x 4 5994, 256 x 3 5880 -- the tuner's ranking (r01bz_rot.csv) does not carry over.
+template <typename T, int N, int OP> struct OpStages {
+    static constexpr int value = Tile<T, N>::kStages;
+};
+#ifdef FNB_NROT_STAGES
+template <typename T, int N> struct OpStages<T, N, FN_OP_NORMALIZE_ROT> {
+    static constexpr int value = FNB_NROT_STAGES;
+};
+#endif
+#ifdef FNB_NROT_ROWS
+template <typename T, int N> struct OpRows<T, N, FN_OP_NORMALIZE_ROT> {
+    static constexpr int value = FNB_NROT_ROWS;
+};
+#endif
+
 // HINTS: bit 0 -> input loads carry an L2 evict-first policy (read once);
 //        bit 1 -> output bulk stores carry an L2 evict-first policy.
-template <typename T, int N, int OP, int TR_ = OpRows<T, N, OP>::value, int S_ = Tile<T, N>::kStages,
+template <typename T, int N, int OP, int TR_ = OpRows<T, N, OP>::value, int S_ = OpStages<T, N, OP>::value,
           int NT = Tile<T, N>::kThreads, int HINTS = Tile<T, N>::kHints, int OB_ = OutTiles<OP>::value>
 __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x, const T* __restrict__ x2,
                                                         int64_t nrows, T* __restrict__ head,

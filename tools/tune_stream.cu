@@ -227,6 +227,10 @@ int main(int argc, char** argv) {
         vs.push_back(VO("rotation_unit_f64", 3, double, 4, FN_OP_ROT_UNIT, 256, 3, 256, 0, 2, 5));
         vs.push_back(VO("rotation_unit_f64", 3, double, 4, FN_OP_ROT_UNIT, 128, 3, 128, 0, 3, 4));
         vs.push_back(VO("rotation_unit_f64", 3, double, 4, FN_OP_ROT_UNIT, 128, 3, 128, 0, 3, 6));
+        vs.push_back(VO("normalize4_rot_f64", 3, double, 4, FN_OP_NORMALIZE_ROT, 256, 3, 256, 0, 2, 3));
+        vs.push_back(VO("normalize4_rot_f64", 3, double, 4, FN_OP_NORMALIZE_ROT, 256, 2, 256, 0, 2, 3));
+        vs.push_back(VO("normalize4_rot_f64", 3, double, 4, FN_OP_NORMALIZE_ROT, 128, 4, 256, 0, 2, 3));
+        vs.push_back(VO("normalize4_rot_f64", 3, double, 4, FN_OP_NORMALIZE_ROT, 128, 3, 256, 0, 3, 3));
         vs.push_back(VO("normalize4_rot_f64", 3, double, 4, FN_OP_NORMALIZE_ROT, 128, 3, 256, 0, 2, 4));
         vs.push_back(VO("normalize4_rot_f64", 3, double, 4, FN_OP_NORMALIZE_ROT, 128, 3, 256, 0, 2, 5));
         vs.push_back(VO("normalize3_f64", 5, double, 3, FN_OP_NORMALIZE, 256, 4, 256, 0, 2, 3));
