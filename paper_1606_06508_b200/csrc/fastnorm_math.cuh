@@ -339,6 +339,9 @@ __device__ __forceinline__ int biased_exp32(float v) { return (int)((__float_as_
 #define FNB_F32_DIV_NATIVE 0
 #endif
 
+#ifndef FNB_F32_DIV_RECIP
+#define FNB_F32_DIV_RECIP 1
+#endif
 template <> struct Divider<float> {
     double b, y;
     float bf;
@@ -371,11 +374,30 @@ template <> struct Divider<float> {
         // The rest goes to special_quotient instead of the library division's slow path:
         // naive3 f32 63 -> 125 Gvec/s, quotient3_fast f32 165 -> 179, quotient3 f32
         // 113 -> 117 (config 4, profiles/r01ad_ab.txt; "old" is the library fallback).
+#if FNB_F32_DIV_RECIP
+        // One binary64 product with the shared reciprocal y = RN64(1/b), rounded once to
+        // binary32.  q = (a/b)(1 + e), |e| <= 2^-52 + 2^-106.  For 24-bit a and b, a
+        // quotient that is not itself a binary32 midpoint lies at least 2^-49 (relative)
+        // from every midpoint of the result grid: a/b - mu = (A 2^s - M B) 2^em / B with
+        // integers A, B < 2^24, M < 2^25 and s >= -1.  The same holds on the subnormal
+        // grid (absolute gap >= 2^-175, error <= M 2^-202).  So q and a/b round to the
+        // same binary32 value.  Exact midpoints need b a power of two, where y and q are
+        // exact.  A zero numerator gives the xor-signed zero by itself.  Checked bit for
+        // bit against __fdiv_rn by fn_selftest_div.
+#ifdef FNB_DIV_NEGATIVE_CONTROL
+        // test-only: a reciprocal truncated to 45 bits must be caught by the selftest's
+        // near-midpoint category (tools/selftest_big.py)
+        if (bok && isfinite(a))
+            return __double2float_rn(__dmul_rn((double)a, __longlong_as_double(__double_as_longlong(y) & ~0xFFll)));
+#endif
+        if (bok && isfinite(a)) return __double2float_rn(__dmul_rn((double)a, y));
+#else
         if (bok && isfinite(a)) {
             const float q = __double2float_rn(div_markstein((double)a, b, y));
             const float z = __uint_as_float((__float_as_uint(a) ^ __float_as_uint(bf)) & 0x80000000u);
             return a != 0.0f ? q : z;
         }
+#endif
         return special_quotient(a, bf);
     }
 };

@@ -120,7 +120,7 @@ __global__ void selftest_f32(uint64_t seed, int64_t n, unsigned long long* out) 
          i += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t w0 = mix(seed + 2 * (uint64_t)i), w1 = mix(seed + 2 * (uint64_t)i + 1);
         unsigned ua = (unsigned)w0, ub = (unsigned)(w0 >> 32);
-        const int cat = (int)(w1 % 8);
+        const int cat = (int)(w1 % 9);
         if (cat == 1) ub = (ub & 0xff800000u) | 0x007fffffu;      // all-ones mantissa
         if (cat == 2) ub &= 0xff800000u;                          // power of two
         if (cat == 3) ua &= 0x807fffffu;                          // subnormal numerator
@@ -133,6 +133,23 @@ __global__ void selftest_f32(uint64_t seed, int64_t n, unsigned long long* out) 
                                     0x7fc00000u, 0x3f800000u};
             if ((w1 >> 8) & 1) ua = sp[(w1 >> 9) % 6];
             if ((w1 >> 12) & 1) ub = sp[(w1 >> 13) % 6];
+        }
+        if (cat == 8) {
+            const uint64_t w2 = mix(w0 ^ (w1 << 1));
+            // Hardest cases for one-product division: a/b at the minimum possible distance
+            // from a binary32 midpoint mu = M 2^em (M odd, 25 bits).  With B odd and
+            // M B = k 2^25 +- 1, a = k 2^ea and b = B 2^eb give |a/b - mu| = 2^em / B.
+            const unsigned B = (unsigned)((w0 >> 40) | 0x800001u) & 0xFFFFFFu;  // odd, 24 bits
+            unsigned inv = B;                                                      // B^-1 mod 2^32
+            for (int it = 0; it < 4; ++it) inv *= 2u - B * inv;
+            unsigned M = inv & 0x1FFFFFFu;
+            if (M < (1u << 24)) M = (1u << 25) - M;                                // M B = -1 mod 2^25
+            const unsigned long long MB = (unsigned long long)M * B;
+            const unsigned k = (unsigned)((MB + (1ull << 24)) >> 25);               // MB = k 2^25 +- 1
+            const int ea = 40 + (int)((w2 >> 8) % 170), eb = 40 + (int)((w2 >> 16) % 170);
+            ua = __float_as_uint(ldexpf((float)k, ea - 150));
+            ub = __float_as_uint(ldexpf((float)B, eb - 150));
+            if ((w2 >> 24) & 1) ua ^= 0x80000000u;
         }
         float a = __uint_as_float(ua), b = __uint_as_float(ub);
         if (cat == 6) a = (w1 >> 8) & 1 ? 0.0f : -0.0f;
