@@ -272,7 +272,10 @@ __device__ __forceinline__ double tiny_quotient(double a, double b, int ea, unsi
 // the library slow path.  Exact (fn_selftest_div, golden, full-size parity), but the
 // division-bound kernels are issue-bound and the per-division range test costs more
 // than it saves: quotient2 cfg 2 55.2 -> 50.9, quotient3 cfg 5 36.6 -> 30.1 and cfg 1
-// 101 -> 79 Gvec/s (profiles/r01bq_ab.txt).  Off.
+// 101 -> 79 Gvec/s (profiles/r01bq_ab.txt).  Also measured: the same out of line
+// (__noinline__), and a form that keeps every lane on __ddiv_rn's fast path (tiny lanes
+// divide 1 by b) and patches afterwards -- both as slow on the unit-range configs
+// (quotient3 cfg 1: 80 / 76 Gvec/s; profiles/r01cg_ab.txt, r01ch_ab.txt).  Off.
 #ifndef FNB_F64_TINY_QUOTIENT
 #define FNB_F64_TINY_QUOTIENT 0
 #endif
