@@ -2,6 +2,8 @@
 against the reference's golden vectors and the pinned oracle (reference rule: NaN
 matches NaN, everything else bit-equal including the sign of zero)."""
 
+import math
+
 import numpy as np
 import pytest
 
@@ -477,3 +479,47 @@ def test_in_place_outputs(cuda_dev):
         ws = fn.scale3(p, torch.from_numpy(xh).to(cuda_dev))
         fn.scale3(p, s, out=(inv, s))
         assert torch.equal(s.view(torch.int64), ws.scaled.view(torch.int64))
+
+
+def _custom_sets():
+    """Valid non-preset parameter sets (validate_conditions passes), and raw constants
+    that fail validation but that the kernels -- like the reference's -- still take."""
+    L = math.ldexp
+    d, s = fn.preset("double"), fn.preset("single")
+    valid = [d.with_field("tau_min", 3 * L(1, -484)),                      # non-power-of-two tau
+             d.with_field("tau_max", L(1, 500)).with_field("sigma_max", L(1, -530)),
+             s.with_field("tau_max", L(1, 60)).with_field("sigma_max", L(1, -70))]
+    for p in valid:
+        assert fn.validate_conditions(p) == (), p
+    raw = [(np.array(fn.kernel_args(d)) * np.array([1, 1, 3, 1, 1 / 3, 1]), False),   # sigma_min = 3 2^592
+           (np.array(fn.kernel_args(s)) * np.array([1, 1, 1, 1.5, 1, 1 / 1.5]), True)]
+    return valid, raw
+
+
+def test_custom_parameter_sets(cuda_dev):
+    """Any parameter set runs on the GPU bit-identically to the oracle: valid non-preset
+    sets through the public API, and raw constants (non-power-of-two sigma, which
+    disables exponent insertion) through the registry's batched kernels."""
+    valid, raw = _custom_sets()
+    for p in valid:
+        single = p.precision == "single"
+        ka = np.array(fn.kernel_args(p))
+        x = _random_rows(1 << 18, 3, single, seed=5)
+        xd = torch.from_numpy(x).to(cuda_dev)
+        for op, f in ((_lib.OP_NORMALIZE, fn.normalize3), (_lib.OP_SCALE, fn.scale3), (_lib.OP_NORM, fn.norm3)):
+            res = f(p, xd)
+            torch.cuda.synchronize()
+            h, b, _ = oracle.run(op, x, ka, threads=8)
+            got = [res] if op == _lib.OP_NORM else list(res)
+            want = [h] if op == _lib.OP_NORM else [h, b]
+            for g, w in zip(got, want):
+                assert oracle.same(g.cpu().numpy(), w).all(), (p, op)
+    for ka, single in raw:
+        prec = "f32" if single else "f64"
+        x = _random_rows(1 << 18, 4, single, seed=6)
+        xd = torch.from_numpy(x).to(cuda_dev)
+        for base, op in (("normalize4", _lib.OP_NORMALIZE), ("scale4", _lib.OP_SCALE)):
+            res = _cuda_kernels.batch_kernel(base, prec)(xd, ka)
+            torch.cuda.synchronize()
+            h, b, _ = oracle.run(op, x, ka, threads=8)
+            assert oracle.same(res.head.cpu().numpy(), h).all() and oracle.same(res.body.cpu().numpy(), b).all()

@@ -26,9 +26,9 @@ KA = {
 }
 
 
-def _rows_vs_reference(x: np.ndarray, prec: str, dim: int):
-    ka = KA[prec]
-    for fam in FAMILIES[dim]:
+def _rows_vs_reference(x: np.ndarray, prec: str, dim: int, ka=None, families=None):
+    ka = KA[prec] if ka is None else tuple(float(v) for v in ka)
+    for fam in families or FAMILIES[dim]:
         fn = getattr(REF, kernel_name(fam, dim, prec))
         h, b, _ = oracle.run(oracle.BASE_OPS[fam], x, ka)
         for i, row in enumerate(x.astype(np.float64).tolist()):
@@ -79,3 +79,30 @@ def test_loop_checksum_vs_reference(cfg):
     want = fn(flat, 1 << 14, (1 << 14) - 1, *ka)
     got = oracle.loop(oracle.ALGO_SCALING, x, 1 << 14, (1 << 14) - 1, ka)
     assert got == want
+
+
+# Non-preset constants: valid sets (non-power-of-two tau_min, a lower tau_max / sigma_max
+# pair) and raw constants that fail validation but that the reference's kernels still
+# take (non-power-of-two sigma).  The GPU side of the same sets is
+# tests/test_gpu_parity.py::test_custom_parameter_sets.
+CUSTOM_KA = {
+    "f64": [(3 * L(1, -484), L(1, 510), L(1, 592), L(1, -514), L(1, -592), L(1, 514)),
+            (L(1, -482), L(1, 500), L(1, 592), L(1, -530), L(1, -592), L(1, 530)),
+            (L(1, -482), L(1, 510), 3 * L(1, 592), L(1, -514), L(1, -592) / 3, L(1, 514))],
+    "f32": [(L(1, -49), L(1, 60), L(1, 100), L(1, -70), L(1, -100), L(1, 70)),
+            (L(1, -49), L(1, 62), L(1, 100), 1.5 * L(1, -66), L(1, -100), L(1, 66) / 1.5)],
+}
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_custom_constants_vs_reference(prec):
+    rng = np.random.default_rng(99)
+    single = prec == "f32"
+    lo, hi = (-149, 127) if single else (-1074, 1023)
+    for ka in CUSTOM_KA[prec]:
+        for dim in (3, 4):
+            m = 1500
+            x = np.ldexp(1.0 + rng.random((m, dim)), rng.integers(lo, hi, (m, dim)))
+            x *= rng.integers(0, 2, (m, dim)) * 2 - 1
+            x = x.astype(np.float32) if single else x
+            _rows_vs_reference(x, prec, dim, ka=ka, families=["scale", "normalize", "norm"])
