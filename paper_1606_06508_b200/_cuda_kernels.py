@@ -64,6 +64,8 @@ def _np_dtype(suffix: str):
 
 
 def _ka_array(ka) -> np.ndarray:
+    if type(ka) is np.ndarray and ka.dtype == np.float64 and ka.shape == (6,) and ka.flags.c_contiguous:
+        return ka  # already the ABI's six doubles (kernel_args_array's cached arrays)
     arr = np.ascontiguousarray(np.asarray(ka, dtype=np.float64))
     if arr.shape != (6,):
         raise ValueError("kernel_args must be six numbers")
@@ -76,11 +78,11 @@ def batch_kernel(base: str, suffix: str):
     op, dim = parse_base(base)
     takes_ka = op in (_lib.OP_SCALE, _lib.OP_NORMALIZE, _lib.OP_NORMALIZE_SQ, _lib.OP_NORM)
     want = "float64" if suffix == "f64" else "float32"
+    prec = "double" if suffix == "f64" else "single"
 
     def run(x, ka=None, out=None):
-        got = str(x.dtype).replace("torch.", "")
-        if got != want:
-            raise TypeError(f"{base}_{suffix} computes in {want}; rows are {got}")
+        if batch.precision_of(x) != prec:
+            raise TypeError(f"{base}_{suffix} computes in {want}; rows are {str(x.dtype).replace('torch.', '')}")
         return batch.run(op, dim, x, _ka_array(ka) if takes_ka else None, out)
 
     run.__name__ = f"{base}_{suffix}_batch"

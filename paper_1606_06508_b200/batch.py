@@ -112,14 +112,24 @@ def _dtype_code(dtype_name: str) -> int:
     raise TypeError(f"rows must be float32 or float64, got {dtype_name}")
 
 
+_prec_of: dict = {}
+
+
 def precision_of(x) -> str:
-    name = str(x.dtype).replace("torch.", "")
-    return "double" if _dtype_code(name) == _lib.F64 else "single"
+    dt = x.dtype
+    prec = _prec_of.get(dt)
+    if prec is None:
+        name = str(dt).replace("torch.", "")
+        prec = _prec_of[dt] = "double" if _dtype_code(name) == _lib.F64 else "single"
+    return prec
 
 
 def _check_out(o, shape, like, what):
     if o is None:
         return None
+    if (is_torch(like) and is_torch(o) and o.dtype == like.dtype and o.shape == shape
+            and o.device == like.device and o.is_contiguous()):
+        return o  # the common case, without building messages or dtype strings
     if tuple(o.shape) != tuple(shape):
         raise ValueError(f"out {what} has shape {tuple(o.shape)}, expected {tuple(shape)}")
     if str(o.dtype) != str(like.dtype):
@@ -132,6 +142,52 @@ def _check_out(o, shape, like, what):
     return o
 
 
+_fast: list = []
+
+
+def _fast_run():
+    """fn_run through the CPython extension (csrc/scalar_ext.c), or None if not built."""
+    if not _fast:
+        import ctypes
+
+        try:
+            from paper_1606_06508_b200 import _scalar
+        except ImportError:
+            _fast.append(None)
+        else:
+            _scalar.bind_run(ctypes.cast(_lib.lib().fn_run, ctypes.c_void_p).value)
+            _fast.append(_scalar.run)
+    return _fast[0]
+
+
+_ka_addrs: dict = {}
+
+
+def _ka_address(ka_arr: np.ndarray) -> int:
+    """Address of a kernel-argument array; read-only arrays (kernel_args_array's cached
+    ones) are remembered together with a reference, so the address stays valid."""
+    if ka_arr.flags.writeable:
+        return ka_arr.ctypes.data
+    hit = _ka_addrs.get(id(ka_arr))
+    if hit is None or hit[0] is not ka_arr:
+        hit = _ka_addrs[id(ka_arr)] = (ka_arr, ka_arr.ctypes.data)
+    return hit[1]
+
+
+_stream_of = None
+_dcode_of: dict = {}
+
+
+def _cuda_stream(torch, dev: int) -> int:
+    """torch's current stream on device ``dev`` as a raw handle (the cheap private
+    accessor when present)."""
+    global _stream_of
+    if _stream_of is None:
+        raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+        _stream_of = raw if raw is not None else (lambda d: torch.cuda.current_stream(d).cuda_stream)
+    return _stream_of(dev)
+
+
 def run(op: int, dim: int, x, ka_arr: np.ndarray | None, out=None, invalid=None) -> BatchOut:
     """Run kernel family ``op`` over rows ``x[N, dim]``; return (head, body, extra).
 
@@ -142,7 +198,7 @@ def run(op: int, dim: int, x, ka_arr: np.ndarray | None, out=None, invalid=None)
     w0, w1, w2 = widths(op, dim)
     n = int(x.shape[0])
     L = _lib.lib()
-    kptr = None if ka_arr is None else ka_arr.ctypes.data
+    kptr = None if ka_arr is None else _ka_address(ka_arr)
     outs = tuple(out) if out is not None else ()
     want = 1 + int(w1 > 0) + int(w2 > 0)
     if out is not None and len(outs) != want:
@@ -153,7 +209,9 @@ def run(op: int, dim: int, x, ka_arr: np.ndarray | None, out=None, invalid=None)
 
     if is_torch(x):
         torch = _torch()
-        dcode = _dtype_code(str(x.dtype).replace("torch.", ""))
+        dcode = _dcode_of.get(x.dtype)
+        if dcode is None:
+            dcode = _dcode_of[x.dtype] = _dtype_code(str(x.dtype).replace("torch.", ""))
         if x.is_cuda:
             x = x.contiguous()
 
@@ -161,19 +219,31 @@ def run(op: int, dim: int, x, ka_arr: np.ndarray | None, out=None, invalid=None)
                 if not w:
                     return None
                 o = _check_out(o, _shape(n, w), x, what)
-                return o if o is not None else torch.empty(_shape(n, w), dtype=x.dtype, device=x.device)
+                return o if o is not None else x.new_empty(_shape(n, w))
 
             head, body, extra = alloc(o_head, w0, "head"), alloc(o_body, w1, "body"), alloc(o_extra, w2, "extra")
             ptr = (lambda t: None if t is None else t.data_ptr())
-            with torch.cuda.device(x.device):
-                stream = torch.cuda.current_stream(x.device).cuda_stream
+            dev = x.device.index
+            # The library launches on the thread's current CUDA device (shared with torch
+            # through the driver's current context): switch only when x lives elsewhere.
+            switch = torch.cuda.current_device() != dev
+            if switch:
+                ctx = torch.cuda.device(dev)
+                ctx.__enter__()
+            try:
+                stream = _cuda_stream(torch, dev)
                 if op in (_lib.OP_ROT_UNIT, _lib.OP_ROT_GENERAL, _lib.OP_NORMALIZE_ROT):
                     rc = L.fn_run_rot(op, x.data_ptr(), n, ptr(head), ptr(body), ptr(extra), kptr,
                                       ptr(invalid), stream)
                 else:
-                    rc = L.fn_run(op, dim, dcode, x.data_ptr(), n, ptr(head), ptr(body), ptr(extra),
-                                  kptr, stream)
-            _lib.check(rc, "fn_run")
+                    fast = _fast_run()
+                    call = fast if fast is not None else L.fn_run
+                    rc = call(op, dim, dcode, x.data_ptr(), n, ptr(head), ptr(body), ptr(extra), kptr, stream)
+            finally:
+                if switch:
+                    ctx.__exit__(None, None, None)
+            if rc:
+                _lib.check(rc, "fn_run")
             return BatchOut(head, body, extra)
         # CPU tensor: host path, results as CPU tensors sharing the numpy buffers
         res = run(op, dim, x.contiguous().numpy(), ka_arr,
