@@ -377,6 +377,20 @@ def _batch_stream_rate(fn, p, x, bytes_per_row, peak, reps, sets=8, per_set=4):
                     fn.normalize3(p, xi, out=(ri, ui))
     torch.cuda.synchronize(x.device)
     launches = sets * per_set
+    # the same launches issued eagerly through the public API (no graph): host cost per
+    # call (~10 us) against ~10 us of kernel
+    eager = []
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        cur = torch.cuda.current_stream(x.device)
+        e0.record(cur)
+        for _ in range(per_set):
+            for xi, ri, ui in bufs:
+                fn.normalize3(p, xi, out=(ri, ui))
+        e1.record(cur)
+        torch.cuda.synchronize(x.device)
+        eager.append(e0.elapsed_time(e1) / 1e3 / launches)
+    t_eager = statistics.median(eager)
     times = []
     for _ in range(max(reps, 3) + 1):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -391,7 +405,9 @@ def _batch_stream_rate(fn, p, x, bytes_per_row, peak, reps, sets=8, per_set=4):
     return {"launches_per_graph": launches, "buffer_sets": sets,
             "bytes_cycled": sets * n * bytes_per_row, "ms_per_launch": t * 1e3,
             "vectors_per_s": n / t, "GB_per_s": n * bytes_per_row / t / 1e9,
-            "frac": n * bytes_per_row / t / 1e9 / peak}
+            "frac": n * bytes_per_row / t / 1e9 / peak,
+            "eager_public_api": {"ms_per_launch": t_eager * 1e3, "vectors_per_s": n / t_eager,
+                                 "frac": n * bytes_per_row / t_eager / 1e9 / peak}}
 
 
 def measure_other_configs(dev, reps: int = 5):

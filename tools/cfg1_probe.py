@@ -42,7 +42,9 @@ def main():
     sob = bench._batch_stream_rate(fn, p, x, 56, peak, 10)
     print(json.dumps({"env": {k: v for k, v in os.environ.items() if k.startswith("FASTNORM_B200")},
                       "lone_ms": t * 1e3, "lone_frac": c.rows * 56 / t / 1e9 / peak,
-                      "stream_ms": sob["ms_per_launch"], "stream_frac": sob["frac"]}), flush=True)
+                      "stream_ms": sob["ms_per_launch"], "stream_frac": sob["frac"],
+                      "eager_ms": sob["eager_public_api"]["ms_per_launch"],
+                      "eager_frac": sob["eager_public_api"]["frac"]}), flush=True)
 
 
 if __name__ == "__main__":
