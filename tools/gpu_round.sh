@@ -3,7 +3,9 @@
 # bench + one full capture of the top kernel).  Usage: bash tools/gpu_round.sh TAG [parts]
 set -u
 OUT=gpurun_out; mkdir -p $OUT
-TAG=${1:-rX}; PARTS=${2:-tests,bench,tune,ncu}
+TAG=${1:-rX}; PARTS=${2:-tests,bench,tune}
+# ncu parts (one ncu run per gpurun call): ncu_launch (launch list of the bench command)
+# and ncu_full (one --set full capture of the headline kernel), e.g. PARTS=ncu_launch
 has() { [[ ",$PARTS," == *",$1,"* ]]; }
 if has tests; then
   timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > $OUT/${TAG}_pytest_gpu.log 2>&1
@@ -18,11 +20,13 @@ if has tune; then
   make -s -C tools tune >/dev/null 2>&1
   timeout 900 tools/tune_stream 28 10 all > $OUT/${TAG}_tune.csv 2>&1; echo "tune rc=$?"
 fi
-if has ncu; then
+if has ncu_launch; then
   BENCH="python bench.py --steps 5 --warmup 3 --e2e-steps 1 --no-cpu-baseline"
   timeout 600 $BENCH > $OUT/${TAG}_bench_plain.log 2>&1 && \
     timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 20 --csv \
       --log-file $OUT/${TAG}_launches.csv $BENCH > $OUT/${TAG}_ncu_launch.log 2>&1; echo "launch list rc=$?"
+fi
+if has ncu_full; then
   PROF="python tools/prof_target.py --cfg 5 --log2-rows 26 --iters 2"
   timeout 300 $PROF > $OUT/${TAG}_prof_plain.log 2>&1 && \
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:tma_stream_kernel -c 1 \
