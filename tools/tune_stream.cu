@@ -28,6 +28,32 @@ extern "C" int fn_generate(int cfg, uint64_t seed, int64_t row0, int64_t n, void
         }                                                                              \
     } while (0)
 
+// Speed-of-light stand-ins with the record shapes of real ops but almost no arithmetic
+// (op codes 90+ are tool-only): they bound what the pipeline and DRAM can do for that
+// traffic mix.
+namespace fnb {
+template <typename T, int N> struct RowOp<T, N, 90> {  // normalize4_rotation shape: 32 B in, 112 B out
+    static constexpr int W0 = 1, W1 = 4, W2 = 9;
+    __device__ __forceinline__ static bool apply(const T (&x)[N], const KArgs<T>&, T* o0, T* o1, T* o2) {
+        o0[0] = x[0];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) o1[c] = x[c];
+#pragma unroll
+        for (int c = 0; c < 9; ++c) o2[c] = x[c & 3];
+        return true;
+    }
+};
+template <typename T, int N> struct RowOp<T, N, 91> {  // normalize3 shape: 24 B in, 32 B out
+    static constexpr int W0 = 1, W1 = 3, W2 = 0;
+    __device__ __forceinline__ static bool apply(const T (&x)[N], const KArgs<T>&, T* o0, T* o1, T*) {
+        o0[0] = x[0];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) o1[c] = x[c];
+        return true;
+    }
+};
+}  // namespace fnb
+
 using namespace fnb;
 
 __global__ void sol_kernel(const double2* __restrict__ x, int64_t npairs, double2* __restrict__ r,
@@ -216,6 +242,13 @@ int main(int argc, char** argv) {
         vs.push_back(V("normalize2_f32", 4, float, 2, FN_OP_NORMALIZE, 1024, 4, 256, 0, 2));
         vs.push_back(V("normalize4_f32", 4, float, 4, FN_OP_NORMALIZE, 512, 3, 256, 0, 2));
         vs.push_back(V("normalize4_f32", 4, float, 4, FN_OP_NORMALIZE, 256, 4, 256, 0, 2));
+    }
+    if (which == "all" || which == "copy") {
+        vs.push_back(V("copy_nrot_shape", 3, double, 4, 90, 128, 3, 256, 0, 2));
+        vs.push_back(V("copy_nrot_shape", 3, double, 4, 90, 256, 2, 256, 0, 2));
+        vs.push_back(V("normalize4_rot_f64", 3, double, 4, FN_OP_NORMALIZE_ROT, 128, 3, 256, 0, 2));
+        vs.push_back(V("copy_n3_shape", 5, double, 3, 91, 256, 4, 256, 0, 2));
+        vs.push_back(V("normalize3_f64", 5, double, 3, FN_OP_NORMALIZE, 256, 4, 256, 0, 2));
     }
     if (which == "all" || which == "rot") {
         vs.push_back(V("rotation_unit_f64", 3, double, 4, FN_OP_ROT_UNIT, 256, 3, 256, 0, 2));
