@@ -127,7 +127,10 @@ def precision_of(x) -> str:
 def _check_out(o, shape, like, what):
     if o is None:
         return None
-    if (is_torch(like) and is_torch(o) and o.dtype == like.dtype and o.shape == shape
+    if type(o) is np.ndarray and type(like) is np.ndarray:
+        if o.dtype == like.dtype and o.shape == shape and o.flags.c_contiguous:
+            return o  # the common host case
+    elif (is_torch(like) and is_torch(o) and o.dtype == like.dtype and o.shape == shape
             and o.device == like.device and o.is_contiguous()):
         return o  # the common case, without building messages or dtype strings
     if tuple(o.shape) != tuple(shape):
@@ -155,8 +158,10 @@ def _fast_run():
         except ImportError:
             _fast.append(None)
         else:
-            _scalar.bind_run(ctypes.cast(_lib.lib().fn_run, ctypes.c_void_p).value)
-            _fast.append(_scalar.run)
+            L = _lib.lib()
+            _scalar.bind_run(ctypes.cast(L.fn_run, ctypes.c_void_p).value)
+            _scalar.bind_host(ctypes.cast(L.fn_host_run, ctypes.c_void_p).value)
+            _fast.append(_scalar)
     return _fast[0]
 
 
@@ -237,7 +242,7 @@ def run(op: int, dim: int, x, ka_arr: np.ndarray | None, out=None, invalid=None)
                                       ptr(invalid), stream)
                 else:
                     fast = _fast_run()
-                    call = fast if fast is not None else L.fn_run
+                    call = fast.run if fast is not None else L.fn_run
                     rc = call(op, dim, dcode, x.data_ptr(), n, ptr(head), ptr(body), ptr(extra), kptr, stream)
             finally:
                 if switch:
@@ -253,8 +258,11 @@ def run(op: int, dim: int, x, ka_arr: np.ndarray | None, out=None, invalid=None)
 
     if not isinstance(x, np.ndarray):
         raise TypeError(f"rows must be a numpy array or torch tensor, got {type(x).__name__}")
-    dcode = _dtype_code(str(x.dtype))
-    x = np.ascontiguousarray(x)
+    dcode = _dcode_of.get(x.dtype)
+    if dcode is None:
+        dcode = _dcode_of[x.dtype] = _dtype_code(str(x.dtype))
+    if not x.flags.c_contiguous:
+        x = np.ascontiguousarray(x)
 
     def alloc_np(o, w, what):
         if not w:
@@ -271,8 +279,13 @@ def run(op: int, dim: int, x, ka_arr: np.ndarray | None, out=None, invalid=None)
                                  kptr, darr.ctypes.data, len(devs))
         _lib.check(rc, "fn_host_run_multi")
     else:
-        rc = L.fn_host_run(op, dim, dcode, x.ctypes.data, n, ptr(head), ptr(body), ptr(extra), kptr)
-        _lib.check(rc, "fn_host_run")
+        fast = _fast_run()
+        if fast is not None:
+            rc = fast.host_run(op, dim, dcode, x, n, head, body, extra, kptr)
+        else:
+            rc = L.fn_host_run(op, dim, dcode, x.ctypes.data, n, ptr(head), ptr(body), ptr(extra), kptr)
+        if rc:
+            _lib.check(rc, "fn_host_run")
     return BatchOut(head, body, extra)
 
 

@@ -114,12 +114,16 @@ static inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; 
 // thread-safe initialisation):
 //   FASTNORM_B200_PATH=direct       force the per-row kernel (diagnostics)
 //   FASTNORM_B200_CTAS_PER_SM=<k>   CTAs per SM for the streaming kernel (experiments)
+// The zero-copy small-batch host path (rows in mapped page-locked memory) asks for the
+// per-row kernel on its own thread.
+static thread_local bool tl_direct = false;
+
 static bool force_direct() {
     static const bool v = [] {
         const char* e = getenv("FASTNORM_B200_PATH");
         return e && strcmp(e, "direct") == 0;
     }();
-    return v;
+    return v || tl_direct;
 }
 
 static int cps_override() {
@@ -551,6 +555,60 @@ static int host_staging_get(Staging* st, size_t bytes_per_pipe) {
     return FN_OK;
 }
 
+// ---------------------------------------------------------------------------------
+// Small host batches (up to kSmallHostBytes of rows in and results out): copy the rows
+// into a per-thread page-locked buffer mapped into the device, run the per-row kernel
+// on it in place (the kernel reads and writes host memory over PCIe), synchronise, copy
+// the results out.  One launch and one synchronisation instead of the staged pipeline's
+// transfers and events: ~48 -> ~15 us for a few hundred rows (profiles/r01cr_*).
+// ---------------------------------------------------------------------------------
+constexpr size_t kSmallHostBytes = 256 << 10;
+
+struct SmallCtx {
+    int dev = -1;
+    cudaStream_t stream = nullptr;
+    char* host = nullptr;
+    char* dptr = nullptr;
+};
+
+static int host_run_small(int op, int dim, int dtype, const void* x, const void* x2, int dim2, int64_t n,
+                          void* head, void* body, void* sq, const double* ka, int dev) {
+    static thread_local std::vector<SmallCtx> ctxs;
+    if ((int)ctxs.size() <= dev) ctxs.resize(dev + 1);
+    SmallCtx& c = ctxs[dev];
+    cudaError_t e;
+    if (c.dev < 0) {
+        e = cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
+        e = cudaHostAlloc(reinterpret_cast<void**>(&c.host), kSmallHostBytes + 8 * 256, cudaHostAllocMapped);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaHostAlloc");
+        e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c.dptr), c.host, 0);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaHostGetDevicePointer");
+        c.dev = dev;
+    }
+    const size_t w = dtype == FN_F64 ? 8 : 4;
+    const Widths wd = op_widths(op, dim);
+    const size_t bx = align256(n * dim * w), bx2 = align256(n * dim2 * w), b0 = align256(n * wd.w0 * w),
+                 b1 = align256(n * wd.w1 * w);
+    const size_t off[5] = {0, bx, bx + bx2, bx + bx2 + b0, bx + bx2 + b0 + b1};
+    memcpy(c.host + off[0], x, n * dim * w);
+    if (x2) memcpy(c.host + off[1], x2, n * dim2 * w);
+    void* d0 = c.dptr + off[2];
+    void* d1 = wd.w1 ? c.dptr + off[3] : nullptr;
+    void* d2 = wd.w2 ? c.dptr + off[4] : nullptr;
+    tl_direct = true;
+    const int rc = x2 ? run_rows2(op, c.dptr + off[0], c.dptr + off[1], n, d0, ka, nullptr, c.stream)
+                      : run(op, dim, dtype, c.dptr + off[0], n, d0, d1, d2, ka, c.stream);
+    tl_direct = false;
+    if (rc != FN_OK) return rc;
+    e = cudaStreamSynchronize(c.stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+    memcpy(head, c.host + off[2], n * wd.w0 * w);
+    if (wd.w1) memcpy(body, c.host + off[3], n * wd.w1 * w);
+    if (wd.w2) memcpy(sq, c.host + off[4], n * wd.w2 * w);
+    return FN_OK;
+}
+
 // x2 / dim2: the second input of the two-input ops (NULL / 0 otherwise).
 static int host_run_impl(int op, int dim, int dtype, const void* x, const void* x2, int dim2, int64_t n,
                          void* head, void* body, void* sq, const double* ka) {
@@ -561,9 +619,32 @@ static int host_run_impl(int op, int dim, int dtype, const void* x, const void* 
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
     const size_t w = dtype == FN_F64 ? 8 : 4;
     const Widths wd = op_widths(op, dim);
-    // ~48 MiB of input per chunk: three chunks in flight, per-copy latency amortised.
-    const int64_t chunk_mb = env_int("FASTNORM_B200_HOST_CHUNK_MB", 48, 1, 1024);
-    const int64_t chunk_rows = std::max<int64_t>(4096, (chunk_mb << 20) / (int64_t)((dim + dim2) * w));
+    if ((size_t)n * (dim + dim2 + wd.w0 + wd.w1 + wd.w2) * w + 8 * 256 <= kSmallHostBytes &&
+        env_int("FASTNORM_B200_HOST_SMALL", 1, 0, 1))  // FASTNORM_B200_HOST_SMALL=0: always stage
+        return host_run_small(op, dim, dtype, x, x2, dim2, n, head, body, sq, ka, dev);
+    // Pageable caller memory cannot be DMA'd asynchronously: such sides go through
+    // page-locked staging filled / drained by the parallel host copier, overlapped with
+    // the transfers and kernels of the other pipes.
+    const bool stage_in = !is_page_locked(x);
+    const bool stage_in2 = x2 && !is_page_locked(x2);
+    const bool stage_out = !is_page_locked(head) || (wd.w1 && !is_page_locked(body)) ||
+                           (wd.w2 && !is_page_locked(sq));
+    const bool staged = stage_in || stage_in2 || stage_out;
+    // Input bytes per chunk (profiles/r01cs_chunks.txt, 3-D f64 rows):
+    //  * page-locked callers: 48 MiB for large arrays, and at least 8 chunks of >= 4 MiB
+    //    for mid-size ones so transfers and kernels of different chunks overlap;
+    //  * pageable callers: 8-16 MiB (each staging copy still gets the parallel copier).
+    // FASTNORM_B200_HOST_CHUNK_MB fixes the chunk size instead.
+    const int64_t row_in = (int64_t)((dim + dim2) * w), in_total = n * row_in;
+    int64_t chunk_bytes;
+    if (getenv("FASTNORM_B200_HOST_CHUNK_MB")) {
+        chunk_bytes = (int64_t)env_int("FASTNORM_B200_HOST_CHUNK_MB", 48, 1, 1024) << 20;
+    } else if (staged) {
+        chunk_bytes = std::max<int64_t>((int64_t)8 << 20, std::min<int64_t>((int64_t)16 << 20, in_total / 3));
+    } else {
+        chunk_bytes = std::max<int64_t>((int64_t)4 << 20, std::min<int64_t>((int64_t)48 << 20, in_total / 8));
+    }
+    const int64_t chunk_rows = std::max<int64_t>(4096, chunk_bytes / row_in);
     const int64_t rows = std::min<int64_t>(n, chunk_rows);
     const size_t bx = align256(rows * dim * w), bx2 = align256(rows * dim2 * w),
                  b0 = align256(rows * wd.w0 * w), b1 = align256(rows * wd.w1 * w),
@@ -573,14 +654,7 @@ static int host_run_impl(int op, int dim, int dtype, const void* x, const void* 
     Staging* st = nullptr;
     rc = staging_get(dev, per_pipe, &st);
     if (rc != FN_OK) return rc;
-    // Pageable caller memory cannot be DMA'd asynchronously: such sides go through
-    // page-locked staging filled / drained by the parallel host copier, overlapped with
-    // the transfers and kernels of the other pipes.
-    const bool stage_in = !is_page_locked(x);
-    const bool stage_in2 = x2 && !is_page_locked(x2);
-    const bool stage_out = !is_page_locked(head) || (wd.w1 && !is_page_locked(body)) ||
-                           (wd.w2 && !is_page_locked(sq));
-    if (stage_in || stage_in2 || stage_out) {
+    if (staged) {
         rc = host_staging_get(st, per_pipe);
         if (rc != FN_OK) return rc;
     }

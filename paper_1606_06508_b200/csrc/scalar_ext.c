@@ -15,8 +15,10 @@
 
 typedef int (*scalar_fn)(int, int, int, const double*, double*, const double*);
 typedef int (*run_fn)(int, int, int, const void*, int64_t, void*, void*, void*, const double*, void*);
+typedef int (*host_fn)(int, int, int, const void*, int64_t, void*, void*, void*, const double*);
 static scalar_fn g_fn = NULL;
 static run_fn g_run = NULL;
+static host_fn g_host = NULL;
 
 static PyObject* bind(PyObject* self, PyObject* arg) {
     (void)self;
@@ -111,7 +113,60 @@ static PyObject* run(PyObject* self, PyObject* const* a, Py_ssize_t na) {
     return PyLong_FromLong(rc);
 }
 
+static PyObject* bind_host(PyObject* self, PyObject* arg) {
+    (void)self;
+    void* p = PyLong_AsVoidPtr(arg);
+    if (!p && PyErr_Occurred()) return NULL;
+    g_host = (host_fn)p;
+    Py_RETURN_NONE;
+}
+
+/* host_run(op, dim, dtype, x, n, head, body, sq, ka) -> fn_status: fn_host_run with the
+ * arrays passed as C-contiguous buffer objects (numpy arrays; None = NULL) and ka as an
+ * address.  Taking the buffers here avoids numpy's .ctypes objects on small calls. */
+static PyObject* host_run(PyObject* self, PyObject* const* a, Py_ssize_t na) {
+    (void)self;
+    if (na != 9) {
+        PyErr_SetString(PyExc_TypeError, "host_run(op, dim, dtype, x, n, head, body, sq, ka)");
+        return NULL;
+    }
+    if (!g_host) {
+        PyErr_SetString(PyExc_RuntimeError, "fn_host_run is not bound");
+        return NULL;
+    }
+    const int op = (int)PyLong_AsLong(a[0]), dim = (int)PyLong_AsLong(a[1]), dtype = (int)PyLong_AsLong(a[2]);
+    const long long n = PyLong_AsLongLong(a[4]);
+    void* ka = as_ptr(a[8]);
+    if (PyErr_Occurred()) return NULL;
+    Py_buffer views[4];
+    int held[4] = {0, 0, 0, 0};
+    void* ptrs[4] = {NULL, NULL, NULL, NULL};
+    const int slots[4] = {3, 5, 6, 7};
+    PyObject* result = NULL;
+    for (int k = 0; k < 4; ++k) {
+        PyObject* o = a[slots[k]];
+        if (o == Py_None) continue;
+        const int flags = PyBUF_C_CONTIGUOUS | (k ? PyBUF_WRITABLE : 0);
+        if (PyObject_GetBuffer(o, &views[k], flags) != 0) goto done;
+        held[k] = 1;
+        ptrs[k] = views[k].buf;
+    }
+    {
+        int rc;
+        Py_BEGIN_ALLOW_THREADS
+        rc = g_host(op, dim, dtype, ptrs[0], (int64_t)n, ptrs[1], ptrs[2], ptrs[3], (const double*)ka);
+        Py_END_ALLOW_THREADS
+        result = PyLong_FromLong(rc);
+    }
+done:
+    for (int k = 0; k < 4; ++k)
+        if (held[k]) PyBuffer_Release(&views[k]);
+    return result;
+}
+
 static PyMethodDef methods[] = {
+    {"bind_host", bind_host, METH_O, "bind_host(address of fn_host_run)"},
+    {"host_run", (PyCFunction)(void (*)(void))host_run, METH_FASTCALL, "fn_host_run on buffer objects"},
     {"bind", bind, METH_O, "bind(address of fn_scalar)"},
     {"bind_run", bind_run, METH_O, "bind_run(address of fn_run)"},
     {"run", (PyCFunction)(void (*)(void))run, METH_FASTCALL, "fn_run with integer pointers"},

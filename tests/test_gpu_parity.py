@@ -523,3 +523,30 @@ def test_custom_parameter_sets(cuda_dev):
             torch.cuda.synchronize()
             h, b, _ = oracle.run(op, x, ka, threads=8)
             assert oracle.same(res.head.cpu().numpy(), h).all() and oracle.same(res.body.cpu().numpy(), b).all()
+
+
+@pytest.mark.parametrize("small", ["1", "0"])
+def test_host_path_small_batches(cuda_dev, small, monkeypatch):
+    """Host arrays up to 256 KiB of traffic take the zero-copy path (rows in mapped
+    page-locked memory, per-row kernel in place); FASTNORM_B200_HOST_SMALL=0 forces the
+    staged pipeline.  Both equal the device path for every family, precision and the
+    two-input rotation, at sizes around the path boundary and a tile."""
+    monkeypatch.setenv("FASTNORM_B200_HOST_SMALL", small)
+    for prec, single in (("f64", False), ("f32", True)):
+        ka = np.array(fn.kernel_args(fn.preset("single" if single else "double")))
+        for dim in (2, 3, 4):
+            for n in (1, 7, 255, 256, 1000, 4681):
+                x = _random_rows(n, dim, single, seed=n + dim)
+                xd = torch.from_numpy(x).to(cuda_dev)
+                for base in [_base(f, dim) for f in FAMILIES[dim]] + [f"normalize{dim}_sq"]:
+                    scaling = base.startswith(("scale", "normalize", "norm"))
+                    k = _cuda_kernels.batch_kernel(base, prec)
+                    got, want = k(x, ka if scaling else None), k(xd, ka if scaling else None)
+                    for g, w in zip(got, want):
+                        if g is not None:
+                            assert oracle.same(np.asarray(g), w.cpu().numpy()).all(), (base, prec, n)
+    q, v = _random_rows(300, 4, False, seed=3), _random_rows(300, 3, False, seed=4)
+    got = fn.normalize4_rotate(fn.preset("double"), q, v, strict=False)
+    want = fn.normalize4_rotate(fn.preset("double"), torch.from_numpy(q).to(cuda_dev),
+                                torch.from_numpy(v).to(cuda_dev), strict=False)
+    assert oracle.same(got, want.cpu().numpy()).all()
