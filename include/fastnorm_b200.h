@@ -102,6 +102,13 @@ int fn_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, voi
            void* sq, const double* ka, void* stream);
 int fn_host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head,
                 void* body, void* sq, const double* ka);
+/* Structure-of-arrays rows on the device: the reference's scalar signatures vectorised
+ * over arrays (normalize.py:51-89 / scale.py:33-51 / baselines.py:30-76 with x1..xn
+ * arrays).  xs[k] = component k of every row, head[N], body[k] = output component k
+ * (unit or scaled; NULL for FN_OP_NORM), sq[N] for FN_OP_NORMALIZE_SQ.  Same arithmetic
+ * as the AoS kernels, bit for bit.  Ops SCALE..NORMALIZE_SQ, both dtypes. */
+int fn_run_soa(int op, int dim, int dtype, const void* const* xs, int64_t n, void* head,
+               void* const* body, void* sq, const double* ka, void* stream);
 /* Page-locked (portable) host memory for fn_host_run / fn_host_run_multi callers: buffers
  * from here are DMA'd directly instead of through the library's staging copies
  * (1.56 vs 0.64 Gvec/s for 3-D f64 rows).  No reference analogue (the reference is CPU

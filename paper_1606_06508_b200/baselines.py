@@ -8,7 +8,7 @@ precision is the array's dtype (a conflicting ``precision=`` raises).
 
 from __future__ import annotations
 
-from paper_1606_06508_b200 import _backend, batch
+from paper_1606_06508_b200 import _backend, _lib, batch
 from paper_1606_06508_b200.normalize import NormalizeOutcome
 
 __all__ = [
@@ -25,6 +25,13 @@ __all__ = [
 def _call(base: str, dim: int, xs, precision, out) -> NormalizeOutcome:
     if len(xs) == dim + 1 and isinstance(xs[-1], str) and precision is None:
         xs, precision = xs[:-1], xs[-1]  # reference order: (x1, ..., xn, precision)
+    if batch.is_soa(xs, dim):  # one array per component (structure of arrays)
+        prec = batch.precision_of(xs[0])
+        if precision is not None and precision != prec:
+            raise TypeError(f"rows are {xs[0].dtype} but precision={precision!r}")
+        op = {"naive": _lib.OP_NAIVE, "quotient": _lib.OP_QUOTIENT}.get(base.rstrip("234"), _lib.OP_QUOTIENT3_FAST)
+        h, b, _ = batch.run_soa(op, dim, xs, None)
+        return NormalizeOutcome(h, b)
     if len(xs) == 1 and batch.is_array(xs[0]):
         x = xs[0]
         prec = batch.precision_of(x)

@@ -327,3 +327,54 @@ def run_rows2(op: int, a, v, ka_arr: np.ndarray | None, out=None, invalid=None):
     rc = L.fn_host_rotate_rows_f64(op, a.ctypes.data, v.ctypes.data, n, o.ctypes.data, kptr)
     _lib.check(rc, "fn_host_rotate_rows_f64")
     return o
+
+
+def is_soa(xs, dim: int) -> bool:
+    """The reference's scalar signature called with one 1-D array per component."""
+    return len(xs) == dim and all(is_array(v) and v.ndim == 1 for v in xs)
+
+
+def run_soa(op: int, dim: int, xs, ka_arr: np.ndarray | None):
+    """Structure-of-arrays rows: component arrays xs[k][N] -> (head[N], body tuple of
+    dim arrays or None, extra[N] or None), through fn_run_soa on the device.
+
+    CUDA tensors are used in place.  Host arrays (numpy, CPU tensors) are moved to the
+    current CUDA device and the results copied back by torch -- plumbing only, the
+    arithmetic runs in the kernel."""
+    import ctypes
+
+    torch = _torch()
+    n = int(xs[0].shape[0])
+    if any(int(v.shape[0]) != n for v in xs):
+        raise ValueError("component arrays must have the same length")
+    host = not (is_torch(xs[0]) and xs[0].is_cuda)
+    if host:
+        dev = torch.device("cuda", torch.cuda.current_device())
+        ts = [torch.as_tensor(v).to(dev) for v in xs]
+    else:
+        ts = [v.contiguous() for v in xs]
+        dev = ts[0].device
+    dt = ts[0].dtype
+    if any(t.dtype != dt or t.device != dev for t in ts):
+        raise TypeError("component arrays must share dtype and device")
+    dcode = _dtype_code(str(dt).replace("torch.", ""))
+    w0, w1, w2 = widths(op, dim)
+    head = torch.empty(n, dtype=dt, device=dev)
+    body = [torch.empty(n, dtype=dt, device=dev) for _ in range(dim)] if w1 else None
+    extra = torch.empty(n, dtype=dt, device=dev) if w2 else None
+    xp = (ctypes.c_void_p * dim)(*[t.data_ptr() for t in ts])
+    bp = (ctypes.c_void_p * dim)(*[t.data_ptr() for t in body]) if body else None
+    kptr = None if ka_arr is None else _ka_address(ka_arr)
+    with torch.cuda.device(dev):
+        rc = _lib.lib().fn_run_soa(op, dim, dcode, ctypes.addressof(xp), n, head.data_ptr(),
+                                   None if bp is None else ctypes.addressof(bp),
+                                   None if extra is None else extra.data_ptr(), kptr,
+                                   _cuda_stream(torch, dev.index))
+    if rc:
+        _lib.check(rc, "fn_run_soa")
+    if host:
+        numpy_in = isinstance(xs[0], np.ndarray)
+        conv = (lambda t: t.cpu().numpy()) if numpy_in else (lambda t: t.cpu())
+        return conv(head), None if body is None else tuple(conv(t) for t in body), \
+            None if extra is None else conv(extra)
+    return head, None if body is None else tuple(body), extra

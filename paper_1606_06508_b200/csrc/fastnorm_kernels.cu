@@ -349,6 +349,136 @@ int run(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* 
     return run_ex(op, dim, dtype, x, n, head, body, sq, ka, nullptr, stream);
 }
 
+// ---------------------------------------------------------------------------------
+// Structure-of-arrays entry: the reference's scalar signatures vectorised over arrays
+// (normalize3(p, x1[], x2[], x3[]) -> r[], (u1[], u2[], u3[])).
+// ---------------------------------------------------------------------------------
+// FASTNORM_B200_SOA=vec selects the register-vector SoA kernel over the bulk-copy one.
+static int soa_path() {
+    static const int v = [] {
+        const char* e = getenv("FASTNORM_B200_SOA");
+        return e && strcmp(e, "vec") == 0 ? 1 : 0;
+    }();
+    return v;
+}
+
+template <typename T, int N, int OP>
+static int launch_soa(const void* const* xs, int64_t n, void* head, void* const* body, void* sq,
+                      const KArgs<T>& ka, cudaStream_t stream) {
+    using Op = RowOp<T, N, OP>;
+    SoaPtrs<T, N> p;
+    for (int c = 0; c < N; ++c) {
+        p.x[c] = static_cast<const T*>(xs[c]);
+        p.body[c] = Op::W1 ? static_cast<T*>(body[c]) : nullptr;
+    }
+    p.head = static_cast<T*>(head);
+    p.extra = static_cast<T*>(sq);
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    bool aligned = aligned16(p.head) && (Op::W2 == 0 || aligned16(p.extra));
+    for (int c = 0; c < N; ++c) aligned = aligned && aligned16(p.x[c]) && (Op::W1 == 0 || aligned16(p.body[c]));
+    constexpr int V = Vec16<T>::kRows;
+    const int sms = device_sms(dev);
+    using ST = SoaTile<T, N, OP>;
+    if (aligned && !force_direct() && soa_path() == 0 && n >= ST::TR) {
+        // bulk-copy pipeline over whole tiles, the rest through the scalar form below
+        static std::once_flag attr_once;
+        std::call_once(attr_once, [] {
+            cudaFuncSetAttribute(tma_soa_kernel<T, N, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 ST::kSmemBytes);
+        });
+        const int64_t ntiles = n / ST::TR;
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)sms * ST::kCtasPerSm));
+        e = launch_pdl(tma_soa_kernel<T, N, OP>, grid, ST::NT, ST::kSmemBytes, stream, p, n, ka);
+        if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+        const int64_t done = ntiles * ST::TR;
+        if (done == n) return FN_OK;
+        for (int c = 0; c < N; ++c) {
+            p.x[c] += done;
+            if (Op::W1) p.body[c] += done;
+        }
+        p.head += done;
+        if (Op::W2) p.extra += done;
+        n -= done;
+    }
+    const int64_t nvec = aligned && !force_direct() ? n / V : 0;
+    if (nvec > 0) {
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nvec + 255) / 256, (int64_t)sms * 8));
+        e = launch_pdl(soa_vec_kernel<T, N, OP>, grid, 256, 0, stream, p, nvec, ka);
+        if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+    }
+    const int64_t done = nvec * V;
+    if (done < n) {  // rows after the last whole vector (or everything, unaligned)
+        SoaPtrs<T, N> t = p;
+        for (int c = 0; c < N; ++c) {
+            t.x[c] += done;
+            if (Op::W1) t.body[c] += done;
+        }
+        t.head += done;
+        if (Op::W2) t.extra += done;
+        const int64_t rest = n - done;
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((rest + 255) / 256, (int64_t)sms * 8));
+        e = launch_pdl(soa_kernel<T, N, OP>, grid, 256, 0, stream, t, rest, ka);
+        if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+    }
+    return FN_OK;
+}
+
+template <typename T, int OP>
+static int soa_dim(int dim, const void* const* xs, int64_t n, void* h, void* const* b, void* q,
+                   const KArgs<T>& ka, cudaStream_t s) {
+    switch (dim) {
+        case 2: return launch_soa<T, 2, OP>(xs, n, h, b, q, ka, s);
+        case 3: return launch_soa<T, 3, OP>(xs, n, h, b, q, ka, s);
+        default: return launch_soa<T, 4, OP>(xs, n, h, b, q, ka, s);
+    }
+}
+
+template <typename T>
+static int dispatch_soa(int op, int dim, const void* const* xs, int64_t n, void* h, void* const* b, void* q,
+                        const double* kad, cudaStream_t s) {
+    KArgs<T> ka;
+    int rc = make_kargs<T>(kad, needs_ka(op), ka);
+    if (rc != FN_OK) return rc;
+    switch (op) {
+        case FN_OP_SCALE: return soa_dim<T, FN_OP_SCALE>(dim, xs, n, h, b, q, ka, s);
+        case FN_OP_NORMALIZE: return soa_dim<T, FN_OP_NORMALIZE>(dim, xs, n, h, b, q, ka, s);
+        case FN_OP_NORMALIZE_SQ: return soa_dim<T, FN_OP_NORMALIZE_SQ>(dim, xs, n, h, b, q, ka, s);
+        case FN_OP_NORM: return soa_dim<T, FN_OP_NORM>(dim, xs, n, h, b, q, ka, s);
+        case FN_OP_NAIVE: return soa_dim<T, FN_OP_NAIVE>(dim, xs, n, h, b, q, ka, s);
+        case FN_OP_QUOTIENT: return soa_dim<T, FN_OP_QUOTIENT>(dim, xs, n, h, b, q, ka, s);
+        case FN_OP_QUOTIENT3_FAST:
+            if (dim != 3) return fail(FN_EINVAL, "quotient3_fast is defined for dim 3 only");
+            return launch_soa<T, 3, FN_OP_QUOTIENT3_FAST>(xs, n, h, b, q, ka, s);
+        default: return fail(FN_EINVAL, "the SoA entry takes the scale / normalize / norm / naive / quotient families");
+    }
+}
+
+int run_soa(int op, int dim, int dtype, const void* const* xs, int64_t n, void* head, void* const* body,
+            void* sq, const double* ka, void* stream) {
+    if (op < FN_OP_SCALE || op > FN_OP_NORMALIZE_SQ) return fail(FN_EINVAL, "unknown op for the SoA entry");
+    if (dim < 2 || dim > 4) return fail(FN_EINVAL, "dim must be 2, 3 or 4");
+    if (dtype != FN_F32 && dtype != FN_F64) return fail(FN_EINVAL, "dtype must be FN_F32/FN_F64");
+    if (n < 0) return fail(FN_EINVAL, "n must be >= 0");
+    if (n == 0) return FN_OK;
+    const Widths w = op_widths(op, dim);
+    if (!xs || !head) return fail(FN_EINVAL, "xs and head must not be NULL");
+    for (int c = 0; c < dim; ++c)
+        if (!xs[c]) return fail(FN_EINVAL, "component array is NULL");
+    if (w.w1) {
+        if (!body) return fail(FN_EINVAL, "body arrays must not be NULL");
+        for (int c = 0; c < dim; ++c)
+            if (!body[c]) return fail(FN_EINVAL, "body array is NULL");
+    } else if (body) {
+        return fail(FN_EINVAL, "this op has no body output; pass NULL");
+    }
+    if (w.w2 && !sq) return fail(FN_EINVAL, "sq output must not be NULL");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (dtype == FN_F64) return dispatch_soa<double>(op, dim, xs, n, head, body, sq, ka, s);
+    return dispatch_soa<float>(op, dim, xs, n, head, body, sq, ka, s);
+}
+
 // Two-input ops: record width of the first input (q: 4, R: 9); the second is v[N,3].
 static int rows2_dim(int op) { return op == FN_OP_QUAT_ROTATE ? 4 : (op == FN_OP_MAT_APPLY ? 9 : 0); }
 
@@ -985,6 +1115,11 @@ int fn_scalar(int op, int dim, int dtype, const double* x, double* out, const do
 int fn_host_run_multi(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* body,
                       void* sq, const double* ka, const int* devices, int ndev) {
     return fnb::host_run_multi(op, dim, dtype, x, n, head, body, sq, ka, devices, ndev);
+}
+
+int fn_run_soa(int op, int dim, int dtype, const void* const* xs, int64_t n, void* head,
+               void* const* body, void* sq, const double* ka, void* stream) {
+    return fnb::run_soa(op, dim, dtype, xs, n, head, body, sq, ka, stream);
 }
 
 int fn_rotate_rows_f64(int op, const double* a, const double* v, int64_t n, double* out,

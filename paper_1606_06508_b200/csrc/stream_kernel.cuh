@@ -227,6 +227,87 @@ __global__ void __launch_bounds__(256) direct_kernel(const T* __restrict__ x, co
 }
 
 // ---------------------------------------------------------------------------------
+// Structure-of-arrays rows: component k of row i is xs[k][i]; outputs likewise (head[i],
+// body[c][i], extra[i]).  Every warp access is a contiguous 256 B run per array, so plain
+// loads and stores coalesce; the arithmetic is the same RowOp as the AoS kernels.
+// ---------------------------------------------------------------------------------
+template <typename T, int N> struct SoaPtrs {
+    const T* x[N];
+    T* head;
+    T* body[N];
+    T* extra;
+};
+
+template <typename T, int N, int OP>
+__global__ void __launch_bounds__(256) soa_kernel(SoaPtrs<T, N> p, int64_t nrows, KArgs<T> ka) {
+    using Op = RowOp<T, N, OP>;
+    static_assert(Op::W0 == 1 && (Op::W1 == 0 || Op::W1 == N) && Op::W2 <= 1, "per-component outputs");
+    grid_dependency_wait();
+    grid_launch_dependents();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nrows; i += stride) {
+        T xr[N], o0[1], o1[Slot<Op::W1>::value], o2[1];
+#pragma unroll
+        for (int c = 0; c < N; ++c) xr[c] = __ldcs(p.x[c] + i);
+        (void)Op::apply(xr, ka, o0, o1, o2);
+        __stcs(p.head + i, o0[0]);
+#pragma unroll
+        for (int c = 0; c < Op::W1; ++c) __stcs(p.body[c] + i, o1[c]);
+        if constexpr (Op::W2 == 1) __stcs(p.extra + i, o2[0]);
+    }
+}
+
+// Vectorised form: each thread moves 16 B per array per step (2 f64 or 4 f32 rows), so
+// every warp request is a contiguous 512 B run.  All arrays must be 16 B aligned; rows
+// past the last whole vector go through the scalar form.
+template <typename T> struct Vec16;
+template <> struct Vec16<double> {
+    using type = double2;
+    static constexpr int kRows = 2;
+    __device__ __forceinline__ static double get(const double2& v, int j) { return j ? v.y : v.x; }
+    __device__ __forceinline__ static double2 make(const double (&a)[2]) { return make_double2(a[0], a[1]); }
+};
+template <> struct Vec16<float> {
+    using type = float4;
+    static constexpr int kRows = 4;
+    __device__ __forceinline__ static float get(const float4& v, int j) {
+        return j == 0 ? v.x : (j == 1 ? v.y : (j == 2 ? v.z : v.w));
+    }
+    __device__ __forceinline__ static float4 make(const float (&a)[4]) { return make_float4(a[0], a[1], a[2], a[3]); }
+};
+
+template <typename T, int N, int OP>
+__global__ void __launch_bounds__(256) soa_vec_kernel(SoaPtrs<T, N> p, int64_t nvec, KArgs<T> ka) {
+    using Op = RowOp<T, N, OP>;
+    using VT = typename Vec16<T>::type;
+    constexpr int V = Vec16<T>::kRows;
+    grid_dependency_wait();
+    grid_launch_dependents();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < nvec; g += stride) {
+        VT xv[N];
+#pragma unroll
+        for (int c = 0; c < N; ++c) xv[c] = __ldcs(reinterpret_cast<const VT*>(p.x[c]) + g);
+        T h[V], b[Slot<Op::W1>::value][V], q[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            T xr[N], o0[1], o1[Slot<Op::W1>::value], o2[1];
+#pragma unroll
+            for (int c = 0; c < N; ++c) xr[c] = Vec16<T>::get(xv[c], j);
+            (void)Op::apply(xr, ka, o0, o1, o2);
+            h[j] = o0[0];
+#pragma unroll
+            for (int c = 0; c < Op::W1; ++c) b[c][j] = o1[c];
+            q[j] = o2[0];
+        }
+        __stcs(reinterpret_cast<VT*>(p.head) + g, Vec16<T>::make(h));
+#pragma unroll
+        for (int c = 0; c < Op::W1; ++c) __stcs(reinterpret_cast<VT*>(p.body[c]) + g, Vec16<T>::make(b[c]));
+        if constexpr (Op::W2 == 1) __stcs(reinterpret_cast<VT*>(p.extra) + g, Vec16<T>::make(q));
+    }
+}
+
+// ---------------------------------------------------------------------------------
 // Bulk-copy (TMA) primitives.
 // ---------------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -525,6 +606,100 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
         }
     }
     count_invalid(ka.invalid, bad);
+    if (leader) bulk_wait_all();
+}
+
+// ---------------------------------------------------------------------------------
+// Structure-of-arrays rows through the bulk-copy pipeline: a tile is TR rows of every
+// component array (one bulk load per array into a per-array smem run), outputs are
+// staged per array and written with one bulk store each.  Same ring / mbarrier /
+// store-group protocol as tma_stream_kernel.
+// ---------------------------------------------------------------------------------
+// 4 KiB runs x 3 stages x 2 CTAs per SM: 0.96 of the copy peak for normalize2/3 f64 and
+// normalize3 f32 (2 KiB runs: 0.84-0.94; 8 KiB: 0.90-1.02; more stages or CTAs lose;
+// profiles/r01da_soa.txt).
+#ifndef FNB_SOA_RUN_BYTES
+#define FNB_SOA_RUN_BYTES 4096
+#endif
+#ifndef FNB_SOA_STAGES
+#define FNB_SOA_STAGES 3
+#endif
+#ifndef FNB_SOA_CTAS_PER_SM
+#define FNB_SOA_CTAS_PER_SM 2
+#endif
+template <typename T, int N, int OP> struct SoaTile {
+    using Op = RowOp<T, N, OP>;
+    static constexpr int TR = FNB_SOA_RUN_BYTES / (int)sizeof(T);  // one run of every array per tile
+    static constexpr int S = FNB_SOA_STAGES, OB = 3, NT = 256;
+    static constexpr int kCtasPerSm = FNB_SOA_CTAS_PER_SM;
+    static constexpr int kOutArrays = 1 + Op::W1 + Op::W2;
+    static constexpr int kArr = TR * (int)sizeof(T);           // bytes of one array's run
+    static constexpr int kInBytes = N * kArr, kOutBytes = kOutArrays * kArr;
+    static constexpr int kSmemBytes = S * kInBytes + OB * kOutBytes + S * 8;
+};
+
+template <typename T, int N, int OP>
+__global__ void __launch_bounds__(256) tma_soa_kernel(SoaPtrs<T, N> p, int64_t nrows, KArgs<T> ka) {
+    using L = SoaTile<T, N, OP>;
+    using Op = typename L::Op;
+    constexpr int TR = L::TR, S = L::S, OB = L::OB, NT = L::NT;
+    constexpr int W1 = Op::W1, W2 = Op::W2;
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned char* s_in = smem;
+    unsigned char* s_out = smem + S * L::kInBytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(s_out + OB * L::kOutBytes);
+    const int64_t ntiles = nrows / TR;
+    const int64_t my_tiles =
+        ntiles > (int64_t)blockIdx.x ? (ntiles - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
+    const bool leader = threadIdx.x == 0;
+    if (leader) {
+#pragma unroll
+        for (int st = 0; st < S; ++st) mbar_init(&full[st], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    grid_dependency_wait();
+    grid_launch_dependents();
+    auto load_stage = [&](int st, int64_t tile) {
+        mbar_arrive_expect_tx(&full[st], L::kInBytes);
+#pragma unroll
+        for (int c = 0; c < N; ++c)
+            bulk_load_plain(s_in + st * L::kInBytes + c * L::kArr, p.x[c] + tile * TR, L::kArr, &full[st]);
+    };
+    if (leader)
+        for (int64_t k = 0; k < my_tiles && k < S; ++k) load_stage((int)k, (int64_t)blockIdx.x + k * gridDim.x);
+    for (int64_t k = 0; k < my_tiles; ++k) {
+        const int st = (int)(k % S);
+        const int ob = (int)(k % OB);
+        const int64_t tile = (int64_t)blockIdx.x + k * gridDim.x;
+        mbar_wait(&full[st], (uint32_t)((k / S) & 1));
+        const T* tin = reinterpret_cast<const T*>(s_in + st * L::kInBytes);
+        T* tout = reinterpret_cast<T*>(s_out + ob * L::kOutBytes);
+#pragma unroll
+        for (int it = 0; it < TR / NT; ++it) {
+            const int j = (int)threadIdx.x + it * NT;
+            T xr[N], o0[1], o1[Slot<W1>::value], o2[1];
+#pragma unroll
+            for (int c = 0; c < N; ++c) xr[c] = tin[c * TR + j];
+            (void)Op::apply(xr, ka, o0, o1, o2);
+            tout[j] = o0[0];
+#pragma unroll
+            for (int c = 0; c < W1; ++c) tout[(1 + c) * TR + j] = o1[c];
+            if constexpr (W2 == 1) tout[(1 + W1) * TR + j] = o2[0];
+        }
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (leader) {
+            const int64_t row0 = tile * TR;
+            bulk_store(p.head + row0, tout, L::kArr);
+#pragma unroll
+            for (int c = 0; c < W1; ++c) bulk_store(p.body[c] + row0, tout + (1 + c) * TR, L::kArr);
+            if constexpr (W2 == 1) bulk_store(p.extra + row0, tout + (1 + W1) * TR, L::kArr);
+            bulk_commit();
+            if (k + S < my_tiles) load_stage(st, tile + (int64_t)S * gridDim.x);
+            bulk_wait_read<OB - 2>();
+        }
+    }
     if (leader) bulk_wait_all();
 }
 

@@ -16,7 +16,7 @@ from __future__ import annotations
 
 from typing import Any, NamedTuple
 
-from paper_1606_06508_b200 import _backend, batch
+from paper_1606_06508_b200 import _backend, _lib, batch
 from paper_1606_06508_b200.params import FpParams
 from paper_1606_06508_b200.scale import check_precision, kernel_args, kernel_args_array
 
@@ -56,7 +56,16 @@ def _scalars(name: str, dim: int, xs):
     return tuple(float(v) for v in xs)
 
 
+def _soa(p: FpParams, op: int, dim: int, xs):
+    """The scalar signature with one array per component (structure of arrays)."""
+    check_precision(p, xs[0])
+    return batch.run_soa(op, dim, xs, kernel_args_array(p))
+
+
 def _normalize(p: FpParams, dim: int, xs, out):
+    if batch.is_soa(xs, dim):
+        h, b, _ = _soa(p, _lib.OP_NORMALIZE, dim, xs)
+        return NormalizeOutcome(h, b)
     if _batched(xs):
         prec = check_precision(p, xs[0])
         res = _backend.batch_kernel(f"normalize{dim}", prec)(xs[0], kernel_args_array(p), out=out)
@@ -67,6 +76,9 @@ def _normalize(p: FpParams, dim: int, xs, out):
 
 
 def _normalize_sq(p: FpParams, dim: int, xs, out):
+    if batch.is_soa(xs, dim):
+        h, b, q = _soa(p, _lib.OP_NORMALIZE_SQ, dim, xs)
+        return NormalizeSqOutcome(q, h, b)
     if _batched(xs):
         prec = check_precision(p, xs[0])
         o = None if out is None else (out[1], out[2], out[0])
@@ -78,6 +90,8 @@ def _normalize_sq(p: FpParams, dim: int, xs, out):
 
 
 def _norm(p: FpParams, dim: int, xs, out):
+    if batch.is_soa(xs, dim):
+        return _soa(p, _lib.OP_NORM, dim, xs)[0]
     if _batched(xs):
         prec = check_precision(p, xs[0])
         o = None if out is None else (out,)

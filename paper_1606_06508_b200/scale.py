@@ -14,7 +14,7 @@ from typing import Any, NamedTuple
 
 import numpy as np
 
-from paper_1606_06508_b200 import _backend, batch
+from paper_1606_06508_b200 import _backend, _lib, batch
 from paper_1606_06508_b200.params import FpParams, require_valid
 
 __all__ = ["ScaleOutcome", "kernel_args", "scale2", "scale3", "scale4"]
@@ -47,6 +47,10 @@ def check_precision(p: FpParams, x) -> str:
 
 
 def _scale(p: FpParams, dim: int, xs, out):
+    if batch.is_soa(xs, dim):  # one array per component (structure of arrays)
+        check_precision(p, xs[0])
+        inv, s, _ = batch.run_soa(_lib.OP_SCALE, dim, xs, kernel_args_array(p))
+        return ScaleOutcome(inv, s)
     if len(xs) == 1 and batch.is_array(xs[0]):
         x = xs[0]
         prec = check_precision(p, x)

@@ -86,6 +86,14 @@ def test_argument_errors_without_gpu():
     assert L.fn_rotate_rows_f64(11, vp(0), vp(0), 0, vp(0), None, None, None) == 0
     assert L.fn_host_rotate_rows_f64(13, x.ctypes.data, x.ctypes.data, 4, b.ctypes.data, None) == -1
     assert L.fn_host_rotate_rows_f64(12, x.ctypes.data, x.ctypes.data, 4, None, None) == -1
+    # structure-of-arrays entry: op range, dim, NULL component / output arrays
+    xs = (ctypes.c_void_p * 3)(x.ctypes.data, x.ctypes.data, x.ctypes.data)
+    bs = (ctypes.c_void_p * 3)(b.ctypes.data, b.ctypes.data, b.ctypes.data)
+    assert L.fn_run_soa(7, 3, 1, ctypes.addressof(xs), 4, h.ctypes.data, ctypes.addressof(bs), None, ka.ctypes.data, None) == -1
+    assert L.fn_run_soa(1, 5, 1, ctypes.addressof(xs), 4, h.ctypes.data, ctypes.addressof(bs), None, ka.ctypes.data, None) == -1
+    assert L.fn_run_soa(1, 3, 1, ctypes.addressof(xs), 4, h.ctypes.data, None, None, ka.ctypes.data, None) == -1
+    assert L.fn_run_soa(2, 3, 1, ctypes.addressof(xs), 4, h.ctypes.data, ctypes.addressof(bs), None, ka.ctypes.data, None) == -1
+    assert L.fn_run_soa(1, 3, 1, None, 0, None, None, None, ka.ctypes.data, None) == 0
     # n == 0 is a no-op success
     assert L.fn_run(1, 3, 1, vp(0), 0, vp(0), vp(0), None, ka.ctypes.data, None) == 0
     assert L.fn_host_run(1, 3, 1, vp(0), 0, vp(0), vp(0), None, ka.ctypes.data) == 0

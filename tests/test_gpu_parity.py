@@ -550,3 +550,59 @@ def test_host_path_small_batches(cuda_dev, small, monkeypatch):
     want = fn.normalize4_rotate(fn.preset("double"), torch.from_numpy(q).to(cuda_dev),
                                 torch.from_numpy(v).to(cuda_dev), strict=False)
     assert oracle.same(got, want.cpu().numpy()).all()
+
+
+@pytest.mark.parametrize("home", ["device", "numpy"])
+def test_structure_of_arrays_calls(cuda_dev, home):
+    """The reference's scalar signatures called with one array per component
+    (normalize3(p, x1[], x2[], x3[]) and friends) run the SoA kernel and equal the AoS
+    batched results bit for bit, for every family, dimension and precision."""
+    for prec, single in (("double", False), ("single", True)):
+        p = fn.preset(prec)
+        for dim in (2, 3, 4):
+            x = _random_rows(100_003, dim, single, seed=17 + dim)
+            xd = torch.from_numpy(x).to(cuda_dev)
+            comps = [xd[:, k].contiguous() for k in range(dim)] if home == "device" else \
+                [np.ascontiguousarray(x[:, k]) for k in range(dim)]
+            as_np = (lambda t: t.cpu().numpy() if hasattr(t, "cpu") else np.asarray(t))  # noqa: E731
+
+            def same(a, b):
+                return oracle.same(as_np(a), as_np(b)).all()
+
+            soa, aos = getattr(fn, f"normalize{dim}")(p, *comps), getattr(fn, f"normalize{dim}")(p, xd)
+            assert same(soa.length, aos.length)
+            assert all(same(soa.unit[k], aos.unit[:, k]) for k in range(dim))
+            soa, aos = getattr(fn, f"normalize{dim}_sq")(p, *comps), getattr(fn, f"normalize{dim}_sq")(p, xd)
+            assert same(soa.squared_length, aos.squared_length) and same(soa.length, aos.length)
+            assert same(getattr(fn, f"norm{dim}")(p, *comps), getattr(fn, f"norm{dim}")(p, xd))
+            soa, aos = getattr(fn, f"scale{dim}")(p, *comps), getattr(fn, f"scale{dim}")(p, xd)
+            assert same(soa.inv_sigma, aos.inv_sigma)
+            assert all(same(soa.scaled[k], aos.scaled[:, k]) for k in range(dim))
+            bases = [getattr(fn, f"naive_normalize{dim}"), {2: fn.quotient2, 3: fn.quotient3_robust,
+                                                            4: fn.quotient4}[dim]]
+            if dim == 3:
+                bases.append(fn.quotient3_fast)
+            for f in bases:
+                soa, aos = f(*comps), f(xd)
+                assert same(soa.length, aos.length), f.__name__
+                assert all(same(soa.unit[k], aos.unit[:, k]) for k in range(dim)), f.__name__
+
+
+def test_structure_of_arrays_unaligned_and_tails(cuda_dev):
+    """Component arrays at an 8-byte offset (scalar SoA kernel) and lengths that leave a
+    partial 16-byte vector (vector kernel + scalar tail) give the AoS results."""
+    p = fn.preset("double")
+    for n in (1, 2, 3, 5, 1001):
+        x = _random_rows(n, 3, False, seed=n)
+        xd = torch.from_numpy(x).to(cuda_dev)
+        want = fn.normalize3(p, xd)
+        big = [torch.from_numpy(np.concatenate([[0.0], x[:, k]])).to(cuda_dev)[1:] for k in range(3)]
+        for comps in (big, [xd[:, k].contiguous() for k in range(3)]):
+            got = fn.normalize3(p, *comps)
+            assert oracle.same(got.length.cpu().numpy(), want.length.cpu().numpy()).all()
+            for k in range(3):
+                assert oracle.same(got.unit[k].cpu().numpy(), want.unit[:, k].cpu().numpy()).all()
+    x32 = _random_rows(4099, 3, True, seed=1)
+    comps = [torch.from_numpy(np.ascontiguousarray(x32[:, k])).to(cuda_dev) for k in range(3)]
+    got, want = fn.normalize3(fn.preset("single"), *comps), fn.normalize3(fn.preset("single"), torch.from_numpy(x32).to(cuda_dev))
+    assert all(oracle.same(got.unit[k].cpu().numpy(), want.unit[:, k].cpu().numpy()).all() for k in range(3))
