@@ -39,9 +39,23 @@ def main():
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1) / 1e3)
     t = statistics.median(times)
+    # the same harness around a 1-row launch: the launch + event floor of a lone launch
+    x1 = x[:1].contiguous()
+    floor = []
+    for _ in range(30):
+        flush.sum(dtype=torch.int32)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn.normalize3(p, x1)
+        e1.record()
+        torch.cuda.synchronize()
+        floor.append(e0.elapsed_time(e1) / 1e3)
+    t_floor = statistics.median(floor)
     sob = bench._batch_stream_rate(fn, p, x, 56, peak, 10)
     print(json.dumps({"env": {k: v for k, v in os.environ.items() if k.startswith("FASTNORM_B200")},
                       "lone_ms": t * 1e3, "lone_frac": c.rows * 56 / t / 1e9 / peak,
+                      "one_row_launch_ms": t_floor * 1e3,
+                      "lone_minus_floor_frac": c.rows * 56 / (t - t_floor) / 1e9 / peak,
                       "stream_ms": sob["ms_per_launch"], "stream_frac": sob["frac"],
                       "eager_ms": sob["eager_public_api"]["ms_per_launch"],
                       "eager_frac": sob["eager_public_api"]["frac"]}), flush=True)
