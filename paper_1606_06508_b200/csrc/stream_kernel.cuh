@@ -495,6 +495,22 @@ template <typename T, int N> struct OpRows<T, N, FN_OP_NORMALIZE_ROT> {
 
 // HINTS: bit 0 -> input loads carry an L2 evict-first policy (read once);
 //        bit 1 -> output bulk stores carry an L2 evict-first policy.
+// Per-CTA timeline (developer probe tools/probe/cfg1_timeline.cu only; compiled out of
+// the library): thread 0 of each CTA stores %globaltimer at five points of the kernel
+// into fnb_timeline[blockIdx.x * 5 + slot].
+#ifdef FNB_TIMELINE
+__device__ unsigned long long* fnb_timeline;
+__device__ __forceinline__ void timeline_mark(int slot) {
+    if (threadIdx.x == 0 && fnb_timeline != nullptr) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        fnb_timeline[blockIdx.x * 5 + slot] = t;
+    }
+}
+#else
+__device__ __forceinline__ void timeline_mark(int) {}
+#endif
+
 template <typename T, int N, int OP, int TR_ = OpRows<T, N, OP>::value, int S_ = OpStages<T, N, OP>::value,
           int NT = Tile<T, N>::kThreads, int HINTS = Tile<T, N>::kHints, int OB_ = OutTiles<OP>::value>
 __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x, const T* __restrict__ x2,
@@ -511,6 +527,7 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
     unsigned char* s_in2 = smem + S * L::kInBytes;  // second input ring (two-input ops)
     unsigned char* s_out = s_in2 + S * L::kIn2Bytes;
     uint64_t* full = reinterpret_cast<uint64_t*>(s_out + OB * L::kOutBytes);
+    timeline_mark(0);
 
     const int64_t ntiles = nrows / TR;
     const int64_t my_tiles =
@@ -528,6 +545,7 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
     __syncthreads();
     grid_dependency_wait();
     grid_launch_dependents();
+    timeline_mark(1);
     // One stage = the tile's input records (and its second-input records), one mbarrier.
     auto load_stage = [&](int st, int64_t tile) {
         mbar_arrive_expect_tx(&full[st], L::kInBytes + L::kIn2Bytes);
@@ -548,6 +566,7 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
         const int ob = (int)(k % OB);
         const int64_t tile = (int64_t)blockIdx.x + k * gridDim.x;
         mbar_wait(&full[s], parity);
+        if (k == 0) timeline_mark(2);
 
         const T* tin = reinterpret_cast<const T*>(s_in + s * L::kInBytes);
         const T* tin2 = reinterpret_cast<const T*>(s_in2 + s * L::kIn2Bytes);
@@ -605,8 +624,10 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
             if (i < nrows) bad += row_global<T, N, OP>(x, x2, i, head, body, extra, ka) ? 0 : 1;
         }
     }
+    timeline_mark(3);
     count_invalid(ka.invalid, bad);
     if (leader) bulk_wait_all();
+    timeline_mark(4);
 }
 
 // ---------------------------------------------------------------------------------
