@@ -100,6 +100,15 @@ int fn_device_count(void);
  * for the naive / quotient families, which take no constants (_kernels.pyx:481-520). */
 int fn_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* body,
            void* sq, const double* ka, void* stream);
+/* fn_run over rows that are ldx elements apart (ldx >= dim): row i is x[i*ldx .. i*ldx+dim),
+ * the other ldx - dim elements of each record are not used.  Padded records such as xyz
+ * in xyzw (dim 3, ldx 4; float4-style 16 B / 32 B records) and views like X[:, :3] of a
+ * wider array run without a gather copy.  dim 3 with ldx 4 and 16 B aligned buffers uses
+ * the bulk-copy kernel (whole records staged, the first three elements read); other
+ * strides use the per-row kernel.  Outputs are dense, as for fn_run.  ldx == dim is
+ * fn_run.  No reference interface: the reference takes one row per call. */
+int fn_run_ld(int op, int dim, int dtype, const void* x, int64_t n, int64_t ldx, void* head,
+              void* body, void* sq, const double* ka, void* stream);
 int fn_host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head,
                 void* body, void* sq, const double* ka);
 /* Structure-of-arrays rows on the device: the reference's scalar signatures vectorised

@@ -193,6 +193,19 @@ def _cuda_stream(torch, dev: int) -> int:
     return _stream_of(dev)
 
 
+def _overlaps(x, n: int, ldx: int, dim: int, outs) -> bool:
+    """Whether any output tensor's bytes meet the span of strided rows x."""
+    es = x.element_size()
+    lo = x.data_ptr()
+    hi = lo + ((n - 1) * ldx + dim) * es
+    for o in outs:
+        if o is not None and o.numel():
+            a = o.data_ptr()
+            if a < hi and lo < a + o.numel() * es:
+                return True
+    return False
+
+
 def run(op: int, dim: int, x, ka_arr: np.ndarray | None, out=None, invalid=None) -> BatchOut:
     """Run kernel family ``op`` over rows ``x[N, dim]``; return (head, body, extra).
 
@@ -218,7 +231,15 @@ def run(op: int, dim: int, x, ka_arr: np.ndarray | None, out=None, invalid=None)
         if dcode is None:
             dcode = _dcode_of[x.dtype] = _dtype_code(str(x.dtype).replace("torch.", ""))
         if x.is_cuda:
-            x = x.contiguous()
+            # Rows that are ldx elements apart (padded records, X[:, :dim] of a wider
+            # array) go to fn_run_ld as they are; any other layout is gathered first.
+            ldx = dim
+            rot = op in (_lib.OP_ROT_UNIT, _lib.OP_ROT_GENERAL, _lib.OP_NORMALIZE_ROT)
+            if not x.is_contiguous():
+                if not rot and x.stride(1) == 1 and x.stride(0) >= dim and n > 0:
+                    ldx = int(x.stride(0))
+                else:
+                    x = x.contiguous()
 
             def alloc(o, w, what):
                 if not w:
@@ -227,6 +248,9 @@ def run(op: int, dim: int, x, ka_arr: np.ndarray | None, out=None, invalid=None)
                 return o if o is not None else x.new_empty(_shape(n, w))
 
             head, body, extra = alloc(o_head, w0, "head"), alloc(o_body, w1, "body"), alloc(o_extra, w2, "extra")
+            if ldx != dim and _overlaps(x, n, ldx, dim, (head, body, extra)):
+                # an output written over strided input rows of other tiles: gather first
+                x, ldx = x.contiguous(), dim
             ptr = (lambda t: None if t is None else t.data_ptr())
             dev = x.device.index
             # The library launches on the thread's current CUDA device (shared with torch
@@ -237,9 +261,12 @@ def run(op: int, dim: int, x, ka_arr: np.ndarray | None, out=None, invalid=None)
                 ctx.__enter__()
             try:
                 stream = _cuda_stream(torch, dev)
-                if op in (_lib.OP_ROT_UNIT, _lib.OP_ROT_GENERAL, _lib.OP_NORMALIZE_ROT):
+                if rot:
                     rc = L.fn_run_rot(op, x.data_ptr(), n, ptr(head), ptr(body), ptr(extra), kptr,
                                       ptr(invalid), stream)
+                elif ldx != dim:
+                    rc = L.fn_run_ld(op, dim, dcode, x.data_ptr(), n, ldx, ptr(head), ptr(body), ptr(extra),
+                                     kptr, stream)
                 else:
                     fast = _fast_run()
                     call = fast.run if fast is not None else L.fn_run

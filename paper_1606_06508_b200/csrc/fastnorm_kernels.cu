@@ -87,15 +87,19 @@ static bool is_rotation(int op) {
 }
 
 // Per-instantiation occupancy (computed once per process and device).
-template <typename T, int N, int OP> struct TmaLaunch {
-    using L = TileLayout<T, N, OP, OpRows<T, N, OP>::value, OpStages<T, N, OP>::value>;
+template <typename T, int N, int OP, int LDX = 0> struct TmaLaunch {
+    using L = TileLayout<T, N, OP, OpRows<T, N, OP>::value, OpStages<T, N, OP>::value, OutTiles<OP>::value, LDX>;
+    static constexpr auto kernel() {
+        return tma_stream_kernel<T, N, OP, OpRows<T, N, OP>::value, OpStages<T, N, OP>::value, Tile<T, N>::kThreads,
+                                 Tile<T, N>::kHints, OutTiles<OP>::value, LDX>;
+    }
     static int blocks_per_sm(int dev) {
         static std::mutex mu;
         static int cache[64] = {0};
         std::lock_guard<std::mutex> lk(mu);
         if (dev < 0 || dev >= 64) return 1;
         if (cache[dev] == 0) {
-            auto kern = tma_stream_kernel<T, N, OP>;
+            auto kern = kernel();
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemBytes);
             int nb = 0;
             if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, Tile<T, N>::kThreads,
@@ -172,9 +176,28 @@ static int ctas_per_sm_for(int64_t ntiles, int sms) {
     return tiles_per_cta < 32 ? 64 : CtasPerSm<OP>::value;
 }
 
+// Input records of LDX elements, N of them read per row (LDX > N only for N = 3, LDX = 4,
+// the xyz-in-xyzw layout; other strides take the per-row kernel).
+template <int N> struct PaddedLdx {
+    static constexpr int value = N == 3 ? 4 : 0;
+};
+
+template <typename T, int N, int OP, int LDX = 0>
+static cudaError_t launch_tma(const T* x, const T* x2, int64_t n, T* head, T* body, T* extra, const KArgs<T>& ka,
+                              int dev, int sms, cudaStream_t stream) {
+    using TL = TmaLaunch<T, N, OP, LDX>;
+    using L = typename TL::L;
+    const int64_t ntiles = n / L::TR;
+    const int64_t per_sm = std::min<int64_t>(TL::blocks_per_sm(dev), ctas_per_sm_for<OP>(ntiles, sms));
+    const int64_t resident = per_sm * sms;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, resident));
+    return launch_pdl(TL::kernel(), grid, Tile<T, N>::kThreads, L::kSmemBytes, stream, x, x2, n, head, body, extra,
+                      ka);
+}
+
 template <typename T, int N, int OP>
 static int launch(const void* xv, const void* x2v, int64_t n, void* hv, void* bv, void* qv,
-                  const KArgs<T>& ka, cudaStream_t stream) {
+                  const KArgs<T>& ka, cudaStream_t stream, int64_t ldx = N) {
     using TL = TmaLaunch<T, N, OP>;
     using L = typename TL::L;
     using Op = typename L::Op;
@@ -191,17 +214,15 @@ static int launch(const void* xv, const void* x2v, int64_t n, void* hv, void* bv
     const int sms = device_sms(dev);
     const bool aligned = aligned16(x) && (N2 == 0 || aligned16(x2)) && aligned16(head) &&
                          (Op::W1 == 0 || aligned16(body)) && (Op::W2 == 0 || aligned16(extra));
-    if (aligned && !force_direct() && n >= (int64_t)L::TR) {
-        const int64_t ntiles = n / L::TR;
-        const int64_t per_sm = std::min<int64_t>(TL::blocks_per_sm(dev), ctas_per_sm_for<OP>(ntiles, sms));
-        const int64_t resident = per_sm * sms;
-        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, resident));
-        e = launch_pdl(tma_stream_kernel<T, N, OP>, grid, Tile<T, N>::kThreads, L::kSmemBytes,
-                       stream, x, x2, n, head, body, extra, ka);
+    constexpr int kPad = PaddedLdx<N>::value;
+    if (aligned && !force_direct() && ldx == N && n >= (int64_t)L::TR) {
+        e = launch_tma<T, N, OP>(x, x2, n, head, body, extra, ka, dev, sms, stream);
+    } else if (kPad > 0 && aligned && !force_direct() && ldx == kPad && n > (int64_t)L::TR) {
+        if constexpr (kPad > 0 && N2 == 0) e = launch_tma<T, N, OP, kPad>(x, x2, n, head, body, extra, ka, dev, sms, stream);
     } else {
         const int64_t want = (n + 255) / 256;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 8));
-        e = launch_pdl(direct_kernel<T, N, OP>, grid, 256, 0, stream, x, x2, n, head, body, extra, ka);
+        e = launch_pdl(direct_kernel<T, N, OP>, grid, 256, 0, stream, x, x2, n, head, body, extra, ka, ldx);
     }
     if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
     e = cudaGetLastError();
@@ -260,11 +281,11 @@ static int make_kargs_op(int op, const double* ka, bool needed, KArgs<T>& out) {
 
 template <typename T, int OP>
 static int dispatch_dim(int dim, const void* x, int64_t n, void* h, void* b, void* q,
-                        const KArgs<T>& ka, cudaStream_t s) {
+                        const KArgs<T>& ka, cudaStream_t s, int64_t ldx) {
     switch (dim) {
-        case 2: return launch<T, 2, OP>(x, nullptr, n, h, b, q, ka, s);
-        case 3: return launch<T, 3, OP>(x, nullptr, n, h, b, q, ka, s);
-        case 4: return launch<T, 4, OP>(x, nullptr, n, h, b, q, ka, s);
+        case 2: return launch<T, 2, OP>(x, nullptr, n, h, b, q, ka, s, ldx);
+        case 3: return launch<T, 3, OP>(x, nullptr, n, h, b, q, ka, s, ldx);
+        case 4: return launch<T, 4, OP>(x, nullptr, n, h, b, q, ka, s, ldx);
         default: return fail(FN_EINVAL, "dim must be 2, 3 or 4");
     }
 }
@@ -276,38 +297,38 @@ static bool needs_ka(int op) {
 
 template <typename T>
 static int dispatch(int op, int dim, const void* x, int64_t n, void* h, void* b, void* q,
-                    const double* kad, unsigned long long* invalid, cudaStream_t s) {
+                    const double* kad, unsigned long long* invalid, cudaStream_t s, int64_t ldx) {
     KArgs<T> ka;
     int rc = make_kargs<T>(kad, needs_ka(op), ka);
     if (rc != FN_OK) return rc;
     ka.invalid = invalid;
     switch (op) {
-        case FN_OP_SCALE: return dispatch_dim<T, FN_OP_SCALE>(dim, x, n, h, b, q, ka, s);
-        case FN_OP_NORMALIZE: return dispatch_dim<T, FN_OP_NORMALIZE>(dim, x, n, h, b, q, ka, s);
+        case FN_OP_SCALE: return dispatch_dim<T, FN_OP_SCALE>(dim, x, n, h, b, q, ka, s, ldx);
+        case FN_OP_NORMALIZE: return dispatch_dim<T, FN_OP_NORMALIZE>(dim, x, n, h, b, q, ka, s, ldx);
         case FN_OP_NORMALIZE_SQ:
-            return dispatch_dim<T, FN_OP_NORMALIZE_SQ>(dim, x, n, h, b, q, ka, s);
-        case FN_OP_NORM: return dispatch_dim<T, FN_OP_NORM>(dim, x, n, h, b, q, ka, s);
-        case FN_OP_NAIVE: return dispatch_dim<T, FN_OP_NAIVE>(dim, x, n, h, b, q, ka, s);
-        case FN_OP_QUOTIENT: return dispatch_dim<T, FN_OP_QUOTIENT>(dim, x, n, h, b, q, ka, s);
+            return dispatch_dim<T, FN_OP_NORMALIZE_SQ>(dim, x, n, h, b, q, ka, s, ldx);
+        case FN_OP_NORM: return dispatch_dim<T, FN_OP_NORM>(dim, x, n, h, b, q, ka, s, ldx);
+        case FN_OP_NAIVE: return dispatch_dim<T, FN_OP_NAIVE>(dim, x, n, h, b, q, ka, s, ldx);
+        case FN_OP_QUOTIENT: return dispatch_dim<T, FN_OP_QUOTIENT>(dim, x, n, h, b, q, ka, s, ldx);
         case FN_OP_QUOTIENT3_FAST:
             if (dim != 3) return fail(FN_EINVAL, "quotient3_fast is defined for dim 3 only");
-            return launch<T, 3, FN_OP_QUOTIENT3_FAST>(x, nullptr, n, h, b, q, ka, s);
+            return launch<T, 3, FN_OP_QUOTIENT3_FAST>(x, nullptr, n, h, b, q, ka, s, ldx);
         default: return fail(FN_EINVAL, "unknown op");
     }
 }
 
 // Rotations: quaternions in binary64 only (the reference computes them in Python floats).
 static int dispatch_rot(int op, const void* x, int64_t n, void* h, void* b, void* q,
-                        const double* kad, unsigned long long* invalid, cudaStream_t s) {
+                        const double* kad, unsigned long long* invalid, cudaStream_t s, int64_t ldx) {
     KArgs<double> ka;
     int rc = make_kargs_op<double>(op, kad, needs_ka(op), ka);
     if (rc != FN_OK) return rc;
     ka.invalid = invalid;
     switch (op) {
-        case FN_OP_ROT_UNIT: return launch<double, 4, FN_OP_ROT_UNIT>(x, nullptr, n, h, b, q, ka, s);
-        case FN_OP_ROT_GENERAL: return launch<double, 4, FN_OP_ROT_GENERAL>(x, nullptr, n, h, b, q, ka, s);
-        case FN_OP_NORMALIZE_ROT: return launch<double, 4, FN_OP_NORMALIZE_ROT>(x, nullptr, n, h, b, q, ka, s);
-        case FN_OP_ROT_APPLY: return launch<double, 3, FN_OP_ROT_APPLY>(x, nullptr, n, h, b, q, ka, s);
+        case FN_OP_ROT_UNIT: return launch<double, 4, FN_OP_ROT_UNIT>(x, nullptr, n, h, b, q, ka, s, ldx);
+        case FN_OP_ROT_GENERAL: return launch<double, 4, FN_OP_ROT_GENERAL>(x, nullptr, n, h, b, q, ka, s, ldx);
+        case FN_OP_NORMALIZE_ROT: return launch<double, 4, FN_OP_NORMALIZE_ROT>(x, nullptr, n, h, b, q, ka, s, ldx);
+        case FN_OP_ROT_APPLY: return launch<double, 3, FN_OP_ROT_APPLY>(x, nullptr, n, h, b, q, ka, s, ldx);
         default: return fail(FN_EINVAL, "unknown rotation op");
     }
 }
@@ -334,14 +355,18 @@ int check_args(int op, int dim, int dtype, const void* x, int64_t n, const void*
     return FN_OK;
 }
 
+// ldx: elements from one input row to the next (0 = dim, dense rows).
 int run_ex(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* body, void* sq,
-           const double* ka, unsigned long long* invalid, void* stream) {
+           const double* ka, unsigned long long* invalid, void* stream, int64_t ldx = 0) {
     int rc = check_args(op, dim, dtype, x, n, head, body, sq);
     if (rc != FN_OK || n == 0) return rc;
+    if (ldx == 0) ldx = dim;
+    if (ldx < dim) return fail(FN_EINVAL, "ldx (elements per input row) must be >= dim");
+    if (ldx > (INT64_MAX - dim) / n) return fail(FN_EINVAL, "n * ldx overflows");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (is_rotation(op)) return dispatch_rot(op, x, n, head, body, sq, ka, invalid, s);
-    if (dtype == FN_F64) return dispatch<double>(op, dim, x, n, head, body, sq, ka, invalid, s);
-    return dispatch<float>(op, dim, x, n, head, body, sq, ka, invalid, s);
+    if (is_rotation(op)) return dispatch_rot(op, x, n, head, body, sq, ka, invalid, s, ldx);
+    if (dtype == FN_F64) return dispatch<double>(op, dim, x, n, head, body, sq, ka, invalid, s, ldx);
+    return dispatch<float>(op, dim, x, n, head, body, sq, ka, invalid, s, ldx);
 }
 
 int run(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* body, void* sq,
@@ -1077,6 +1102,12 @@ int fn_device_count(void) {
 int fn_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* body, void* sq,
            const double* ka, void* stream) {
     return fnb::run(op, dim, dtype, x, n, head, body, sq, ka, stream);
+}
+
+int fn_run_ld(int op, int dim, int dtype, const void* x, int64_t n, int64_t ldx, void* head, void* body,
+              void* sq, const double* ka, void* stream) {
+    if (ldx < 1) return fnb::set_error(FN_EINVAL, "ldx must be >= dim");
+    return fnb::run_ex(op, dim, dtype, x, n, head, body, sq, ka, nullptr, stream, ldx);
 }
 
 int fn_host_alloc(size_t bytes, void** ptr) {

@@ -167,16 +167,18 @@ __device__ __forceinline__ bool apply_op(const T (&x)[N], const T (&x2)[N2S], co
         return Op::apply(x, ka, o0, o1, o2);
 }
 
-// One row through global memory (tails, unaligned arrays, tiny batches).
+// One row through global memory (tails, unaligned arrays, tiny batches).  Row i of x
+// starts at element i * ldx (ldx = N for dense records; larger for padded records such
+// as xyz in xyzw, whose extra elements are not read).
 template <typename T, int N, int OP>
 __device__ __forceinline__ bool row_global(const T* __restrict__ x, const T* __restrict__ x2, int64_t i,
                                            T* __restrict__ head, T* __restrict__ body,
-                                           T* __restrict__ extra, const KArgs<T>& ka) {
+                                           T* __restrict__ extra, const KArgs<T>& ka, int64_t ldx = N) {
     using Op = RowOp<T, N, OP>;
     constexpr int N2 = InWidth2<Op>::value;
     T xr[N], x2r[Slot<N2>::value], o0[Slot<Op::W0>::value], o1[Slot<Op::W1>::value], o2[Slot<Op::W2>::value];
 #pragma unroll
-    for (int c = 0; c < N; ++c) xr[c] = __ldg(x + i * N + c);
+    for (int c = 0; c < N; ++c) xr[c] = __ldg(x + i * ldx + c);
 #pragma unroll
     for (int c = 0; c < N2; ++c) x2r[c] = __ldg(x2 + i * N2 + c);
     const bool ok = apply_op<Op>(xr, x2r, ka, o0, o1, o2);
@@ -213,7 +215,7 @@ template <typename T, int N, int OP>
 __global__ void __launch_bounds__(256) direct_kernel(const T* __restrict__ x, const T* __restrict__ x2,
                                                      int64_t nrows, T* __restrict__ head,
                                                      T* __restrict__ body, T* __restrict__ extra,
-                                                     KArgs<T> ka) {
+                                                     KArgs<T> ka, int64_t ldx) {
     grid_dependency_wait();
     grid_launch_dependents();
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -222,7 +224,7 @@ __global__ void __launch_bounds__(256) direct_kernel(const T* __restrict__ x, co
     const int64_t trips = nrows > start ? (nrows - 1 - start) / stride + 1 : 0;
     // uniform trip count per warp so the shuffle-reduce below sees every lane
     for (int64_t t = 0, i = start; t < trips; ++t, i += stride)
-        bad += row_global<T, N, OP>(x, x2, i, head, body, extra, ka) ? 0 : 1;
+        bad += row_global<T, N, OP>(x, x2, i, head, body, extra, ka, ldx) ? 0 : 1;
     count_invalid(ka.invalid, bad);
 }
 
@@ -430,13 +432,17 @@ template <int OP> struct OutTiles {
         (OP == FN_OP_ROT_UNIT || OP == FN_OP_ROT_GENERAL || OP == FN_OP_NORMALIZE_ROT) ? FNB_ROT_OUT_TILES : 3;
 };
 
-template <typename T, int N, int OP, int TR_, int S_, int OB_ = OutTiles<OP>::value> struct TileLayout {
+// LDX_: elements per input record (0 = N, dense rows; N = 3 with LDX_ = 4 reads xyz out of
+// xyzw records: the bulk copy moves whole records, the row op reads the first N).
+template <typename T, int N, int OP, int TR_, int S_, int OB_ = OutTiles<OP>::value, int LDX_ = 0> struct TileLayout {
     using Op = RowOp<T, N, OP>;
     static constexpr int TR = TR_;
     static constexpr int S = S_;
     static constexpr int OB = OB_;  // output staging tiles (bulk-store groups in flight)
+    static constexpr int LDX = LDX_ > 0 ? LDX_ : N;
     static_assert(OB >= 3, "the store pipeline keeps OB - 2 groups reading behind the current one");
-    static constexpr int kInBytes = TR * N * (int)sizeof(T);
+    static_assert(LDX >= N, "an input record holds at least the N components");
+    static constexpr int kInBytes = TR * LDX * (int)sizeof(T);
     static constexpr int kIn2Bytes = TR * InWidth2<Op>::value * (int)sizeof(T);  // second input
     static constexpr int kB0 = TR * Op::W0 * (int)sizeof(T);
     static constexpr int kB1 = TR * Op::W1 * (int)sizeof(T);
@@ -512,14 +518,15 @@ __device__ __forceinline__ void timeline_mark(int) {}
 #endif
 
 template <typename T, int N, int OP, int TR_ = OpRows<T, N, OP>::value, int S_ = OpStages<T, N, OP>::value,
-          int NT = Tile<T, N>::kThreads, int HINTS = Tile<T, N>::kHints, int OB_ = OutTiles<OP>::value>
+          int NT = Tile<T, N>::kThreads, int HINTS = Tile<T, N>::kHints, int OB_ = OutTiles<OP>::value,
+          int LDX_ = 0>
 __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x, const T* __restrict__ x2,
                                                         int64_t nrows, T* __restrict__ head,
                                                         T* __restrict__ body, T* __restrict__ extra,
                                                         KArgs<T> ka) {
-    using L = TileLayout<T, N, OP, TR_, S_, OB_>;
+    using L = TileLayout<T, N, OP, TR_, S_, OB_, LDX_>;
     using Op = typename L::Op;
-    constexpr int TR = L::TR, S = L::S, OB = L::OB;
+    constexpr int TR = L::TR, S = L::S, OB = L::OB, LDX = L::LDX;
     constexpr int W0 = Op::W0, W1 = Op::W1, W2 = Op::W2;
     constexpr int N2 = InWidth2<Op>::value;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -529,7 +536,9 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
     uint64_t* full = reinterpret_cast<uint64_t*>(s_out + OB * L::kOutBytes);
     timeline_mark(0);
 
-    const int64_t ntiles = nrows / TR;
+    // Padded records: the last row may end at its N-th element (a strided view of a
+    // shorter allocation), so it never rides in a bulk tile that would read its padding.
+    const int64_t ntiles = (LDX == N ? nrows : nrows - 1) / TR;
     const int64_t my_tiles =
         ntiles > (int64_t)blockIdx.x ? (ntiles - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
     const bool leader = threadIdx.x == 0;
@@ -550,9 +559,9 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
     auto load_stage = [&](int st, int64_t tile) {
         mbar_arrive_expect_tx(&full[st], L::kInBytes + L::kIn2Bytes);
         if (HINTS & 1)
-            bulk_load(s_in + st * L::kInBytes, x + tile * TR * N, L::kInBytes, &full[st], policy);
+            bulk_load(s_in + st * L::kInBytes, x + tile * TR * LDX, L::kInBytes, &full[st], policy);
         else
-            bulk_load_plain(s_in + st * L::kInBytes, x + tile * TR * N, L::kInBytes, &full[st]);
+            bulk_load_plain(s_in + st * L::kInBytes, x + tile * TR * LDX, L::kInBytes, &full[st]);
         if constexpr (N2 > 0)
             bulk_load_plain(s_in2 + st * L::kIn2Bytes, x2 + tile * TR * N2, L::kIn2Bytes, &full[st]);
     };
@@ -576,7 +585,7 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
         auto row = [&](int j) {
             T xr[N], x2r[Slot<N2>::value], o0[Slot<W0>::value], o1[Slot<W1>::value], o2[Slot<W2>::value];
 #pragma unroll
-            for (int c = 0; c < N; ++c) xr[c] = tin[j * N + c];
+            for (int c = 0; c < N; ++c) xr[c] = tin[j * LDX + c];
 #pragma unroll
             for (int c = 0; c < N2; ++c) x2r[c] = tin2[j * N2 + c];
             bad += apply_op<Op>(xr, x2r, ka, o0, o1, o2) ? 0 : 1;
@@ -621,7 +630,7 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
         const int64_t tail = nrows - ntiles * TR;
         for (int64_t j = threadIdx.x & ~31; j < tail; j += NT) {
             const int64_t i = ntiles * TR + j + (threadIdx.x & 31);
-            if (i < nrows) bad += row_global<T, N, OP>(x, x2, i, head, body, extra, ka) ? 0 : 1;
+            if (i < nrows) bad += row_global<T, N, OP>(x, x2, i, head, body, extra, ka, LDX) ? 0 : 1;
         }
     }
     timeline_mark(3);

@@ -168,6 +168,81 @@ def test_out_buffers_and_noncontiguous(cuda_dev):
         fn.normalize4(p, x, out=(r[:10], u))
 
 
+def _padded(x_np, ldx, dev, fill=np.nan, offset=0):
+    """Rows of x as a [N, dim] view into [N, ldx] records (extra elements = fill), the
+    storage shifted by `offset` elements."""
+    n, dim = x_np.shape
+    buf = torch.full((offset + n * ldx,), fill, dtype=torch.from_numpy(x_np).dtype, device=dev)
+    rec = buf[offset:].view(n, ldx)
+    rec[:, :dim] = torch.from_numpy(x_np).to(dev)
+    return rec[:, :dim]
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("n", [1, 255, 256, 257, 513, 4099, (1 << 20) + 3])
+def test_padded_records_xyz_in_xyzw(cuda_dev, prec, n):
+    """xyz out of xyzw records (fn_run_ld, ldx 4): the bulk-copy kernel stages whole
+    records; every family, bit for bit against the oracle; padding never read into a row."""
+    single = prec == "f32"
+    x = _random_rows(n, 3, single, seed=n + single)
+    xv = _padded(x, 4, cuda_dev)
+    assert n == 1 or not xv.is_contiguous()  # torch calls one row contiguous whatever its stride
+    ka = np.array(fn.kernel_args(fn.preset(PREC[prec])))
+    for fam in FAMILIES[3] + ["normalize_sq"]:
+        base = "normalize3_sq" if fam == "normalize_sq" else _base(fam, 3)
+        op = _lib.OP_NORMALIZE_SQ if fam == "normalize_sq" else OPS[fam]
+        takes = fam in SCALING or fam == "normalize_sq"
+        res = _cuda_kernels.batch_kernel(base, prec)(xv, ka if takes else None)
+        torch.cuda.synchronize()
+        bad, first = compare_chunked(op, xv, res.head, res.body, res.sq, ka if takes else None)
+        assert bad == 0, (fam, prec, n, bad, first)
+
+
+def test_strided_rows_other_layouts(cuda_dev):
+    """Other row strides (per-row kernel), a misaligned padded view, a last record that
+    ends at its third element, rotation apply on padded vectors, and outputs overlapping
+    strided input (gathered first)."""
+    p = fn.preset("double")
+    ka = np.array(fn.kernel_args(p))
+    n = 5003
+    for dim, ldx in ((2, 3), (3, 5), (4, 6), (3, 4)):
+        x = _random_rows(n, dim, False, seed=ldx * 7 + dim)
+        for offset in (0, 1):
+            xv = _padded(x, ldx, cuda_dev, offset=offset)
+            res = _cuda_kernels.batch_kernel(f"normalize{dim}", "f64")(xv, ka)
+            torch.cuda.synchronize()
+            bad, first = compare_chunked(_lib.OP_NORMALIZE, xv, res.head, res.body, None, ka)
+            assert bad == 0, (dim, ldx, offset, first)
+    # storage ends right after the last row's z: the last row must not ride in a tile
+    x = _random_rows(4 * 256 + 1, 3, False, seed=77)
+    m = x.shape[0]
+    buf = torch.full(((m - 1) * 4 + 3,), np.nan, dtype=torch.float64, device=cuda_dev)
+    xv = buf.as_strided((m, 3), (4, 1))
+    xv.copy_(torch.from_numpy(x))
+    res = fn.normalize3(p, xv)
+    torch.cuda.synchronize()
+    bad, first = compare_chunked(_lib.OP_NORMALIZE, xv, res.length, res.unit, None, ka)
+    assert bad == 0, first
+    # RotationMatrix.apply over padded vectors
+    R = fn.rotation_unit((0.5, 0.5, 0.5, 0.5))
+    v = _random_rows(3001, 3, False, seed=5)
+    v[~np.isfinite(v)] = 1.0
+    got = R.apply(_padded(v, 4, cuda_dev))
+    want = R.apply(torch.from_numpy(v).to(cuda_dev))
+    torch.cuda.synchronize()
+    assert oracle.same(got.cpu().numpy(), want.cpu().numpy()).all()
+    # outputs overlapping the strided rows: gathered before the launch
+    x = _random_rows(4096, 3, False, seed=8)
+    rec = torch.zeros((4096, 4), dtype=torch.float64, device=cuda_dev)
+    rec[:, :3] = torch.from_numpy(x).to(cuda_dev)
+    u = rec.view(-1)[: 4096 * 3].view(4096, 3)
+    r = torch.empty(4096, dtype=torch.float64, device=cuda_dev)
+    fn.normalize3(p, rec[:, :3], out=(r, u))
+    torch.cuda.synchronize()
+    h, b, _ = oracle.run(_lib.OP_NORMALIZE, x, ka)
+    assert oracle.same(r.cpu().numpy(), h).all() and oracle.same(u.cpu().numpy(), b).all()
+
+
 def test_norm_equals_normalize_length(cuda_dev):
     for prec, dt in (("double", torch.float64), ("single", torch.float32)):
         p = fn.preset(prec)
