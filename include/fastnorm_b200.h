@@ -136,6 +136,14 @@ int fn_scalar(int op, int dim, int dtype, const double* x, double* out, const do
  * shard (no inter-device traffic; each device brings its own PCIe link). */
 int fn_host_run_multi(int op, int dim, int dtype, const void* x, int64_t n, void* head,
                       void* body, void* sq, const double* ka, const int* devices, int ndev);
+/* fn_host_run / fn_host_run_multi over host rows ldx elements apart (see fn_run_ld):
+ * each chunk's records cross PCIe as they are (no host-side gather) and the device
+ * kernel reads them with the same stride.  Outputs are dense host arrays. */
+int fn_host_run_ld(int op, int dim, int dtype, const void* x, int64_t n, int64_t ldx, void* head,
+                   void* body, void* sq, const double* ka);
+int fn_host_run_multi_ld(int op, int dim, int dtype, const void* x, int64_t n, int64_t ldx,
+                         void* head, void* body, void* sq, const double* ka, const int* devices,
+                         int ndev);
 /* fn_run for the rotation ops, with a device counter (uint64, accumulated; may be NULL)
  * of rows the reference would reject. */
 int fn_run_rot(int op, const double* q, int64_t n, double* head, double* body, double* extra,

@@ -278,7 +278,7 @@ def run(op: int, dim: int, x, ka_arr: np.ndarray | None, out=None, invalid=None)
                 _lib.check(rc, "fn_run")
             return BatchOut(head, body, extra)
         # CPU tensor: host path, results as CPU tensors sharing the numpy buffers
-        res = run(op, dim, x.contiguous().numpy(), ka_arr,
+        res = run(op, dim, x.numpy(), ka_arr,
                   None if out is None else tuple(o.numpy() for o in outs))
         conv = (lambda a: None if a is None else torch.from_numpy(a))
         return BatchOut(conv(res.head), conv(res.body), conv(res.sq))
@@ -288,8 +288,17 @@ def run(op: int, dim: int, x, ka_arr: np.ndarray | None, out=None, invalid=None)
     dcode = _dcode_of.get(x.dtype)
     if dcode is None:
         dcode = _dcode_of[x.dtype] = _dtype_code(str(x.dtype))
+    # Rows ldx elements apart (padded records, X[:, :dim] of a wider array) cross PCIe as
+    # they are (fn_host_run_ld); any other layout is gathered first.
+    ldx = dim
     if not x.flags.c_contiguous:
-        x = np.ascontiguousarray(x)
+        es = x.itemsize
+        st0, st1 = x.strides
+        rot = op in (_lib.OP_ROT_UNIT, _lib.OP_ROT_GENERAL, _lib.OP_NORMALIZE_ROT)
+        if not rot and n > 0 and st1 == es and st0 % es == 0 and st0 >= dim * es:
+            ldx = st0 // es
+        else:
+            x = np.ascontiguousarray(x)
 
     def alloc_np(o, w, what):
         if not w:
@@ -298,13 +307,18 @@ def run(op: int, dim: int, x, ka_arr: np.ndarray | None, out=None, invalid=None)
         return o if o is not None else np.empty(_shape(n, w), dtype=x.dtype)
 
     head, body, extra = alloc_np(o_head, w0, "head"), alloc_np(o_body, w1, "body"), alloc_np(o_extra, w2, "extra")
+    if ldx != dim and any(o is not None and np.may_share_memory(x, o) for o in (head, body, extra)):
+        x, ldx = np.ascontiguousarray(x), dim  # outputs written over strided input rows
     ptr = (lambda a: None if a is None else a.ctypes.data)
     devs = getattr(_host, "devices", None)
     if devs:
         darr = np.array(devs, dtype=np.int32)
-        rc = L.fn_host_run_multi(op, dim, dcode, x.ctypes.data, n, ptr(head), ptr(body), ptr(extra),
-                                 kptr, darr.ctypes.data, len(devs))
+        rc = L.fn_host_run_multi_ld(op, dim, dcode, x.ctypes.data, n, ldx, ptr(head), ptr(body), ptr(extra),
+                                    kptr, darr.ctypes.data, len(devs))
         _lib.check(rc, "fn_host_run_multi")
+    elif ldx != dim:
+        rc = L.fn_host_run_ld(op, dim, dcode, x.ctypes.data, n, ldx, ptr(head), ptr(body), ptr(extra), kptr)
+        _lib.check(rc, "fn_host_run")
     else:
         fast = _fast_run()
         if fast is not None:

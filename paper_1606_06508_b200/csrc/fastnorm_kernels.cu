@@ -727,7 +727,7 @@ struct SmallCtx {
 };
 
 static int host_run_small(int op, int dim, int dtype, const void* x, const void* x2, int dim2, int64_t n,
-                          void* head, void* body, void* sq, const double* ka, int dev) {
+                          void* head, void* body, void* sq, const double* ka, int dev, int64_t ldx) {
     static thread_local std::vector<SmallCtx> ctxs;
     if ((int)ctxs.size() <= dev) ctxs.resize(dev + 1);
     SmallCtx& c = ctxs[dev];
@@ -743,17 +743,17 @@ static int host_run_small(int op, int dim, int dtype, const void* x, const void*
     }
     const size_t w = dtype == FN_F64 ? 8 : 4;
     const Widths wd = op_widths(op, dim);
-    const size_t bx = align256(n * dim * w), bx2 = align256(n * dim2 * w), b0 = align256(n * wd.w0 * w),
+    const size_t bx = align256(n * ldx * w), bx2 = align256(n * dim2 * w), b0 = align256(n * wd.w0 * w),
                  b1 = align256(n * wd.w1 * w);
     const size_t off[5] = {0, bx, bx + bx2, bx + bx2 + b0, bx + bx2 + b0 + b1};
-    memcpy(c.host + off[0], x, n * dim * w);
+    memcpy(c.host + off[0], x, ((n - 1) * ldx + dim) * w);
     if (x2) memcpy(c.host + off[1], x2, n * dim2 * w);
     void* d0 = c.dptr + off[2];
     void* d1 = wd.w1 ? c.dptr + off[3] : nullptr;
     void* d2 = wd.w2 ? c.dptr + off[4] : nullptr;
     tl_direct = true;
     const int rc = x2 ? run_rows2(op, c.dptr + off[0], c.dptr + off[1], n, d0, ka, nullptr, c.stream)
-                      : run(op, dim, dtype, c.dptr + off[0], n, d0, d1, d2, ka, c.stream);
+                      : run_ex(op, dim, dtype, c.dptr + off[0], n, d0, d1, d2, ka, nullptr, c.stream, ldx);
     tl_direct = false;
     if (rc != FN_OK) return rc;
     e = cudaStreamSynchronize(c.stream);
@@ -764,19 +764,25 @@ static int host_run_small(int op, int dim, int dtype, const void* x, const void*
     return FN_OK;
 }
 
-// x2 / dim2: the second input of the two-input ops (NULL / 0 otherwise).
+// x2 / dim2: the second input of the two-input ops (NULL / 0 otherwise).  ldx: elements
+// from one row of x to the next (0 = dim); each chunk moves its rows' records as they are
+// ((m - 1) * ldx + dim elements, the last row's padding excluded) and the kernel reads
+// them with the same stride.
 static int host_run_impl(int op, int dim, int dtype, const void* x, const void* x2, int dim2, int64_t n,
-                         void* head, void* body, void* sq, const double* ka) {
+                         void* head, void* body, void* sq, const double* ka, int64_t ldx = 0) {
     int rc = x2 ? check_rows2(op, x, x2, n, head) : check_args(op, dim, dtype, x, n, head, body, sq);
     if (rc != FN_OK || n == 0) return rc;
+    if (ldx == 0) ldx = dim;
+    if (ldx < dim || (x2 && ldx != dim)) return fail(FN_EINVAL, "ldx (elements per input row) must be >= dim");
+    if (ldx > (INT64_MAX / 16 - dim) / n) return fail(FN_EINVAL, "n * ldx overflows");
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
     const size_t w = dtype == FN_F64 ? 8 : 4;
     const Widths wd = op_widths(op, dim);
-    if ((size_t)n * (dim + dim2 + wd.w0 + wd.w1 + wd.w2) * w + 8 * 256 <= kSmallHostBytes &&
+    if ((size_t)n * (ldx + dim2 + wd.w0 + wd.w1 + wd.w2) * w + 8 * 256 <= kSmallHostBytes &&
         env_int("FASTNORM_B200_HOST_SMALL", 1, 0, 1))  // FASTNORM_B200_HOST_SMALL=0: always stage
-        return host_run_small(op, dim, dtype, x, x2, dim2, n, head, body, sq, ka, dev);
+        return host_run_small(op, dim, dtype, x, x2, dim2, n, head, body, sq, ka, dev, ldx);
     // Pageable caller memory cannot be DMA'd asynchronously: such sides go through
     // page-locked staging filled / drained by the parallel host copier, overlapped with
     // the transfers and kernels of the other pipes.
@@ -790,7 +796,7 @@ static int host_run_impl(int op, int dim, int dtype, const void* x, const void* 
     //    for mid-size ones so transfers and kernels of different chunks overlap;
     //  * pageable callers: 8-16 MiB (each staging copy still gets the parallel copier).
     // FASTNORM_B200_HOST_CHUNK_MB fixes the chunk size instead.
-    const int64_t row_in = (int64_t)((dim + dim2) * w), in_total = n * row_in;
+    const int64_t row_in = (int64_t)((ldx + dim2) * w), in_total = n * row_in;
     int64_t chunk_bytes;
     if (getenv("FASTNORM_B200_HOST_CHUNK_MB")) {
         chunk_bytes = (int64_t)env_int("FASTNORM_B200_HOST_CHUNK_MB", 48, 1, 1024) << 20;
@@ -801,7 +807,7 @@ static int host_run_impl(int op, int dim, int dtype, const void* x, const void* 
     }
     const int64_t chunk_rows = std::max<int64_t>(4096, chunk_bytes / row_in);
     const int64_t rows = std::min<int64_t>(n, chunk_rows);
-    const size_t bx = align256(rows * dim * w), bx2 = align256(rows * dim2 * w),
+    const size_t bx = align256(rows * ldx * w), bx2 = align256(rows * dim2 * w),
                  b0 = align256(rows * wd.w0 * w), b1 = align256(rows * wd.w1 * w),
                  b2 = align256(rows * wd.w2 * w);
     const size_t per_pipe = bx + bx2 + b0 + b1 + b2;
@@ -845,12 +851,13 @@ static int host_run_impl(int op, int dim, int dtype, const void* x, const void* 
         char* hbase = static_cast<char*>(st->hbuf[p]);
         void* dx = base;
         void* dptr[3] = {base + offs[0], wd.w1 ? base + offs[1] : nullptr, wd.w2 ? base + offs[2] : nullptr};
-        const char* src = static_cast<const char*>(x) + r0 * dim * w;
+        const char* src = static_cast<const char*>(x) + r0 * ldx * w;
+        const size_t in_bytes = ((m - 1) * ldx + dim) * w;
         if (stage_in) {
-            copy_pool().copy(hbase, src, m * dim * w);
+            copy_pool().copy(hbase, src, in_bytes);
             src = hbase;
         }
-        e = cudaMemcpyAsync(dx, src, m * dim * w, cudaMemcpyHostToDevice, s);
+        e = cudaMemcpyAsync(dx, src, in_bytes, cudaMemcpyHostToDevice, s);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync H2D");
         if (x2) {
             void* dx2 = base + bx;
@@ -863,7 +870,7 @@ static int host_run_impl(int op, int dim, int dtype, const void* x, const void* 
             if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync H2D");
             rc = run_rows2(op, dx, dx2, m, dptr[0], ka, nullptr, s);
         } else {
-            rc = run(op, dim, dtype, dx, m, dptr[0], dptr[1], dptr[2], ka, s);
+            rc = run_ex(op, dim, dtype, dx, m, dptr[0], dptr[1], dptr[2], ka, nullptr, s, ldx);
         }
         if (rc != FN_OK) return rc;
         for (int k = 0; k < 3 && e == cudaSuccess; ++k) {
@@ -888,8 +895,8 @@ static int host_run_impl(int op, int dim, int dtype, const void* x, const void* 
 }
 
 int host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* body,
-             void* sq, const double* ka) {
-    return host_run_impl(op, dim, dtype, x, nullptr, 0, n, head, body, sq, ka);
+             void* sq, const double* ka, int64_t ldx = 0) {
+    return host_run_impl(op, dim, dtype, x, nullptr, 0, n, head, body, sq, ka, ldx);
 }
 
 // ---------------------------------------------------------------------------------
@@ -1042,10 +1049,12 @@ int scalar_run(int op, int dim, int dtype, const double* xin, double* out, const
 // chunked host pipeline above on its own streams and staging buffers.  No data moves
 // between devices (rows are independent, _kernels.pyx:167-412).
 int host_run_multi(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* body,
-                   void* sq, const double* ka, const int* devices, int ndev) {
+                   void* sq, const double* ka, const int* devices, int ndev, int64_t ldx = 0) {
     if (ndev < 1 || !devices) return fail(FN_EINVAL, "need at least one device");
     int rc = check_args(op, dim, dtype, x, n, head, body, sq);
     if (rc != FN_OK || n == 0) return rc;
+    if (ldx == 0) ldx = dim;
+    if (ldx < dim) return fail(FN_EINVAL, "ldx (elements per input row) must be >= dim");
     int count = 0;
     cudaError_t e = cudaGetDeviceCount(&count);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
@@ -1067,10 +1076,10 @@ int host_run_multi(int op, int dim, int dtype, const void* x, int64_t n, void* h
             if (ee != cudaSuccess) {
                 rcs[k] = cuda_fail(ee, "cudaSetDevice");
             } else if (m > 0) {
-                rcs[k] = host_run(op, dim, dtype, static_cast<const char*>(x) + r0 * dim * w, m,
+                rcs[k] = host_run(op, dim, dtype, static_cast<const char*>(x) + r0 * ldx * w, m,
                                   static_cast<char*>(head) + r0 * wd.w0 * w,
                                   wd.w1 ? static_cast<char*>(body) + r0 * wd.w1 * w : nullptr,
-                                  wd.w2 ? static_cast<char*>(sq) + r0 * wd.w2 * w : nullptr, ka);
+                                  wd.w2 ? static_cast<char*>(sq) + r0 * wd.w2 * w : nullptr, ka, ldx);
             }
             if (rcs[k] != FN_OK) errs[k] = g_last_error;
         });
@@ -1146,6 +1155,18 @@ int fn_scalar(int op, int dim, int dtype, const double* x, double* out, const do
 int fn_host_run_multi(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* body,
                       void* sq, const double* ka, const int* devices, int ndev) {
     return fnb::host_run_multi(op, dim, dtype, x, n, head, body, sq, ka, devices, ndev);
+}
+
+int fn_host_run_ld(int op, int dim, int dtype, const void* x, int64_t n, int64_t ldx, void* head, void* body,
+                   void* sq, const double* ka) {
+    if (ldx < 1) return fnb::set_error(FN_EINVAL, "ldx must be >= dim");
+    return fnb::host_run(op, dim, dtype, x, n, head, body, sq, ka, ldx);
+}
+
+int fn_host_run_multi_ld(int op, int dim, int dtype, const void* x, int64_t n, int64_t ldx, void* head,
+                         void* body, void* sq, const double* ka, const int* devices, int ndev) {
+    if (ldx < 1) return fnb::set_error(FN_EINVAL, "ldx must be >= dim");
+    return fnb::host_run_multi(op, dim, dtype, x, n, head, body, sq, ka, devices, ndev, ldx);
 }
 
 int fn_run_soa(int op, int dim, int dtype, const void* const* xs, int64_t n, void* head,

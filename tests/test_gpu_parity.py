@@ -243,6 +243,43 @@ def test_strided_rows_other_layouts(cuda_dev):
     assert oracle.same(r.cpu().numpy(), h).all() and oracle.same(u.cpu().numpy(), b).all()
 
 
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("n", [1, 300, 4099, 3_000_001])
+@pytest.mark.parametrize("pinned", [False, True])
+def test_host_padded_records(cuda_dev, prec, n, pinned):
+    """Host (numpy) xyz-of-xyzw rows through fn_host_run_ld: records cross PCIe as they
+    are (small zero-copy path, staged pipeline, page-locked caller buffers), every
+    family bit for bit against the oracle; 3e6 rows span several pipeline chunks."""
+    single = prec == "f32"
+    x = _random_rows(n, 3, single, seed=n * 3 + single)
+    rec = fn.host_empty((n, 4), dtype=x.dtype) if pinned else np.empty((n, 4), dtype=x.dtype)
+    rec[:, 3] = np.nan
+    rec[:, :3] = x
+    xv = rec[:, :3]
+    ka = np.array(fn.kernel_args(fn.preset(PREC[prec])))
+    for fam in FAMILIES[3] + ["normalize_sq"]:
+        base = "normalize3_sq" if fam == "normalize_sq" else _base(fam, 3)
+        op = _lib.OP_NORMALIZE_SQ if fam == "normalize_sq" else OPS[fam]
+        takes = fam in SCALING or fam == "normalize_sq"
+        res = _cuda_kernels.batch_kernel(base, prec)(xv, ka if takes else None)
+        h, b, q = oracle.run(op, x, ka if takes else None, threads=8)
+        assert oracle.same(res.head, h).all(), (fam, prec, n)
+        if b is not None:
+            assert oracle.same(res.body, b).all(), (fam, prec, n)
+        if q is not None:
+            assert oracle.same(res.sq, q).all(), (fam, prec, n)
+    # other strides and a CPU tensor view
+    x2 = _random_rows(5000, 2, False, seed=4)
+    r5 = np.zeros((5000, 5))
+    r5[:, 1:3] = x2
+    got = fn.normalize2(fn.preset("double"), r5[:, 1:3])
+    h, b, _ = oracle.run(_lib.OP_NORMALIZE, x2, np.array(fn.kernel_args(fn.preset("double"))))
+    assert oracle.same(got.length, h).all() and oracle.same(got.unit, b).all()
+    t = torch.from_numpy(r5)[:, 1:3]
+    got = fn.normalize2(fn.preset("double"), t)
+    assert oracle.same(got.length.numpy(), h).all() and oracle.same(got.unit.numpy(), b).all()
+
+
 def test_norm_equals_normalize_length(cuda_dev):
     for prec, dt in (("double", torch.float64), ("single", torch.float32)):
         p = fn.preset(prec)
