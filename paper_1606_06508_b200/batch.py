@@ -375,6 +375,30 @@ def is_soa(xs, dim: int) -> bool:
     return len(xs) == dim and all(is_array(v) and v.ndim == 1 for v in xs)
 
 
+def _columns_of_records(xs, dim: int):
+    """If the component arrays are consecutive columns of one array of records (same
+    dtype and home, one common row stride >= dim elements, column k starting k elements
+    after column 0), return that [N, dim] strided view of the records, else None."""
+    x0 = xs[0]
+    if is_torch(x0):
+        if not all(is_torch(v) and v.dim() == 1 and v.dtype == x0.dtype and v.device == x0.device for v in xs):
+            return None
+        es, st = x0.element_size(), x0.stride(0)
+        if len(x0) < 2 or st < dim or any(v.stride(0) != st for v in xs):
+            return None
+        if any(v.data_ptr() != x0.data_ptr() + k * es for k, v in enumerate(xs)):
+            return None
+        return x0.as_strided((len(x0), dim), (st, 1))
+    if not all(isinstance(v, np.ndarray) and v.ndim == 1 and v.dtype == x0.dtype for v in xs):
+        return None
+    es, st = x0.itemsize, x0.strides[0]
+    if len(x0) < 2 or st % es or st < dim * es or any(v.strides[0] != st for v in xs):
+        return None
+    if any(v.ctypes.data != x0.ctypes.data + k * es for k, v in enumerate(xs)):
+        return None
+    return np.lib.stride_tricks.as_strided(x0, shape=(len(x0), dim), strides=(st, es), writeable=False)
+
+
 def run_soa(op: int, dim: int, xs, ka_arr: np.ndarray | None):
     """Structure-of-arrays rows: component arrays xs[k][N] -> (head[N], body tuple of
     dim arrays or None, extra[N] or None), through fn_run_soa on the device.
@@ -384,10 +408,17 @@ def run_soa(op: int, dim: int, xs, ka_arr: np.ndarray | None):
     arithmetic runs in the kernel."""
     import ctypes
 
-    torch = _torch()
     n = int(xs[0].shape[0])
     if any(int(v.shape[0]) != n for v in xs):
         raise ValueError("component arrays must have the same length")
+    aos = _columns_of_records(xs, dim)
+    if aos is not None:
+        # the components are the columns of one record array (X[:, 0], X[:, 1], ...):
+        # run the AoS kernels on the records in place, return column views
+        res = run(op, dim, aos, ka_arr)
+        body = None if res.body is None else tuple(res.body[:, k] for k in range(dim))
+        return res.head, body, res.sq
+    torch = _torch()
     host = not (is_torch(xs[0]) and xs[0].is_cuda)
     if host:
         dev = torch.device("cuda", torch.cuda.current_device())

@@ -370,6 +370,14 @@ def test_host_run_multi_device_sharding(cuda_dev):
     assert oracle.same(got.length, ref.length).all() and oracle.same(got.unit, ref.unit).all()
     qr = fn.quotient2(x[:, :2].copy())
     assert oracle.same(q.unit, qr.unit).all()
+    # strided rows (fn_host_run_multi_ld): xyz of xyzw records and a view of a wider array
+    rec = np.full((x.shape[0], 4), np.nan)
+    rec[:, :3] = x
+    with host_devices([0, 0, 0]):
+        got = fn.normalize3(p, rec[:, :3])
+        q = fn.quotient2(x[:, :2])
+    assert oracle.same(got.length, ref.length).all() and oracle.same(got.unit, ref.unit).all()
+    assert oracle.same(q.unit, qr.unit).all()
 
 
 @pytest.mark.parametrize("x_pinned,out_pinned", [(False, False), (True, False), (False, True), (True, True)])
@@ -698,6 +706,29 @@ def test_structure_of_arrays_calls(cuda_dev, home):
                 soa, aos = f(*comps), f(xd)
                 assert same(soa.length, aos.length), f.__name__
                 assert all(same(soa.unit[k], aos.unit[:, k]) for k in range(dim)), f.__name__
+
+
+@pytest.mark.parametrize("home", ["device", "host"])
+def test_structure_of_arrays_columns_of_records(cuda_dev, home):
+    """Component arrays that are the columns of one record array (X[:, 0], X[:, 1], ...,
+    dense or padded records) run the AoS kernels on the records in place; the results
+    equal the AoS call bit for bit.  Columns out of order take the SoA kernels."""
+    for prec, single in (("double", False), ("single", True)):
+        p = fn.preset(prec)
+        for dim, width in ((3, 3), (3, 4), (2, 2), (4, 4), (2, 5)):
+            x = _random_rows(70_001, dim, single, seed=dim * 31 + width)
+            rec = np.full((x.shape[0], width), np.nan, dtype=x.dtype)
+            rec[:, :dim] = x
+            if home == "device":
+                rec = torch.from_numpy(rec).to(cuda_dev)
+            comps = [rec[:, k] for k in range(dim)]
+            as_np = (lambda t: t.cpu().numpy() if hasattr(t, "cpu") else np.asarray(t))  # noqa: E731
+            for order in (list(range(dim)), list(range(dim))[::-1]):
+                want = getattr(fn, f"normalize{dim}")(p, torch.from_numpy(np.ascontiguousarray(x[:, order])).to(cuda_dev))
+                got = getattr(fn, f"normalize{dim}")(p, *[comps[k] for k in order])
+                assert oracle.same(as_np(got.length), as_np(want.length)).all(), (prec, dim, width, order)
+                for j in range(dim):
+                    assert oracle.same(as_np(got.unit[j]), as_np(want.unit[:, j])).all(), (prec, dim, width, order)
 
 
 def test_structure_of_arrays_unaligned_and_tails(cuda_dev):
