@@ -9,6 +9,10 @@ Accepts ``[N, n]`` row arrays in either of two homes:
   out (``fn_host_run``: chunked H2D / kernel / D2H pipeline).  Page-locked (pinned)
   host memory gives full PCIe bandwidth.
 
+Rows need not be dense: a view whose rows are ``ldx`` elements apart with unit column
+stride (xyz of xyzw records, ``X[:, :n]`` of a wider array) runs as it is
+(``fn_run_ld`` / ``fn_host_run_ld``); other layouts are gathered first.
+
 No path computes on the CPU: without the CUDA library every call raises.
 """
 
@@ -21,6 +25,7 @@ from typing import Any, NamedTuple
 import numpy as np
 
 from paper_1606_06508_b200 import _lib
+
 
 def widths(op: int, dim: int) -> tuple[int, int, int]:
     """Elements per row of the (head, body, extra) outputs of a kernel family."""
