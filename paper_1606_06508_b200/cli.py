@@ -228,6 +228,47 @@ def cmd_selftest(a) -> int:
     return 0 if not any(res.values()) else 1
 
 
+def _same_bits(a, b):
+    """The reference's comparison rule (tests/test_backends.py:33-38): NaN matches NaN,
+    everything else must be bit-equal, zero signs included."""
+    import numpy as np
+
+    a, b = np.asarray(a), np.asarray(b)
+    both_nan = np.isnan(a) & np.isnan(b)
+    return both_nan | (a.view(np.uint8).reshape(a.shape + (-1,)) ==
+                       b.view(np.uint8).reshape(b.shape + (-1,))).all(axis=-1)
+
+
+def cmd_compare(a) -> int:
+    """Compare two result files (.npz of named arrays, e.g. this build's `batch` output
+    against one produced by the reference) array by array and row by row; print the
+    mismatch count per array and the first mismatching rows in hex floats."""
+    import numpy as np
+
+    fa, fb = np.load(a.a), np.load(a.b)
+    names = [k for k in fa.files if k in fb.files] if not a.arrays else a.arrays
+    if not names:
+        raise SystemExit("no array names in common")
+    report, worst = {}, 0
+    single = None
+    for k in names:
+        x, y = fa[k], fb[k]
+        if x.shape != y.shape or x.dtype != y.dtype:
+            raise SystemExit(f"{k}: {x.shape} {x.dtype} vs {y.shape} {y.dtype}")
+        single = x.dtype == np.float32
+        ok = _same_bits(x, y)
+        rows_ok = ok.reshape(ok.shape[0], -1).all(axis=1) if ok.ndim > 1 else ok
+        bad = np.flatnonzero(~rows_ok)
+        worst = max(worst, len(bad))
+        report[k] = {"rows": int(rows_ok.shape[0]), "mismatching_rows": int(len(bad)),
+                     "first": [{"row": int(i),
+                                "a": [_fmt(float(v), True, single) for v in np.ravel(x[i])],
+                                "b": [_fmt(float(v), True, single) for v in np.ravel(y[i])]}
+                               for i in bad[: a.show]]}
+    print(json.dumps(report))
+    return 0 if worst == 0 else 1
+
+
 def build_parser() -> argparse.ArgumentParser:
     ap = argparse.ArgumentParser(prog="python -m paper_1606_06508_b200", description=__doc__,
                                  formatter_class=argparse.RawDescriptionHelpFormatter)
@@ -270,6 +311,14 @@ def build_parser() -> argparse.ArgumentParser:
     s.add_argument("--in", dest="inp", required=True)
     s.add_argument("--out", required=True)
     s.set_defaults(fn=cmd_batch)
+
+    s = sub.add_parser("compare", help="bit-compare two result .npz files (NaN == NaN); "
+                                       "report mismatching rows in hex floats")
+    s.add_argument("a")
+    s.add_argument("b")
+    s.add_argument("--array", dest="arrays", action="append", help="array name (default: all shared)")
+    s.add_argument("--show", type=int, default=5, help="mismatching rows to print per array")
+    s.set_defaults(fn=cmd_compare)
 
     s = sub.add_parser("bench", help="time a kernel family on a BASELINE config in HBM")
     s.add_argument("--config", type=int, choices=(1, 2, 3, 4, 5), default=1)

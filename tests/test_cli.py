@@ -38,6 +38,27 @@ def test_parser_rejects_bad_args():
         cli.main(["rotate", "1", "2", "3"])
 
 
+def test_compare(capsys, tmp_path):
+    """compare: the reference's _same rule (NaN == NaN, zero signs count), per-array row
+    counts and hex-float reports of the first mismatches."""
+    u = np.array([[0.6, 0.8, 0.0], [np.nan, np.nan, np.nan], [1.0, -0.0, 0.0]])
+    r = np.array([5.0, np.nan, 3.0])
+    np.savez(tmp_path / "a.npz", length=r, unit=u)
+    np.savez(tmp_path / "b.npz", length=r.copy(), unit=u.copy())
+    assert cli.main(["compare", str(tmp_path / "a.npz"), str(tmp_path / "b.npz")]) == 0
+    out = json.loads(capsys.readouterr().out)
+    assert out["unit"]["mismatching_rows"] == 0 and out["length"]["rows"] == 3
+    u2 = u.copy()
+    u2[2, 1] = 0.0  # -0.0 -> +0.0 is a mismatch
+    u2[0, 0] = np.nextafter(0.6, 1.0)
+    np.savez(tmp_path / "c.npz", length=r, unit=u2)
+    assert cli.main(["compare", str(tmp_path / "a.npz"), str(tmp_path / "c.npz"), "--array", "unit"]) == 1
+    out = json.loads(capsys.readouterr().out)
+    assert out["unit"]["mismatching_rows"] == 2 and list(out) == ["unit"]
+    first = out["unit"]["first"][0]
+    assert first["row"] == 0 and first["a"][0] == (0.6).hex() and first["b"][0] == np.nextafter(0.6, 1.0).hex()
+
+
 @pytest.mark.gpu
 def test_gpu_subcommands(capsys, tmp_path, cuda_dev):
     assert cli.main(["normalize", "--dim", "3", "3", "4", "12"]) == 0
