@@ -24,12 +24,18 @@ def main():
     ap.add_argument("--op", default="normalize",
                     choices=["normalize", "normalize_sq", "norm", "quotient", "quotient3_fast", "naive", "scale",
                              "normalize4_rotation"])
+    ap.add_argument("--padded", action="store_true",
+                    help="rows as xyz of xyzw records (3-D configs; fn_run_ld with ldx 4)")
     a = ap.parse_args()
     c = workloads.CONFIGS[a.cfg]
     dt = torch.float64 if c.dtype == "float64" else torch.float32
     n = 1 << a.log2_rows
     x = torch.empty((n, c.dim), dtype=dt, device="cuda")
     workloads.generate_device(a.cfg, x)
+    if a.padded:
+        rec = torch.zeros((n, c.dim + 1), dtype=dt, device="cuda")
+        rec[:, :c.dim] = x
+        x = rec[:, :c.dim]
     p = fn.preset("double" if dt == torch.float64 else "single")
     d = c.dim
     for _ in range(a.iters):
