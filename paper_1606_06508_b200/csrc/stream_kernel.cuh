@@ -345,6 +345,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     while (!mbar_try_wait(bar, parity)) {
     }
 }
+// Plain arrive (release at CTA scope): one count of the barrier's current phase.
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
 // global -> shared bulk copy, completion counted on the mbarrier; streaming input is
 // read exactly once, so it is marked evict-first in L2.
 __device__ __forceinline__ void bulk_load(void* dst_smem, const void* src_gmem, uint32_t bytes,
@@ -502,19 +506,31 @@ template <typename T, int N> struct OpRows<T, N, FN_OP_NORMALIZE_ROT> {
 // HINTS: bit 0 -> input loads carry an L2 evict-first policy (read once);
 //        bit 1 -> output bulk stores carry an L2 evict-first policy.
 // Per-CTA timeline (developer probe tools/probe/cfg1_timeline.cu only; compiled out of
-// the library): thread 0 of each CTA stores %globaltimer at five points of the kernel
-// into fnb_timeline[blockIdx.x * 5 + slot].
+// the library): thread 0 of each CTA stores %globaltimer into
+// fnb_timeline[blockIdx.x * kTimelineSlots + slot]: slots 0-4 at five points of the
+// kernel, and for its first kTimelineTiles tiles three per tile (data landed, tile
+// computed and staged, previous store group read out).
 #ifdef FNB_TIMELINE
+constexpr int kTimelineSlots = 64, kTimelineTiles = 19;
 __device__ unsigned long long* fnb_timeline;
+__device__ int fnb_timeline_tiles;  // per-tile marks on (they perturb the timing)
 __device__ __forceinline__ void timeline_mark(int slot) {
     if (threadIdx.x == 0 && fnb_timeline != nullptr) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        fnb_timeline[blockIdx.x * 5 + slot] = t;
+        fnb_timeline[blockIdx.x * kTimelineSlots + slot] = t;
+    }
+}
+__device__ __forceinline__ void timeline_tile(int64_t k, int phase, bool me = true) {
+    if (me && k < kTimelineTiles && fnb_timeline != nullptr && fnb_timeline_tiles) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        fnb_timeline[blockIdx.x * kTimelineSlots + 5 + 3 * (int)k + phase] = t;
     }
 }
 #else
 __device__ __forceinline__ void timeline_mark(int) {}
+__device__ __forceinline__ void timeline_tile(int64_t, int, bool = true) {}
 #endif
 
 template <typename T, int N, int OP, int TR_ = OpRows<T, N, OP>::value, int S_ = OpStages<T, N, OP>::value,
@@ -576,6 +592,7 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
         const int64_t tile = (int64_t)blockIdx.x + k * gridDim.x;
         mbar_wait(&full[s], parity);
         if (k == 0) timeline_mark(2);
+        timeline_tile(k, 0, threadIdx.x == 0);
 
         const T* tin = reinterpret_cast<const T*>(s_in + s * L::kInBytes);
         const T* tin2 = reinterpret_cast<const T*>(s_in2 + s * L::kIn2Bytes);
@@ -605,6 +622,7 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
         }
         fence_proxy_async_smem();  // generic-proxy smem traffic -> visible to bulk copies
         __syncthreads();
+        timeline_tile(k, 1, threadIdx.x == 0);
         if (leader) {
             const int64_t row0 = tile * TR;
             if (HINTS & 2) {
@@ -621,6 +639,7 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
             // Threads write staging tile (k+2) % OB after the next __syncthreads, so group
             // k+2-OB must have been read out by then: at most OB-2 groups stay pending.
             bulk_wait_read<OB - 2>();
+            timeline_tile(k, 2, true);
         }
     }
 

@@ -15,7 +15,7 @@
 #include <string>
 #include <vector>
 
-#include "../paper_1606_06508_b200/csrc/stream_kernel.cuh"
+#include "ws_kernel.cuh"
 
 extern "C" int fn_generate(int cfg, uint64_t seed, int64_t row0, int64_t n, void* x, void* stream);
 
@@ -121,6 +121,38 @@ float time_variant(const Bufs& b, int cps, int reps, int sms, int* occ_out) {
     return ms / reps;
 }
 
+// The warp-specialised kernel (NT compute threads + a producer warp); H is unused.
+template <typename T, int N, int OP, int TR, int S, int NT, int H>
+float time_variant_ws(const Bufs& b, int cps, int reps, int sms, int* occ_out) {
+    using L = TileLayout<T, N, OP, TR, S>;
+    auto kern = tma_ws_kernel<T, N, OP, TR, S, NT>;
+    const int smem = L::kSmemBytes + (S + 2 * L::OB) * 8;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT + 32, smem));
+    *occ_out = occ;
+    const int per = cps > 0 ? std::min(cps, occ) : occ;
+    const int64_t ntiles = b.n / TR;
+    const int grid = (int)std::min<int64_t>((int64_t)per * sms, ntiles);
+    const KArgs<T> ka = make_ka<T>();
+    const T* x = (const T*)b.x;
+    T *h = (T*)b.h, *bd = (T*)b.b, *q = (T*)b.q;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    for (int i = 0; i < 2; ++i) kern<<<grid, NT + 32, smem>>>(x, (const T*)b.b, b.n, h, bd, q, ka);
+    CK(cudaEventRecord(e0));
+    for (int i = 0; i < reps; ++i) kern<<<grid, NT + 32, smem>>>(x, (const T*)b.b, b.n, h, bd, q, ka);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    CK(cudaGetLastError());
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    CK(cudaEventDestroy(e0));
+    CK(cudaEventDestroy(e1));
+    return ms / reps;
+}
+
 struct Variant {
     std::string fam;
     int cfg, tr, s, nt, h, cps, bytes_per_row;
@@ -138,6 +170,10 @@ constexpr int row_bytes() {
 #define V(FAM, CFG, T, N, OP, TR, S, NT, H, CPS)                                         \
     Variant{FAM, CFG, TR, S, NT, H, CPS, row_bytes<T, N, OP>(),                          \
             &time_variant<T, N, OP, TR, S, NT, H>, {}, 0}
+// warp-specialised kernel (family name gets a _ws suffix)
+#define VW(FAM, CFG, T, N, OP, TR, S, NT, CPS)                                           \
+    Variant{FAM "_ws", CFG, TR, S, NT, 0, CPS, row_bytes<T, N, OP>(),                    \
+            &time_variant_ws<T, N, OP, TR, S, NT, 0>, {}, 0}
 // same with OB output staging tiles (reported in the HINTS column as 10*OB + HINTS)
 #define VO(FAM, CFG, T, N, OP, TR, S, NT, H, CPS, OB)                                    \
     Variant{FAM, CFG, TR, S, NT, 10 * OB + H, CPS, row_bytes<T, N, OP>(),                \
@@ -296,6 +332,25 @@ int main(int argc, char** argv) {
         vs.push_back(V("normalize3_f32", 4, float, 3, FN_OP_NORMALIZE, 1024, 4, 256, 0, 2));
         vs.push_back(V("normalize3_f32", 4, float, 3, FN_OP_NORMALIZE, 1024, 2, 256, 0, 2));
         vs.push_back(V("quotient3_f32", 4, float, 3, FN_OP_QUOTIENT, 512, 4, 256, 0, 2));
+    }
+    if (which == "all" || which == "ws") {
+        vs.push_back(V("normalize3_f64", 5, double, 3, FN_OP_NORMALIZE, 256, 4, 256, 0, 2));
+        vs.push_back(VW("normalize3_f64", 5, double, 3, FN_OP_NORMALIZE, 256, 4, 256, 2));
+        vs.push_back(VW("normalize3_f64", 5, double, 3, FN_OP_NORMALIZE, 256, 3, 256, 2));
+        vs.push_back(VW("normalize3_f64", 5, double, 3, FN_OP_NORMALIZE, 256, 4, 128, 2));
+        vs.push_back(VW("normalize3_f64", 5, double, 3, FN_OP_NORMALIZE, 256, 4, 256, 3));
+        vs.push_back(V("normalize2_f64", 2, double, 2, FN_OP_NORMALIZE, 512, 4, 256, 0, 2));
+        vs.push_back(VW("normalize2_f64", 2, double, 2, FN_OP_NORMALIZE, 512, 4, 256, 2));
+        vs.push_back(V("normalize4_sq_f64", 3, double, 4, FN_OP_NORMALIZE_SQ, 256, 3, 256, 0, 2));
+        vs.push_back(VW("normalize4_sq_f64", 3, double, 4, FN_OP_NORMALIZE_SQ, 256, 3, 256, 2));
+        vs.push_back(V("normalize3_f32", 4, float, 3, FN_OP_NORMALIZE, 512, 4, 256, 0, 2));
+        vs.push_back(VW("normalize3_f32", 4, float, 3, FN_OP_NORMALIZE, 512, 4, 256, 2));
+        vs.push_back(V("norm3_f64", 5, double, 3, FN_OP_NORM, 256, 4, 256, 0, 4));
+        vs.push_back(VW("norm3_f64", 5, double, 3, FN_OP_NORM, 256, 4, 256, 4));
+        vs.push_back(V("quotient3_f64", 5, double, 3, FN_OP_QUOTIENT, 256, 4, 256, 0, 8));
+        vs.push_back(VW("quotient3_f64", 5, double, 3, FN_OP_QUOTIENT, 256, 4, 256, 8));
+        vs.push_back(V("normalize4_rot_f64", 3, double, 4, FN_OP_NORMALIZE_ROT, 128, 3, 256, 0, 2));
+        vs.push_back(VW("normalize4_rot_f64", 3, double, 4, FN_OP_NORMALIZE_ROT, 128, 3, 256, 2));
     }
     // generate the input each variant family needs (configs 2..5) once per group
     int cur_cfg = -1;
