@@ -217,7 +217,8 @@ static int launch(const void* xv, const void* x2v, int64_t n, void* hv, void* bv
     constexpr int kPad = PaddedLdx<N>::value;
     if (aligned && !force_direct() && ldx == N && n >= (int64_t)L::TR) {
         e = launch_tma<T, N, OP>(x, x2, n, head, body, extra, ka, dev, sms, stream);
-    } else if (kPad > 0 && aligned && !force_direct() && ldx == kPad && n > (int64_t)L::TR) {
+    } else if (kPad > 0 && N2 == 0 && aligned && !force_direct() && ldx == kPad && n > (int64_t)L::TR) {
+        // (the branch is only reachable when the instantiation below exists)
         if constexpr (kPad > 0 && N2 == 0) e = launch_tma<T, N, OP, kPad>(x, x2, n, head, body, extra, ka, dev, sms, stream);
     } else {
         const int64_t want = (n + 255) / 256;
