@@ -41,6 +41,29 @@ int main(int argc, char** argv) {
             fprintf(stderr, "row %lld: unexpected length %.17g\n", (long long)i, r[i]);
             return 3;
         }
+    /* the same rows as xyz of xyzw records (padding never read): fn_host_run_ld, ldx 4 */
+    double* x4 = malloc(sizeof(double) * 4 * n);
+    double* r4 = malloc(sizeof(double) * n);
+    double* u4 = malloc(sizeof(double) * 3 * n);
+    if (!x4 || !r4 || !u4) return 1;
+    for (int64_t i = 0; i < n; ++i) {
+        for (int c = 0; c < 3; ++c) x4[4 * i + c] = x[3 * i + c];
+        x4[4 * i + 3] = NAN;
+    }
+    rc = fn_host_run_ld(FN_OP_NORMALIZE, 3, FN_F64, x4, n, 4, r4, u4, NULL, ka);
+    if (rc != FN_OK) {
+        fprintf(stderr, "fn_host_run_ld failed (%d): %s\n", rc, fn_last_error());
+        return 2;
+    }
+    for (int64_t i = 0; i < n; ++i)
+        if (r4[i] != r[i] || u4[3 * i] != u[3 * i] || u4[3 * i + 1] != u[3 * i + 1] || u4[3 * i + 2] != u[3 * i + 2]) {
+            fprintf(stderr, "row %lld: padded records differ from dense rows\n", (long long)i);
+            return 5;
+        }
+    printf("xyz of xyzw records: %lld rows identical to the dense call\n", (long long)n);
+    free(x4);
+    free(r4);
+    free(u4);
     /* argument errors come back as FN_EINVAL with a message */
     rc = fn_host_run(FN_OP_QUOTIENT3_FAST, 2, FN_F64, x, n, r, u, NULL, NULL);
     printf("quotient3_fast with dim 2 -> %d (%s)\n", rc, fn_last_error());
