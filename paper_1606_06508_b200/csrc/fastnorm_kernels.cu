@@ -212,8 +212,12 @@ static int launch(const void* xv, const void* x2v, int64_t n, void* hv, void* bv
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
     const int sms = device_sms(dev);
-    const bool aligned = aligned16(x) && (N2 == 0 || aligned16(x2)) && aligned16(head) &&
-                         (Op::W1 == 0 || aligned16(body)) && (Op::W2 == 0 || aligned16(extra));
+    // The bulk-copy kernel needs 16-byte aligned outputs (and inputs for the two-input
+    // ops); single-input rows only need element alignment: a misaligned x is loaded from
+    // the 16-byte boundary below each tile (tma_stream_kernel).
+    const bool x_ok = N2 == 0 ? ((uintptr_t)x % sizeof(T)) == 0 : (aligned16(x) && aligned16(x2));
+    const bool aligned = x_ok && aligned16(head) && (Op::W1 == 0 || aligned16(body)) &&
+                         (Op::W2 == 0 || aligned16(extra));
     constexpr int kPad = PaddedLdx<N>::value;
     if (aligned && !force_direct() && ldx == N && n >= (int64_t)L::TR) {
         e = launch_tma<T, N, OP>(x, x2, n, head, body, extra, ka, dev, sms, stream);

@@ -447,12 +447,15 @@ template <typename T, int N, int OP, int TR_, int S_, int OB_ = OutTiles<OP>::va
     static_assert(OB >= 3, "the store pipeline keeps OB - 2 groups reading behind the current one");
     static_assert(LDX >= N, "an input record holds at least the N components");
     static constexpr int kInBytes = TR * LDX * (int)sizeof(T);
+    // a stage holds one tile of records plus 16 bytes: rows whose storage is not 16-byte
+    // aligned are loaded from the aligned address below them (see tma_stream_kernel)
+    static constexpr int kStageBytes = kInBytes + 16;
     static constexpr int kIn2Bytes = TR * InWidth2<Op>::value * (int)sizeof(T);  // second input
     static constexpr int kB0 = TR * Op::W0 * (int)sizeof(T);
     static constexpr int kB1 = TR * Op::W1 * (int)sizeof(T);
     static constexpr int kB2 = TR * Op::W2 * (int)sizeof(T);
     static constexpr int kOutBytes = kB0 + kB1 + kB2;
-    static constexpr int kSmemBytes = S * (kInBytes + kIn2Bytes) + OB * kOutBytes + S * 8;
+    static constexpr int kSmemBytes = S * (kStageBytes + kIn2Bytes) + OB * kOutBytes + S * 8;
     static_assert(kInBytes % 16 == 0 && kIn2Bytes % 16 == 0 && kB0 % 16 == 0 && kB1 % 16 == 0 &&
                       kB2 % 16 == 0,
                   "bulk copies need 16 B multiples");
@@ -547,14 +550,24 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
     constexpr int N2 = InWidth2<Op>::value;
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned char* s_in = smem;
-    unsigned char* s_in2 = smem + S * L::kInBytes;  // second input ring (two-input ops)
+    unsigned char* s_in2 = smem + S * L::kStageBytes;  // second input ring (two-input ops)
     unsigned char* s_out = s_in2 + S * L::kIn2Bytes;
     uint64_t* full = reinterpret_cast<uint64_t*>(s_out + OB * L::kOutBytes);
     timeline_mark(0);
 
-    // Padded records: the last row may end at its N-th element (a strided view of a
-    // shorter allocation), so it never rides in a bulk tile that would read its padding.
-    const int64_t ntiles = (LDX == N ? nrows : nrows - 1) / TR;
+    // Rows whose storage is not 16-byte aligned (x[1:] of a dense array; the outputs and
+    // a second input must be aligned, the host checks): every stage is loaded from the
+    // 16-byte boundary `mis` bytes below its first row, 16 bytes longer, and read at
+    // offset `mis`.  Bulk tiles only cover bytes inside [boundary below x, last row's
+    // end]; the reach below x stays inside x's 16-byte block, hence inside its
+    // allocation.  Padded records: the last row may end at its N-th element (a strided
+    // view of a shorter allocation), so no tile reads past that element either.
+    const int mis = (int)(reinterpret_cast<uintptr_t>(x) & 15);
+    const int64_t avail = ((nrows - 1) * LDX + N) * (int64_t)sizeof(T);  // bytes from x to the last row's end
+    const int64_t reach = mis ? 16 - mis : 0;                               // bytes a load reads past its tile
+    const int64_t ntiles = avail >= reach ? (avail - reach) / L::kInBytes : 0;
+    const unsigned char* xa = reinterpret_cast<const unsigned char*>(x) - mis;
+    const uint32_t load_bytes = L::kInBytes + (mis ? 16 : 0);
     const int64_t my_tiles =
         ntiles > (int64_t)blockIdx.x ? (ntiles - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
     const bool leader = threadIdx.x == 0;
@@ -573,11 +586,11 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
     timeline_mark(1);
     // One stage = the tile's input records (and its second-input records), one mbarrier.
     auto load_stage = [&](int st, int64_t tile) {
-        mbar_arrive_expect_tx(&full[st], L::kInBytes + L::kIn2Bytes);
+        mbar_arrive_expect_tx(&full[st], load_bytes + L::kIn2Bytes);
         if (HINTS & 1)
-            bulk_load(s_in + st * L::kInBytes, x + tile * TR * LDX, L::kInBytes, &full[st], policy);
+            bulk_load(s_in + st * L::kStageBytes, xa + tile * L::kInBytes, load_bytes, &full[st], policy);
         else
-            bulk_load_plain(s_in + st * L::kInBytes, x + tile * TR * LDX, L::kInBytes, &full[st]);
+            bulk_load_plain(s_in + st * L::kStageBytes, xa + tile * L::kInBytes, load_bytes, &full[st]);
         if constexpr (N2 > 0)
             bulk_load_plain(s_in2 + st * L::kIn2Bytes, x2 + tile * TR * N2, L::kIn2Bytes, &full[st]);
     };
@@ -594,7 +607,7 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
         if (k == 0) timeline_mark(2);
         timeline_tile(k, 0, threadIdx.x == 0);
 
-        const T* tin = reinterpret_cast<const T*>(s_in + s * L::kInBytes);
+        const T* tin = reinterpret_cast<const T*>(s_in + s * L::kStageBytes + mis);
         const T* tin2 = reinterpret_cast<const T*>(s_in2 + s * L::kIn2Bytes);
         T* t0 = reinterpret_cast<T*>(s_out + ob * L::kOutBytes);
         T* t1 = t0 + TR * W0;

@@ -198,6 +198,28 @@ def test_padded_records_xyz_in_xyzw(cuda_dev, prec, n):
         assert bad == 0, (fam, prec, n, bad, first)
 
 
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("offset_rows", [1, 2, 3])
+def test_misaligned_rows_bulk_path(cuda_dev, prec, offset_rows):
+    """Rows whose storage starts off a 16-byte boundary (x[k:] of a dense array) run the
+    bulk-copy kernel from the boundary below each tile: every family, sizes around the
+    tile and the end-of-array reach, bit for bit against the oracle."""
+    single = prec == "f32"
+    tr = 512 if single else 256
+    ka = np.array(fn.kernel_args(fn.preset(PREC[prec])))
+    for n in (tr - 1, tr, tr + 1, 2 * tr - 1, 2 * tr + 5, 100_003):
+        x = _random_rows(n + offset_rows, 3, single, seed=n * 7 + offset_rows + single)
+        xd = torch.from_numpy(x).to(cuda_dev)[offset_rows:]
+        for fam in FAMILIES[3] + ["normalize_sq"]:
+            base = "normalize3_sq" if fam == "normalize_sq" else _base(fam, 3)
+            op = _lib.OP_NORMALIZE_SQ if fam == "normalize_sq" else OPS[fam]
+            takes = fam in SCALING or fam == "normalize_sq"
+            res = _cuda_kernels.batch_kernel(base, prec)(xd, ka if takes else None)
+            torch.cuda.synchronize()
+            bad, first = compare_chunked(op, xd, res.head, res.body, res.sq, ka if takes else None)
+            assert bad == 0, (fam, prec, offset_rows, n, first)
+
+
 def test_strided_rows_other_layouts(cuda_dev):
     """Other row strides (per-row kernel), a misaligned padded view, a last record that
     ends at its third element, rotation apply on padded vectors, and outputs overlapping
