@@ -406,21 +406,31 @@ static int launch_soa(const void* const* xs, int64_t n, void* head, void* const*
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-    bool aligned = aligned16(p.head) && (Op::W2 == 0 || aligned16(p.extra));
-    for (int c = 0; c < N; ++c) aligned = aligned && aligned16(p.x[c]) && (Op::W1 == 0 || aligned16(p.body[c]));
+    bool outs_aligned = aligned16(p.head) && (Op::W2 == 0 || aligned16(p.extra));
+    bool ins_aligned = true, ins_elem = true;
+    int64_t reach = 0;  // bytes the bulk loads of a misaligned array read past a run
+    for (int c = 0; c < N; ++c) {
+        outs_aligned = outs_aligned && (Op::W1 == 0 || aligned16(p.body[c]));
+        ins_aligned = ins_aligned && aligned16(p.x[c]);
+        ins_elem = ins_elem && ((uintptr_t)p.x[c] % sizeof(T)) == 0;
+        const int mis = (int)((uintptr_t)p.x[c] & 15);
+        if (mis) reach = std::max<int64_t>(reach, 16 - mis);
+    }
+    const bool aligned = outs_aligned && ins_aligned;
     constexpr int V = Vec16<T>::kRows;
     const int sms = device_sms(dev);
     using ST = SoaTile<T, N, OP>;
-    if (aligned && !force_direct() && soa_path() == 0 && n >= ST::TR) {
+    if (outs_aligned && ins_elem && !force_direct() && soa_path() == 0 && n >= ST::TR) {
         // bulk-copy pipeline over whole tiles, the rest through the scalar form below
         static std::once_flag attr_once;
         std::call_once(attr_once, [] {
             cudaFuncSetAttribute(tma_soa_kernel<T, N, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  ST::kSmemBytes);
         });
-        const int64_t ntiles = n / ST::TR;
+        // whole runs whose loads (and their reach past a misaligned run) stay inside the arrays
+        const int64_t ntiles = (n * (int64_t)sizeof(T) - reach) / ST::kArr;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)sms * ST::kCtasPerSm));
-        e = launch_pdl(tma_soa_kernel<T, N, OP>, grid, ST::NT, ST::kSmemBytes, stream, p, n, ka);
+        if (ntiles > 0) e = launch_pdl(tma_soa_kernel<T, N, OP>, grid, ST::NT, ST::kSmemBytes, stream, p, ntiles, ka);
         if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
         const int64_t done = ntiles * ST::TR;
         if (done == n) return FN_OK;

@@ -696,12 +696,17 @@ template <typename T, int N, int OP> struct SoaTile {
     static constexpr int kCtasPerSm = FNB_SOA_CTAS_PER_SM;
     static constexpr int kOutArrays = 1 + Op::W1 + Op::W2;
     static constexpr int kArr = TR * (int)sizeof(T);           // bytes of one array's run
-    static constexpr int kInBytes = N * kArr, kOutBytes = kOutArrays * kArr;
+    static constexpr int kArrStage = kArr + 16;                 // + room for a misaligned array
+    static constexpr int kInBytes = N * kArrStage, kOutBytes = kOutArrays * kArr;
     static constexpr int kSmemBytes = S * kInBytes + OB * kOutBytes + S * 8;
 };
 
+// A component array whose storage is off the 16-byte grid (a[1:] of an array) is
+// loaded like tma_stream_kernel's misaligned rows: from the boundary below the run,
+// 16 bytes longer, read at the offset.  The host keeps every tile's reach inside the
+// arrays (ntiles is computed with it) and requires 16-byte aligned outputs.
 template <typename T, int N, int OP>
-__global__ void __launch_bounds__(256) tma_soa_kernel(SoaPtrs<T, N> p, int64_t nrows, KArgs<T> ka) {
+__global__ void __launch_bounds__(256) tma_soa_kernel(SoaPtrs<T, N> p, int64_t ntiles, KArgs<T> ka) {
     using L = SoaTile<T, N, OP>;
     using Op = typename L::Op;
     constexpr int TR = L::TR, S = L::S, OB = L::OB, NT = L::NT;
@@ -710,10 +715,16 @@ __global__ void __launch_bounds__(256) tma_soa_kernel(SoaPtrs<T, N> p, int64_t n
     unsigned char* s_in = smem;
     unsigned char* s_out = smem + S * L::kInBytes;
     uint64_t* full = reinterpret_cast<uint64_t*>(s_out + OB * L::kOutBytes);
-    const int64_t ntiles = nrows / TR;
     const int64_t my_tiles =
         ntiles > (int64_t)blockIdx.x ? (ntiles - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
     const bool leader = threadIdx.x == 0;
+    int mis[N];
+    uint32_t tx = 0;
+#pragma unroll
+    for (int c = 0; c < N; ++c) {
+        mis[c] = (int)(reinterpret_cast<uintptr_t>(p.x[c]) & 15);
+        tx += L::kArr + (mis[c] ? 16 : 0);
+    }
     if (leader) {
 #pragma unroll
         for (int st = 0; st < S; ++st) mbar_init(&full[st], 1);
@@ -723,10 +734,12 @@ __global__ void __launch_bounds__(256) tma_soa_kernel(SoaPtrs<T, N> p, int64_t n
     grid_dependency_wait();
     grid_launch_dependents();
     auto load_stage = [&](int st, int64_t tile) {
-        mbar_arrive_expect_tx(&full[st], L::kInBytes);
+        mbar_arrive_expect_tx(&full[st], tx);
 #pragma unroll
         for (int c = 0; c < N; ++c)
-            bulk_load_plain(s_in + st * L::kInBytes + c * L::kArr, p.x[c] + tile * TR, L::kArr, &full[st]);
+            bulk_load_plain(s_in + st * L::kInBytes + c * L::kArrStage,
+                            reinterpret_cast<const unsigned char*>(p.x[c]) - mis[c] + tile * L::kArr,
+                            L::kArr + (mis[c] ? 16 : 0), &full[st]);
     };
     if (leader)
         for (int64_t k = 0; k < my_tiles && k < S; ++k) load_stage((int)k, (int64_t)blockIdx.x + k * gridDim.x);
@@ -735,14 +748,15 @@ __global__ void __launch_bounds__(256) tma_soa_kernel(SoaPtrs<T, N> p, int64_t n
         const int ob = (int)(k % OB);
         const int64_t tile = (int64_t)blockIdx.x + k * gridDim.x;
         mbar_wait(&full[st], (uint32_t)((k / S) & 1));
-        const T* tin = reinterpret_cast<const T*>(s_in + st * L::kInBytes);
+        const unsigned char* tin = s_in + st * L::kInBytes;
         T* tout = reinterpret_cast<T*>(s_out + ob * L::kOutBytes);
 #pragma unroll
         for (int it = 0; it < TR / NT; ++it) {
             const int j = (int)threadIdx.x + it * NT;
             T xr[N], o0[1], o1[Slot<W1>::value], o2[1];
 #pragma unroll
-            for (int c = 0; c < N; ++c) xr[c] = tin[c * TR + j];
+            for (int c = 0; c < N; ++c)
+                xr[c] = *reinterpret_cast<const T*>(tin + c * L::kArrStage + mis[c] + j * (int)sizeof(T));
             (void)Op::apply(xr, ka, o0, o1, o2);
             tout[j] = o0[0];
 #pragma unroll

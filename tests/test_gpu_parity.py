@@ -753,6 +753,34 @@ def test_structure_of_arrays_columns_of_records(cuda_dev, home):
                     assert oracle.same(as_np(got.unit[j]), as_np(want.unit[:, j])).all(), (prec, dim, width, order)
 
 
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_structure_of_arrays_misaligned_bulk_path(cuda_dev, prec):
+    """Component arrays off the 16-byte grid by different amounts (one each of 0, 1, 2, 3
+    elements) through the bulk-copy SoA kernel, sizes around the run length and the end
+    reach: every scaling family equals the AoS call bit for bit."""
+    single = prec == "f32"
+    p = fn.preset(PREC[prec])
+    run = 1024 if single else 512  # rows per 4 KiB run
+    for dim in (2, 3, 4):
+        for n in (run, run + 1, 2 * run - 1, 3 * run + 3, 100_003):
+            x = _random_rows(n, dim, single, seed=n + dim + single)
+            xd = torch.from_numpy(x).to(cuda_dev)
+            comps = []
+            for k in range(dim):  # array k starts k elements past an aligned allocation
+                buf = torch.zeros(n + k, dtype=xd.dtype, device=cuda_dev)
+                buf[k:] = xd[:, k]
+                comps.append(buf[k:])
+            for name in (f"normalize{dim}", f"normalize{dim}_sq", f"norm{dim}", f"scale{dim}"):
+                got, want = getattr(fn, name)(p, *comps), getattr(fn, name)(p, xd)
+                pairs = zip(got, want) if hasattr(got, "_fields") else [(got, want)]
+                for a, b in pairs:
+                    if isinstance(a, tuple):  # per-component arrays vs the AoS columns
+                        assert all(oracle.same(a[k].cpu().numpy(), b[:, k].cpu().numpy()).all()
+                                   for k in range(dim)), (prec, dim, n, name)
+                    else:
+                        assert oracle.same(a.cpu().numpy(), b.cpu().numpy()).all(), (prec, dim, n, name)
+
+
 def test_structure_of_arrays_unaligned_and_tails(cuda_dev):
     """Component arrays at an 8-byte offset (scalar SoA kernel) and lengths that leave a
     partial 16-byte vector (vector kernel + scalar tail) give the AoS results."""
