@@ -87,11 +87,11 @@ static bool is_rotation(int op) {
 }
 
 // Per-instantiation occupancy (computed once per process and device).
-template <typename T, int N, int OP, int LDX = 0> struct TmaLaunch {
-    using L = TileLayout<T, N, OP, OpRows<T, N, OP>::value, OpStages<T, N, OP>::value, OutTiles<OP>::value, LDX>;
+template <typename T, int N, int OP, int LDX = 0, bool MIS = false> struct TmaLaunch {
+    using L = TileLayout<T, N, OP, OpRows<T, N, OP>::value, OpStages<T, N, OP>::value, OutTiles<OP>::value, LDX, MIS>;
     static constexpr auto kernel() {
         return tma_stream_kernel<T, N, OP, OpRows<T, N, OP>::value, OpStages<T, N, OP>::value, Tile<T, N>::kThreads,
-                                 Tile<T, N>::kHints, OutTiles<OP>::value, LDX>;
+                                 Tile<T, N>::kHints, OutTiles<OP>::value, LDX, MIS>;
     }
     static int blocks_per_sm(int dev) {
         static std::mutex mu;
@@ -182,10 +182,10 @@ template <int N> struct PaddedLdx {
     static constexpr int value = N == 3 ? 4 : 0;
 };
 
-template <typename T, int N, int OP, int LDX = 0>
-static cudaError_t launch_tma(const T* x, const T* x2, int64_t n, T* head, T* body, T* extra, const KArgs<T>& ka,
-                              int dev, int sms, cudaStream_t stream) {
-    using TL = TmaLaunch<T, N, OP, LDX>;
+template <typename T, int N, int OP, int LDX, bool MIS>
+static cudaError_t launch_tma_as(const T* x, const T* x2, int64_t n, T* head, T* body, T* extra,
+                                 const KArgs<T>& ka, int dev, int sms, cudaStream_t stream) {
+    using TL = TmaLaunch<T, N, OP, LDX, MIS>;
     using L = typename TL::L;
     const int64_t ntiles = n / L::TR;
     const int64_t per_sm = std::min<int64_t>(TL::blocks_per_sm(dev), ctas_per_sm_for<OP>(ntiles, sms));
@@ -193,6 +193,15 @@ static cudaError_t launch_tma(const T* x, const T* x2, int64_t n, T* head, T* bo
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, resident));
     return launch_pdl(TL::kernel(), grid, Tile<T, N>::kThreads, L::kSmemBytes, stream, x, x2, n, head, body, extra,
                       ka);
+}
+
+// MIS: the instantiation for inputs off the 16-byte grid (tma_stream_kernel).
+template <typename T, int N, int OP, int LDX = 0>
+static cudaError_t launch_tma(const T* x, const T* x2, int64_t n, T* head, T* body, T* extra, const KArgs<T>& ka,
+                              int dev, int sms, cudaStream_t stream) {
+    if (!aligned16(x) || (x2 && !aligned16(x2)))
+        return launch_tma_as<T, N, OP, LDX, true>(x, x2, n, head, body, extra, ka, dev, sms, stream);
+    return launch_tma_as<T, N, OP, LDX, false>(x, x2, n, head, body, extra, ka, dev, sms, stream);
 }
 
 template <typename T, int N, int OP>
@@ -212,10 +221,10 @@ static int launch(const void* xv, const void* x2v, int64_t n, void* hv, void* bv
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
     const int sms = device_sms(dev);
-    // The bulk-copy kernel needs 16-byte aligned outputs (and inputs for the two-input
-    // ops); single-input rows only need element alignment: a misaligned x is loaded from
-    // the 16-byte boundary below each tile (tma_stream_kernel).
-    const bool x_ok = N2 == 0 ? ((uintptr_t)x % sizeof(T)) == 0 : (aligned16(x) && aligned16(x2));
+    // The bulk-copy kernel needs 16-byte aligned outputs; inputs only need element
+    // alignment: a misaligned input is loaded from the 16-byte boundary below each tile
+    // (tma_stream_kernel).
+    const bool x_ok = ((uintptr_t)x % sizeof(T)) == 0 && (N2 == 0 || ((uintptr_t)x2 % sizeof(T)) == 0);
     const bool aligned = x_ok && aligned16(head) && (Op::W1 == 0 || aligned16(body)) &&
                          (Op::W2 == 0 || aligned16(extra));
     constexpr int kPad = PaddedLdx<N>::value;
@@ -421,16 +430,22 @@ static int launch_soa(const void* const* xs, int64_t n, void* head, void* const*
     const int sms = device_sms(dev);
     using ST = SoaTile<T, N, OP>;
     if (outs_aligned && ins_elem && !force_direct() && soa_path() == 0 && n >= ST::TR) {
-        // bulk-copy pipeline over whole tiles, the rest through the scalar form below
+        // bulk-copy pipeline over whole runs (the instantiation for arrays off the 16-byte
+        // grid when any is), the rest through the kernels below
+        const bool mis = !ins_aligned;
+        auto kern = mis ? tma_soa_kernel<T, N, OP, true> : tma_soa_kernel<T, N, OP, false>;
+        const int smem = mis ? SoaTile<T, N, OP, true>::kSmemBytes : ST::kSmemBytes;
         static std::once_flag attr_once;
         std::call_once(attr_once, [] {
-            cudaFuncSetAttribute(tma_soa_kernel<T, N, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cudaFuncSetAttribute(tma_soa_kernel<T, N, OP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  ST::kSmemBytes);
+            cudaFuncSetAttribute(tma_soa_kernel<T, N, OP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 SoaTile<T, N, OP, true>::kSmemBytes);
         });
         // whole runs whose loads (and their reach past a misaligned run) stay inside the arrays
         const int64_t ntiles = (n * (int64_t)sizeof(T) - reach) / ST::kArr;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)sms * ST::kCtasPerSm));
-        if (ntiles > 0) e = launch_pdl(tma_soa_kernel<T, N, OP>, grid, ST::NT, ST::kSmemBytes, stream, p, ntiles, ka);
+        if (ntiles > 0) e = launch_pdl(kern, grid, ST::NT, (size_t)smem, stream, p, ntiles, ka);
         if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
         const int64_t done = ntiles * ST::TR;
         if (done == n) return FN_OK;

@@ -438,7 +438,11 @@ template <int OP> struct OutTiles {
 
 // LDX_: elements per input record (0 = N, dense rows; N = 3 with LDX_ = 4 reads xyz out of
 // xyzw records: the bulk copy moves whole records, the row op reads the first N).
-template <typename T, int N, int OP, int TR_, int S_, int OB_ = OutTiles<OP>::value, int LDX_ = 0> struct TileLayout {
+// MIS_: the instantiation for inputs off the 16-byte grid (see tma_stream_kernel); the
+// aligned instantiation keeps the plain layout and code.
+template <typename T, int N, int OP, int TR_, int S_, int OB_ = OutTiles<OP>::value, int LDX_ = 0,
+          bool MIS_ = false>
+struct TileLayout {
     using Op = RowOp<T, N, OP>;
     static constexpr int TR = TR_;
     static constexpr int S = S_;
@@ -447,15 +451,18 @@ template <typename T, int N, int OP, int TR_, int S_, int OB_ = OutTiles<OP>::va
     static_assert(OB >= 3, "the store pipeline keeps OB - 2 groups reading behind the current one");
     static_assert(LDX >= N, "an input record holds at least the N components");
     static constexpr int kInBytes = TR * LDX * (int)sizeof(T);
-    // a stage holds one tile of records plus 16 bytes: rows whose storage is not 16-byte
-    // aligned are loaded from the aligned address below them (see tma_stream_kernel)
-    static constexpr int kStageBytes = kInBytes + 16;
+    // MIS_: a stage holds one tile of records plus room for 16 more bytes (rows whose
+    // storage is not 16-byte aligned are loaded from the aligned address below them);
+    // 128 bytes of room keep every stage and staging tile 128-byte aligned
+    static constexpr int kRoom = MIS_ ? 128 : 0;
+    static constexpr int kStageBytes = kInBytes + kRoom;
     static constexpr int kIn2Bytes = TR * InWidth2<Op>::value * (int)sizeof(T);  // second input
     static constexpr int kB0 = TR * Op::W0 * (int)sizeof(T);
     static constexpr int kB1 = TR * Op::W1 * (int)sizeof(T);
     static constexpr int kB2 = TR * Op::W2 * (int)sizeof(T);
     static constexpr int kOutBytes = kB0 + kB1 + kB2;
-    static constexpr int kSmemBytes = S * (kStageBytes + kIn2Bytes) + OB * kOutBytes + S * 8;
+    static constexpr int kIn2StageBytes = kIn2Bytes > 0 ? kIn2Bytes + kRoom : 0;  // same room for x2
+    static constexpr int kSmemBytes = S * (kStageBytes + kIn2StageBytes) + OB * kOutBytes + S * 8;
     static_assert(kInBytes % 16 == 0 && kIn2Bytes % 16 == 0 && kB0 % 16 == 0 && kB1 % 16 == 0 &&
                       kB2 % 16 == 0,
                   "bulk copies need 16 B multiples");
@@ -538,12 +545,12 @@ __device__ __forceinline__ void timeline_tile(int64_t, int, bool = true) {}
 
 template <typename T, int N, int OP, int TR_ = OpRows<T, N, OP>::value, int S_ = OpStages<T, N, OP>::value,
           int NT = Tile<T, N>::kThreads, int HINTS = Tile<T, N>::kHints, int OB_ = OutTiles<OP>::value,
-          int LDX_ = 0>
+          int LDX_ = 0, bool MIS = false>
 __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x, const T* __restrict__ x2,
                                                         int64_t nrows, T* __restrict__ head,
                                                         T* __restrict__ body, T* __restrict__ extra,
                                                         KArgs<T> ka) {
-    using L = TileLayout<T, N, OP, TR_, S_, OB_, LDX_>;
+    using L = TileLayout<T, N, OP, TR_, S_, OB_, LDX_, MIS>;
     using Op = typename L::Op;
     constexpr int TR = L::TR, S = L::S, OB = L::OB, LDX = L::LDX;
     constexpr int W0 = Op::W0, W1 = Op::W1, W2 = Op::W2;
@@ -551,23 +558,37 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned char* s_in = smem;
     unsigned char* s_in2 = smem + S * L::kStageBytes;  // second input ring (two-input ops)
-    unsigned char* s_out = s_in2 + S * L::kIn2Bytes;
+    unsigned char* s_out = s_in2 + S * L::kIn2StageBytes;
     uint64_t* full = reinterpret_cast<uint64_t*>(s_out + OB * L::kOutBytes);
     timeline_mark(0);
 
-    // Rows whose storage is not 16-byte aligned (x[1:] of a dense array; the outputs and
-    // a second input must be aligned, the host checks): every stage is loaded from the
-    // 16-byte boundary `mis` bytes below its first row, 16 bytes longer, and read at
-    // offset `mis`.  Bulk tiles only cover bytes inside [boundary below x, last row's
-    // end]; the reach below x stays inside x's 16-byte block, hence inside its
-    // allocation.  Padded records: the last row may end at its N-th element (a strided
-    // view of a shorter allocation), so no tile reads past that element either.
-    const int mis = (int)(reinterpret_cast<uintptr_t>(x) & 15);
-    const int64_t avail = ((nrows - 1) * LDX + N) * (int64_t)sizeof(T);  // bytes from x to the last row's end
-    const int64_t reach = mis ? 16 - mis : 0;                               // bytes a load reads past its tile
-    const int64_t ntiles = avail >= reach ? (avail - reach) / L::kInBytes : 0;
+    // MIS: inputs whose storage is not 16-byte aligned (x[1:] of a dense array; outputs
+    // must be aligned, the host checks).  Every stage is loaded from the 16-byte boundary
+    // `mis` bytes below its first row, 16 bytes longer, and read at offset `mis`.  Bulk
+    // tiles only cover bytes between that boundary and the last row's end; the reach
+    // below x stays inside x's 16-byte block, hence inside its allocation.  The second
+    // input of the two-input ops gets its own offset under the same rule.  (A separate
+    // instantiation: folding this into the aligned kernel cost 1-2.6 % on aligned rows,
+    // profiles/r01s23_ab_mis.txt.)
+    // Padded records: the last row may end at its N-th element (a strided view of a
+    // shorter allocation), so it never rides in a bulk tile that would read its padding.
+    const int mis = MIS ? (int)(reinterpret_cast<uintptr_t>(x) & 15) : 0;
+    const int mis2 = MIS && N2 > 0 ? (int)(reinterpret_cast<uintptr_t>(x2) & 15) : 0;
+    int64_t ntiles = (LDX == N ? nrows : nrows - 1) / TR;
+    if constexpr (MIS) {
+        const int64_t avail = ((nrows - 1) * LDX + N) * (int64_t)sizeof(T);  // x to the last row's end
+        const int64_t reach = mis ? 16 - mis : 0;                               // bytes read past a tile
+        ntiles = avail >= reach ? (avail - reach) / L::kInBytes : 0;
+        if constexpr (N2 > 0) {
+            const int64_t avail2 = nrows * N2 * (int64_t)sizeof(T), reach2 = mis2 ? 16 - mis2 : 0;
+            const int64_t ntiles2 = avail2 >= reach2 ? (avail2 - reach2) / L::kIn2Bytes : 0;
+            if (ntiles2 < ntiles) ntiles = ntiles2;
+        }
+    }
     const unsigned char* xa = reinterpret_cast<const unsigned char*>(x) - mis;
-    const uint32_t load_bytes = L::kInBytes + (mis ? 16 : 0);
+    const unsigned char* x2a = reinterpret_cast<const unsigned char*>(x2) - mis2;
+    const uint32_t load_bytes = L::kInBytes + (MIS && mis ? 16 : 0);
+    const uint32_t load2_bytes = L::kIn2Bytes + (MIS && mis2 ? 16 : 0);
     const int64_t my_tiles =
         ntiles > (int64_t)blockIdx.x ? (ntiles - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
     const bool leader = threadIdx.x == 0;
@@ -586,13 +607,20 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
     timeline_mark(1);
     // One stage = the tile's input records (and its second-input records), one mbarrier.
     auto load_stage = [&](int st, int64_t tile) {
-        mbar_arrive_expect_tx(&full[st], load_bytes + L::kIn2Bytes);
-        if (HINTS & 1)
-            bulk_load(s_in + st * L::kStageBytes, xa + tile * L::kInBytes, load_bytes, &full[st], policy);
-        else
+        if constexpr (MIS) {
+            mbar_arrive_expect_tx(&full[st], load_bytes + (N2 > 0 ? load2_bytes : 0));
             bulk_load_plain(s_in + st * L::kStageBytes, xa + tile * L::kInBytes, load_bytes, &full[st]);
-        if constexpr (N2 > 0)
-            bulk_load_plain(s_in2 + st * L::kIn2Bytes, x2 + tile * TR * N2, L::kIn2Bytes, &full[st]);
+            if constexpr (N2 > 0)
+                bulk_load_plain(s_in2 + st * L::kIn2StageBytes, x2a + tile * L::kIn2Bytes, load2_bytes, &full[st]);
+        } else {
+            mbar_arrive_expect_tx(&full[st], L::kInBytes + L::kIn2Bytes);
+            if (HINTS & 1)
+                bulk_load(s_in + st * L::kInBytes, x + tile * TR * LDX, L::kInBytes, &full[st], policy);
+            else
+                bulk_load_plain(s_in + st * L::kInBytes, x + tile * TR * LDX, L::kInBytes, &full[st]);
+            if constexpr (N2 > 0)
+                bulk_load_plain(s_in2 + st * L::kIn2Bytes, x2 + tile * TR * N2, L::kIn2Bytes, &full[st]);
+        }
     };
     if (leader) {
         for (int64_t k = 0; k < my_tiles && k < S; ++k) load_stage((int)k, (int64_t)blockIdx.x + k * gridDim.x);
@@ -607,8 +635,8 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
         if (k == 0) timeline_mark(2);
         timeline_tile(k, 0, threadIdx.x == 0);
 
-        const T* tin = reinterpret_cast<const T*>(s_in + s * L::kStageBytes + mis);
-        const T* tin2 = reinterpret_cast<const T*>(s_in2 + s * L::kIn2Bytes);
+        const T* tin = reinterpret_cast<const T*>(s_in + s * L::kStageBytes + (MIS ? mis : 0));
+        const T* tin2 = reinterpret_cast<const T*>(s_in2 + s * L::kIn2StageBytes + (MIS ? mis2 : 0));
         T* t0 = reinterpret_cast<T*>(s_out + ob * L::kOutBytes);
         T* t1 = t0 + TR * W0;
         T* t2 = t1 + TR * W1;
@@ -689,14 +717,14 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
 #ifndef FNB_SOA_CTAS_PER_SM
 #define FNB_SOA_CTAS_PER_SM 2
 #endif
-template <typename T, int N, int OP> struct SoaTile {
+template <typename T, int N, int OP, bool MIS = false> struct SoaTile {
     using Op = RowOp<T, N, OP>;
     static constexpr int TR = FNB_SOA_RUN_BYTES / (int)sizeof(T);  // one run of every array per tile
     static constexpr int S = FNB_SOA_STAGES, OB = 3, NT = 256;
     static constexpr int kCtasPerSm = FNB_SOA_CTAS_PER_SM;
     static constexpr int kOutArrays = 1 + Op::W1 + Op::W2;
     static constexpr int kArr = TR * (int)sizeof(T);           // bytes of one array's run
-    static constexpr int kArrStage = kArr + 16;                 // + room for a misaligned array
+    static constexpr int kArrStage = kArr + (MIS ? 128 : 0);    // + room for a misaligned array
     static constexpr int kInBytes = N * kArrStage, kOutBytes = kOutArrays * kArr;
     static constexpr int kSmemBytes = S * kInBytes + OB * kOutBytes + S * 8;
 };
@@ -705,9 +733,9 @@ template <typename T, int N, int OP> struct SoaTile {
 // loaded like tma_stream_kernel's misaligned rows: from the boundary below the run,
 // 16 bytes longer, read at the offset.  The host keeps every tile's reach inside the
 // arrays (ntiles is computed with it) and requires 16-byte aligned outputs.
-template <typename T, int N, int OP>
+template <typename T, int N, int OP, bool MIS = false>
 __global__ void __launch_bounds__(256) tma_soa_kernel(SoaPtrs<T, N> p, int64_t ntiles, KArgs<T> ka) {
-    using L = SoaTile<T, N, OP>;
+    using L = SoaTile<T, N, OP, MIS>;
     using Op = typename L::Op;
     constexpr int TR = L::TR, S = L::S, OB = L::OB, NT = L::NT;
     constexpr int W1 = Op::W1, W2 = Op::W2;
@@ -722,7 +750,7 @@ __global__ void __launch_bounds__(256) tma_soa_kernel(SoaPtrs<T, N> p, int64_t n
     uint32_t tx = 0;
 #pragma unroll
     for (int c = 0; c < N; ++c) {
-        mis[c] = (int)(reinterpret_cast<uintptr_t>(p.x[c]) & 15);
+        mis[c] = MIS ? (int)(reinterpret_cast<uintptr_t>(p.x[c]) & 15) : 0;
         tx += L::kArr + (mis[c] ? 16 : 0);
     }
     if (leader) {

@@ -148,6 +148,30 @@ def test_rotate_rows_golden(golden, cuda_dev, where):
         fn.normalize4_rotate(p, home(q), home(v))  # three non-finite quaternions
 
 
+@pytest.mark.parametrize("shift_q,shift_v", [(0, 1), (1, 0), (1, 1), (0, 2)])
+def test_rotate_rows_misaligned_bulk_path(cuda_dev, shift_q, shift_v):
+    """Two-input kernels with either input off the 16-byte grid (x[k:] views): both
+    inputs are loaded from the boundary below each tile; equal to the aligned call."""
+    n = 100_003
+    p = fn.preset("double")
+    q = torch.empty((n + 2, 4), dtype=torch.float64, device=cuda_dev)
+    workloads.generate_device(3, q)
+    v = torch.empty((n + 2, 3), dtype=torch.float64, device=cuda_dev)
+    workloads.generate_device(5, v)
+    qa, va = q[:n].clone(), v[:n].clone()
+    qs = torch.empty((n + shift_q, 4), dtype=torch.float64, device=cuda_dev)[shift_q:]
+    qs.copy_(qa)
+    flat = torch.empty(n * 3 + shift_v, dtype=torch.float64, device=cuda_dev)  # shift by elements
+    vs = flat[shift_v:].view(n, 3)
+    vs.copy_(va)
+    assert oracle.same(to_np(fn.normalize4_rotate(p, qs, vs)), to_np(fn.normalize4_rotate(p, qa, va))).all()
+    R = fn.rotation_unit(qa)
+    Rflat = torch.empty(n * 9 + shift_q, dtype=torch.float64, device=cuda_dev)
+    Rs = Rflat[shift_q:].view(n, 3, 3)
+    Rs.copy_(R)
+    assert oracle.same(to_np(fn.apply_rotations(Rs, vs)), to_np(fn.apply_rotations(R, va))).all()
+
+
 def test_rotate_rows_full_size(cuda_dev):
     """2^27 config-3 quaternions rotating 2^27 config-5-class vectors, vs the oracle, and
     the per-row matrix form on the rotation_unit matrices of the same quaternions."""
