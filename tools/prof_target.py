@@ -26,12 +26,18 @@ def main():
                              "normalize4_rotation"])
     ap.add_argument("--padded", action="store_true",
                     help="rows as xyz of xyzw records (3-D configs; fn_run_ld with ldx 4)")
+    ap.add_argument("--offset-rows", type=int, default=0,
+                    help="start the rows this many rows into the buffer (storage off the 16-byte grid)")
     a = ap.parse_args()
     c = workloads.CONFIGS[a.cfg]
     dt = torch.float64 if c.dtype == "float64" else torch.float32
     n = 1 << a.log2_rows
     x = torch.empty((n, c.dim), dtype=dt, device="cuda")
     workloads.generate_device(a.cfg, x)
+    if a.offset_rows:
+        big = torch.empty((n + a.offset_rows, c.dim), dtype=dt, device="cuda")
+        big[a.offset_rows:] = x
+        x = big[a.offset_rows:]
     if a.padded:
         rec = torch.zeros((n, c.dim + 1), dtype=dt, device="cuda")
         rec[:, :c.dim] = x
