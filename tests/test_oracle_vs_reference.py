@@ -10,6 +10,8 @@ import math
 
 import numpy as np
 import pytest
+from hypothesis import given, settings
+from hypothesis import strategies as st
 
 from conftest import FAMILIES, SCALING, kernel_name, same_scalar
 
@@ -106,3 +108,21 @@ def test_custom_constants_vs_reference(prec):
             x *= rng.integers(0, 2, (m, dim)) * 2 - 1
             x = x.astype(np.float32) if single else x
             _rows_vs_reference(x, prec, dim, ka=ka, families=["scale", "normalize", "norm"])
+
+
+# Full-range bit patterns, the strategies of the reference's property tests
+# (tests/test_scale.py:23-28): every finite, subnormal, zero, infinite and NaN value of the
+# format can come up, in any position of a row.
+_f64 = st.integers(0, 2 ** 64 - 1).map(lambda b: float(np.array(b, np.uint64).view(np.float64)))
+_f32 = st.integers(0, 2 ** 32 - 1).map(lambda b: float(np.array(b, np.uint32).view(np.float32)))
+
+
+@settings(max_examples=300, deadline=None)
+@given(dim=st.sampled_from([2, 3, 4]), prec=st.sampled_from(["f64", "f32"]), data=st.data())
+def test_hypothesis_rows_vs_reference(dim, prec, data):
+    """Hypothesis-drawn rows: the oracle equals the reference's compiled kernels on every
+    family (the reference's _same rule)."""
+    vals = data.draw(st.lists(st.lists(_f64 if prec == "f64" else _f32, min_size=dim, max_size=dim),
+                              min_size=1, max_size=8))
+    x = np.array(vals, dtype=np.float64 if prec == "f64" else np.float32)
+    _rows_vs_reference(x, prec, dim)
