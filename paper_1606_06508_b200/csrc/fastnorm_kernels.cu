@@ -435,13 +435,18 @@ static int launch_soa(const void* const* xs, int64_t n, void* head, void* const*
         const bool mis = !ins_aligned;
         auto kern = mis ? tma_soa_kernel<T, N, OP, true> : tma_soa_kernel<T, N, OP, false>;
         const int smem = mis ? SoaTile<T, N, OP, true>::kSmemBytes : ST::kSmemBytes;
-        static std::once_flag attr_once;
-        std::call_once(attr_once, [] {
-            cudaFuncSetAttribute(tma_soa_kernel<T, N, OP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 ST::kSmemBytes);
-            cudaFuncSetAttribute(tma_soa_kernel<T, N, OP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 SoaTile<T, N, OP, true>::kSmemBytes);
-        });
+        {  // the shared-memory opt-in is a per-device function attribute
+            static std::mutex mu;
+            static bool attr_set[64] = {false};
+            std::lock_guard<std::mutex> lk(mu);
+            if (dev >= 0 && dev < 64 && !attr_set[dev]) {
+                cudaFuncSetAttribute(tma_soa_kernel<T, N, OP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     ST::kSmemBytes);
+                cudaFuncSetAttribute(tma_soa_kernel<T, N, OP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     SoaTile<T, N, OP, true>::kSmemBytes);
+                attr_set[dev] = true;
+            }
+        }
         // whole runs whose loads (and their reach past a misaligned run) stay inside the arrays
         const int64_t ntiles = (n * (int64_t)sizeof(T) - reach) / ST::kArr;
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)sms * ST::kCtasPerSm));
