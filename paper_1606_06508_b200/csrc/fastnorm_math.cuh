@@ -260,6 +260,26 @@ __device__ __forceinline__ double tiny_quotient(double a, double b, int ea, unsi
     return __longlong_as_double((long long)((unsigned long long)n | sign));
 }
 
+// IEEE quotient when an operand is zero, infinite or NaN (the cases a library division
+// sends to its slow path): NaN for 0/0, inf/inf and any NaN; a signed infinity for
+// x/0 and inf/x; a signed zero for 0/x and x/inf.  Signs combine by xor.
+__device__ __forceinline__ float special_quotient(float a, float b) {
+    const unsigned sign = (__float_as_uint(a) ^ __float_as_uint(b)) & 0x80000000u;
+    const bool nan = isnan(a) || isnan(b) || (a == 0.0f && b == 0.0f) || (isinf(a) && isinf(b));
+    const bool inf = isinf(a) || b == 0.0f;
+    return nan ? __uint_as_float(0x7fc00000u) : __uint_as_float(sign | (inf ? 0x7f800000u : 0u));
+}
+
+__device__ __forceinline__ double special_quotient(double a, double b) {
+    const unsigned long long sign =
+        ((unsigned long long)__double_as_longlong(a) ^ (unsigned long long)__double_as_longlong(b)) &
+        0x8000000000000000ull;
+    const bool nan = isnan(a) || isnan(b) || (a == 0.0 && b == 0.0) || (isinf(a) && isinf(b));
+    const bool inf = isinf(a) || b == 0.0;
+    return nan ? __longlong_as_double(0x7ff8000000000000ll)
+               : __longlong_as_double((long long)(sign | (inf ? 0x7ff0000000000000ull : 0ull)));
+}
+
 #if !FNB_F64_DIV_MARKSTEIN
 // Plain IEEE division per numerator (__ddiv_rn).  Measured alternatives, all exact and
 // checked by fn_selftest_div, all slower on unit-range rows (configs 1, 3):
@@ -279,15 +299,39 @@ __device__ __forceinline__ double tiny_quotient(double a, double b, int ea, unsi
 #ifndef FNB_F64_TINY_QUOTIENT
 #define FNB_F64_TINY_QUOTIENT 0
 #endif
+// FNB_F64_DIV_SPECIAL: 1 = a zero, infinite or NaN divisor (tested once per divisor)
+// gives special_quotient instead of the library division's slow path; 2 = also a zero
+// numerator inline; 0 = plain __ddiv_rn.  Measured mixed (profiles/r01s29_ab_f64special.txt,
+// alternated processes): 1 = naive3 cfg 5 +3.9 %, quotient4 cfg 3 +4.7 %, quotient3
+// cfg 1 +3.4 %, but quotient2 cfg 2 -6.7 %, quotient3 cfg 5 -4.5 %; 2 = quotient2 +5.4 %,
+// naive3 +4.7 %, quotient3 +4.2 %, but quotient3_fast -4.2 %, quotient4 -3.0 %.  The
+// binary32 version pays because binary32 quotients are emulated in binary64; here the
+// special divisors are not where the time goes, so the plain division stays.
+#ifndef FNB_F64_DIV_SPECIAL
+#define FNB_F64_DIV_SPECIAL 0
+#endif
 template <> struct Divider<double> {
     double b;
+    bool bok;
 #if FNB_F64_TINY_QUOTIENT
     int eb;
-    __device__ __forceinline__ explicit Divider(double b_) : b(b_) { eb = biased_exp(b_); }
+    __device__ __forceinline__ explicit Divider(double b_) : b(b_) {
+        eb = biased_exp(b_);
+        bok = isfinite(b_) && b_ != 0.0;
+    }
 #else
-    __device__ __forceinline__ explicit Divider(double b_) : b(b_) {}
+    __device__ __forceinline__ explicit Divider(double b_) : b(b_) { bok = isfinite(b_) && b_ != 0.0; }
 #endif
     __device__ __forceinline__ double operator()(double a) const {
+#if FNB_F64_DIV_SPECIAL >= 1
+        if (!bok) return special_quotient(a, b);
+#endif
+#if FNB_F64_DIV_SPECIAL >= 2
+        if (a == 0.0)
+            return __longlong_as_double(
+                (long long)(((unsigned long long)__double_as_longlong(a) ^ (unsigned long long)__double_as_longlong(b)) &
+                            0x8000000000000000ull));
+#endif
 #if FNB_F64_TINY_QUOTIENT
         // Wide-range rows divide small components by large ones: results on the subnormal
         // grid take tiny_quotient (normal or subnormal numerator, normal divisor).
@@ -310,16 +354,6 @@ template <> struct Divider<double> : MarksteinDivider {
     __device__ __forceinline__ explicit Divider(double b_) : MarksteinDivider(b_) {}
 };
 #endif
-
-// IEEE quotient when an operand is zero, infinite or NaN (the cases a library division
-// sends to its slow path): NaN for 0/0, inf/inf and any NaN; a signed infinity for
-// x/0 and inf/x; a signed zero for 0/x and x/inf.  Signs combine by xor.
-__device__ __forceinline__ float special_quotient(float a, float b) {
-    const unsigned sign = (__float_as_uint(a) ^ __float_as_uint(b)) & 0x80000000u;
-    const bool nan = isnan(a) || isnan(b) || (a == 0.0f && b == 0.0f) || (isinf(a) && isinf(b));
-    const bool inf = isinf(a) || b == 0.0f;
-    return nan ? __uint_as_float(0x7fc00000u) : __uint_as_float(sign | (inf ? 0x7f800000u : 0u));
-}
 
 // Binary32 Markstein division in binary32 arithmetic (same argument as div_markstein
 // above, p = 24): y = RN(1/b) (__frcp_rn), q1 faithful, r1 exact, q2 = RN(a/b).
