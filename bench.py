@@ -401,8 +401,39 @@ def _batch_stream_rate(fn, p, x, bytes_per_row, peak, reps, sets=8, per_set=4):
         torch.cuda.synchronize(x.device)
         times.append(e0.elapsed_time(e1) / 1e3 / launches)
     t = statistics.median(times[1:])
-    del g, bufs
-    return {"launches_per_graph": launches, "buffer_sets": sets,
+    # the same 32 batches as one grouped call (normalize_many -> fn_run_many: one launch),
+    # graph-replayed like the launches above and eagerly through the public API
+    xs = [b[0] for _ in range(per_set) for b in bufs]
+    outs = [(b[1], b[2]) for _ in range(per_set) for b in bufs]
+    gm = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        fn.normalize_many(p, xs, out=outs)
+        torch.cuda.synchronize(x.device)
+        with torch.cuda.graph(gm, stream=s):
+            fn.normalize_many(p, xs, out=outs)
+    torch.cuda.synchronize(x.device)
+
+    def per_batch(run):
+        ts = []
+        for _ in range(max(reps, 3) + 1):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            cur = torch.cuda.current_stream(x.device)
+            e0.record(cur)
+            run()
+            e1.record(cur)
+            torch.cuda.synchronize(x.device)
+            ts.append(e0.elapsed_time(e1) / 1e3 / launches)
+        return statistics.median(ts[1:])
+
+    t_many = per_batch(gm.replay)
+    t_many_eager = per_batch(lambda: fn.normalize_many(p, xs, out=outs))
+    del g, gm, bufs, xs, outs
+    many = {"api": "normalize_many(p, 32 batches) -> fn_run_many, one launch",
+            "ms_per_batch": t_many * 1e3, "vectors_per_s": n / t_many,
+            "frac": n * bytes_per_row / t_many / 1e9 / peak,
+            "eager_public_api": {"ms_per_batch": t_many_eager * 1e3, "vectors_per_s": n / t_many_eager,
+                                 "frac": n * bytes_per_row / t_many_eager / 1e9 / peak}}
+    return {"launches_per_graph": launches, "buffer_sets": sets, "grouped_call": many,
             "bytes_cycled": sets * n * bytes_per_row, "ms_per_launch": t * 1e3,
             "vectors_per_s": n / t, "GB_per_s": n * bytes_per_row / t / 1e9,
             "frac": n * bytes_per_row / t / 1e9 / peak,

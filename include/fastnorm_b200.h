@@ -100,6 +100,15 @@ int fn_device_count(void);
  * for the naive / quotient families, which take no constants (_kernels.pyx:481-520). */
 int fn_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* body,
            void* sq, const double* ka, void* stream);
+/* Many independent batches in one launch: segment j is xs[j] [ns[j], dim] with its own
+ * outputs heads[j] / bodies[j] / extras[j] (bodies / extras may be NULL when the op has
+ * no such output).  16-byte aligned segments stream through one bulk-copy kernel (up to
+ * 48 per launch), so a stream of small batches pays one launch ramp and tail instead of
+ * one per batch; other segments are launched on their own.  Ops SCALE..NORMALIZE_SQ.
+ * Async on stream.  No reference interface (the reference takes one row per call). */
+int fn_run_many(int op, int dim, int dtype, int nseg, const void* const* xs, const int64_t* ns,
+                void* const* heads, void* const* bodies, void* const* extras, const double* ka,
+                void* stream);
 /* fn_run over rows that are ldx elements apart (ldx >= dim): row i is x[i*ldx .. i*ldx+dim),
  * the other ldx - dim elements of each record are not used.  Padded records such as xyz
  * in xyzw (dim 3, ldx 4; float4-style 16 B / 32 B records) and views like X[:, :3] of a

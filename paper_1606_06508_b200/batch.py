@@ -335,6 +335,65 @@ def run(op: int, dim: int, x, ka_arr: np.ndarray | None, out=None, invalid=None)
     return BatchOut(head, body, extra)
 
 
+def run_many(op: int, dim: int, xs, ka_arr: np.ndarray | None, outs=None) -> list:
+    """Kernel family ``op`` over several independent ``[N_j, dim]`` row arrays; returns
+    one BatchOut per array.  CUDA tensors (one device, one dtype) go to the device in one
+    launch per 48 arrays (fn_run_many); host arrays are run one by one (fn_host_run).
+    ``outs``: optional list of per-array ``out`` tuples, as for ``run``."""
+    import ctypes
+
+    xs = list(xs)
+    if outs is not None and len(outs) != len(xs):
+        raise ValueError("outs must hold one entry per array")
+    if not xs:
+        return []
+    if not all(is_torch(x) and x.is_cuda for x in xs):
+        return [run(op, dim, x, ka_arr, None if outs is None else outs[j]) for j, x in enumerate(xs)]
+    torch = _torch()
+    dev, dt = xs[0].device, xs[0].dtype
+    if any(x.device != dev or x.dtype != dt for x in xs):
+        raise TypeError("arrays must share device and dtype")
+    for x in xs:
+        if x.ndim != 2 or x.shape[1] != dim:
+            raise ValueError(f"expected rows of shape [N, {dim}], got {tuple(x.shape)}")
+    xs = [x if x.is_contiguous() else x.contiguous() for x in xs]
+    dcode = _dcode_of.get(dt)
+    if dcode is None:
+        dcode = _dcode_of[dt] = _dtype_code(str(dt).replace("torch.", ""))
+    w0, w1, w2 = widths(op, dim)
+    kinds = [(w0, "head")] + ([(w1, "body")] if w1 else []) + ([(w2, "extra")] if w2 else [])
+    res = []
+    for j, x in enumerate(xs):
+        o = outs[j] if outs is not None and outs[j] is not None else ()
+        n = x.shape[0]
+        arrays = []
+        for k, (w, what) in enumerate(kinds):
+            shape = _shape(n, w)
+            t = o[k] if len(o) > k else None
+            if t is None:
+                t = x.new_empty(shape)
+            elif not (t.dtype is dt and t.device == dev and t.shape == shape and t.is_contiguous()):
+                t = _check_out(t, shape, x, what)
+            arrays.append(t)
+        res.append(BatchOut(arrays[0], arrays[1] if w1 else None, arrays[-1] if w2 else None))
+    m = len(xs)
+    arr = (lambda vals: (ctypes.c_void_p * m)(*vals))
+    xp = arr([x.data_ptr() for x in xs])
+    hp = arr([r.head.data_ptr() for r in res])
+    bp = arr([r.body.data_ptr() for r in res]) if w1 else None
+    qp = arr([r.sq.data_ptr() for r in res]) if w2 else None
+    ns = (ctypes.c_int64 * m)(*[int(x.shape[0]) for x in xs])
+    kptr = None if ka_arr is None else _ka_address(ka_arr)
+    with torch.cuda.device(dev):
+        rc = _lib.lib().fn_run_many(op, dim, dcode, m, ctypes.addressof(xp), ctypes.addressof(ns),
+                                    ctypes.addressof(hp), None if bp is None else ctypes.addressof(bp),
+                                    None if qp is None else ctypes.addressof(qp), kptr,
+                                    _cuda_stream(torch, dev.index))
+    if rc:
+        _lib.check(rc, "fn_run_many")
+    return res
+
+
 def run_rows2(op: int, a, v, ka_arr: np.ndarray | None, out=None, invalid=None):
     """Two-input ops (per-row rotation of vectors): a = q[N, 4] (OP_QUAT_ROTATE) or
     R[N, 9] (OP_MAT_APPLY), v[N, 3], both float64 and in the same home (CUDA tensors on

@@ -383,6 +383,131 @@ int run_ex(int op, int dim, int dtype, const void* x, int64_t n, void* head, voi
     return dispatch<float>(op, dim, x, n, head, body, sq, ka, invalid, s, ldx);
 }
 
+// ---------------------------------------------------------------------------------
+// Many independent batches (segments) per launch: fn_run_many.
+// ---------------------------------------------------------------------------------
+template <typename T, int N, int OP> struct SegLaunch {
+    using L = TileLayout<T, N, OP, OpRows<T, N, OP>::value, OpStages<T, N, OP>::value>;
+    static int blocks_per_sm(int dev) {
+        static std::mutex mu;
+        static int cache[64] = {0};
+        std::lock_guard<std::mutex> lk(mu);
+        if (dev < 0 || dev >= 64) return 1;
+        if (cache[dev] == 0) {
+            auto kern = tma_segments_kernel<T, N, OP>;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemBytes);
+            int nb = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, Tile<T, N>::kThreads, L::kSmemBytes) !=
+                    cudaSuccess ||
+                nb < 1)
+                nb = 1;
+            cache[dev] = nb;
+        }
+        return cache[dev];
+    }
+};
+
+template <typename T, int N, int OP>
+static int launch_many(int nseg, const void* const* xs, const int64_t* ns, void* const* heads, void* const* bodies,
+                       void* const* extras, const KArgs<T>& ka, cudaStream_t stream) {
+    using SL = SegLaunch<T, N, OP>;
+    using L = typename SL::L;
+    using Op = typename L::Op;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    const int sms = device_sms(dev);
+    SegmentTable<T> tab;
+    auto flush = [&]() -> int {
+        if (tab.nseg == 0) return FN_OK;
+        const int64_t work = std::max<int64_t>(tab.ntiles, 1);
+        const int64_t per_sm = std::min<int64_t>(SL::blocks_per_sm(dev), ctas_per_sm_for<OP>(tab.ntiles, sms));
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(work, tab.nseg), per_sm * sms));
+        const cudaError_t le = launch_pdl(tma_segments_kernel<T, N, OP>, grid, Tile<T, N>::kThreads, L::kSmemBytes,
+                                          stream, tab, ka);
+        if (le != cudaSuccess) return cuda_fail(le, "kernel launch");
+        tab.nseg = 0;
+        tab.ntiles = 0;
+        return FN_OK;
+    };
+    tab.nseg = 0;
+    tab.ntiles = 0;
+    for (int j = 0; j < nseg; ++j) {
+        const int64_t n = ns[j];
+        if (n == 0) continue;
+        const bool aligned = aligned16(xs[j]) && aligned16(heads[j]) && (Op::W1 == 0 || aligned16(bodies[j])) &&
+                             (Op::W2 == 0 || aligned16(extras[j]));
+        if (!aligned || force_direct()) {  // this segment on its own (per-row or misaligned kernels)
+            const int rc = launch<T, N, OP>(xs[j], nullptr, n, heads[j], Op::W1 ? bodies[j] : nullptr,
+                                            Op::W2 ? extras[j] : nullptr, ka, stream);
+            if (rc != FN_OK) return rc;
+            continue;
+        }
+        Segment<T>& sg = tab.seg[tab.nseg++];
+        sg.x = static_cast<const T*>(xs[j]);
+        sg.head = static_cast<T*>(heads[j]);
+        sg.body = Op::W1 ? static_cast<T*>(bodies[j]) : nullptr;
+        sg.extra = Op::W2 ? static_cast<T*>(extras[j]) : nullptr;
+        sg.rows = n;
+        sg.tile0 = tab.ntiles;
+        tab.ntiles += n / L::TR;
+        if (tab.nseg == kMaxSegments) {
+            const int rc = flush();
+            if (rc != FN_OK) return rc;
+        }
+    }
+    return flush();
+}
+
+template <typename T, int OP>
+static int many_dim(int dim, int nseg, const void* const* xs, const int64_t* ns, void* const* h, void* const* b,
+                    void* const* q, const KArgs<T>& ka, cudaStream_t s) {
+    switch (dim) {
+        case 2: return launch_many<T, 2, OP>(nseg, xs, ns, h, b, q, ka, s);
+        case 3: return launch_many<T, 3, OP>(nseg, xs, ns, h, b, q, ka, s);
+        case 4: return launch_many<T, 4, OP>(nseg, xs, ns, h, b, q, ka, s);
+        default: return fail(FN_EINVAL, "dim must be 2, 3 or 4");
+    }
+}
+
+template <typename T>
+static int dispatch_many(int op, int dim, int nseg, const void* const* xs, const int64_t* ns, void* const* h,
+                         void* const* b, void* const* q, const double* kad, cudaStream_t s) {
+    KArgs<T> ka;
+    int rc = make_kargs<T>(kad, needs_ka(op), ka);
+    if (rc != FN_OK) return rc;
+    switch (op) {
+        case FN_OP_SCALE: return many_dim<T, FN_OP_SCALE>(dim, nseg, xs, ns, h, b, q, ka, s);
+        case FN_OP_NORMALIZE: return many_dim<T, FN_OP_NORMALIZE>(dim, nseg, xs, ns, h, b, q, ka, s);
+        case FN_OP_NORMALIZE_SQ: return many_dim<T, FN_OP_NORMALIZE_SQ>(dim, nseg, xs, ns, h, b, q, ka, s);
+        case FN_OP_NORM: return many_dim<T, FN_OP_NORM>(dim, nseg, xs, ns, h, b, q, ka, s);
+        case FN_OP_NAIVE: return many_dim<T, FN_OP_NAIVE>(dim, nseg, xs, ns, h, b, q, ka, s);
+        case FN_OP_QUOTIENT: return many_dim<T, FN_OP_QUOTIENT>(dim, nseg, xs, ns, h, b, q, ka, s);
+        case FN_OP_QUOTIENT3_FAST:
+            if (dim != 3) return fail(FN_EINVAL, "quotient3_fast is defined for dim 3 only");
+            return launch_many<T, 3, FN_OP_QUOTIENT3_FAST>(nseg, xs, ns, h, b, q, ka, s);
+        default: return fail(FN_EINVAL, "fn_run_many takes the scaling and baseline families");
+    }
+}
+
+int run_many(int op, int dim, int dtype, int nseg, const void* const* xs, const int64_t* ns, void* const* heads,
+             void* const* bodies, void* const* extras, const double* ka, void* stream) {
+    if (nseg < 0 || (nseg > 0 && (!xs || !ns || !heads))) return fail(FN_EINVAL, "bad segment arrays");
+    if (op < FN_OP_SCALE || op > FN_OP_NORMALIZE_SQ) return fail(FN_EINVAL, "fn_run_many takes the scaling and baseline families");
+    const Widths w = op_widths(op, dim);
+    if (w.w1 && !bodies) return fail(FN_EINVAL, "bodies must not be NULL for this op");
+    if (w.w2 && !extras) return fail(FN_EINVAL, "extras must not be NULL for this op");
+    for (int j = 0; j < nseg; ++j) {
+        const int rc = check_args(op, dim, dtype, xs[j], ns[j], heads[j], w.w1 ? bodies[j] : nullptr,
+                                  w.w2 ? extras[j] : nullptr);
+        if (rc != FN_OK) return rc;
+    }
+    if (nseg == 0) return FN_OK;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (dtype == FN_F64) return dispatch_many<double>(op, dim, nseg, xs, ns, heads, bodies, extras, ka, s);
+    return dispatch_many<float>(op, dim, nseg, xs, ns, heads, bodies, extras, ka, s);
+}
+
 int run(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* body, void* sq,
         const double* ka, void* stream) {
     return run_ex(op, dim, dtype, x, n, head, body, sq, ka, nullptr, stream);
@@ -1146,6 +1271,11 @@ int fn_device_count(void) {
 int fn_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* body, void* sq,
            const double* ka, void* stream) {
     return fnb::run(op, dim, dtype, x, n, head, body, sq, ka, stream);
+}
+
+int fn_run_many(int op, int dim, int dtype, int nseg, const void* const* xs, const int64_t* ns, void* const* heads,
+                void* const* bodies, void* const* extras, const double* ka, void* stream) {
+    return fnb::run_many(op, dim, dtype, nseg, xs, ns, heads, bodies, extras, ka, stream);
 }
 
 int fn_run_ld(int op, int dim, int dtype, const void* x, int64_t n, int64_t ldx, void* head, void* body,

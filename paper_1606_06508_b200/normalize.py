@@ -32,6 +32,8 @@ __all__ = [
     "norm2",
     "norm3",
     "norm4",
+    "normalize_many",
+    "norm_many",
 ]
 
 
@@ -143,3 +145,30 @@ def norm3(p: FpParams, *xs, out=None):
 def norm4(p: FpParams, *xs, out=None):
     """Length only; identical to ``normalize4(...).length`` bit for bit."""
     return _norm(p, 4, xs, out)
+
+
+def normalize_many(p: FpParams, xs, out=None) -> list:
+    """``normalize{n}`` over several independent ``[N_j, n]`` arrays at once (n from the
+    first array): a list of NormalizeOutcome, bit-identical to calling ``normalize{n}`` on
+    each.  CUDA tensors go to the device in one launch (fn_run_many), so a stream of small
+    batches pays one launch ramp and tail instead of one per batch.  ``out``: optional
+    list of ``(length, unit)`` pairs."""
+    xs = list(xs)
+    if not xs:
+        return []
+    check_precision(p, xs[0])
+    dim = int(xs[0].shape[1])
+    outs = None if out is None else [tuple(o) for o in out]
+    return [NormalizeOutcome(r.head, r.body)
+            for r in batch.run_many(_lib.OP_NORMALIZE, dim, xs, kernel_args_array(p), outs)]
+
+
+def norm_many(p: FpParams, xs, out=None) -> list:
+    """``norm{n}`` over several independent arrays at once (see ``normalize_many``)."""
+    xs = list(xs)
+    if not xs:
+        return []
+    check_precision(p, xs[0])
+    dim = int(xs[0].shape[1])
+    outs = None if out is None else [(o,) for o in out]
+    return [r.head for r in batch.run_many(_lib.OP_NORM, dim, xs, kernel_args_array(p), outs)]

@@ -302,6 +302,45 @@ def test_host_padded_records(cuda_dev, prec, n, pinned):
     assert oracle.same(got.length.numpy(), h).all() and oracle.same(got.unit.numpy(), b).all()
 
 
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_run_many_segments(cuda_dev, prec):
+    """fn_run_many: every family over a list of arrays of mixed sizes (empty, one row,
+    around the tile, large), one of them off the 16-byte grid (launched on its own), and
+    60 arrays (two launches of at most 48) equals one call per array bit for bit."""
+    from paper_1606_06508_b200 import batch
+
+    single = prec == "f32"
+    ka = np.array(fn.kernel_args(fn.preset(PREC[prec])))
+    sizes = [0, 1, 255, 256, 257, 511, 513, 5000, 100_003]
+    for dim in (2, 3, 4):
+        xs = [torch.from_numpy(_random_rows(n, dim, single, seed=n + dim)).to(cuda_dev) for n in sizes]
+        big = torch.from_numpy(_random_rows(3001, dim, single, seed=99)).to(cuda_dev)
+        xs.append(big[1:])  # off the 16-byte grid for dim 3 (and f32 dim 2)
+        ops = [OPS[f] for f in FAMILIES[dim]] + [_lib.OP_NORMALIZE_SQ]
+        for op in ops:
+            k = ka if op in (_lib.OP_SCALE, _lib.OP_NORMALIZE, _lib.OP_NORM, _lib.OP_NORMALIZE_SQ) else None
+            got = batch.run_many(op, dim, xs, k)
+            for x, g in zip(xs, got):
+                want = batch.run(op, dim, x, k)
+                for a, b in ((g.head, want.head), (g.body, want.body), (g.sq, want.sq)):
+                    if b is not None:
+                        assert oracle.same(a.cpu().numpy(), b.cpu().numpy()).all(), (prec, dim, op, x.shape)
+    # more arrays than one launch holds, through the public API
+    p = fn.preset(PREC[prec])
+    xs = [torch.from_numpy(_random_rows(300 + 37 * j, 3, single, seed=j)).to(cuda_dev) for j in range(60)]
+    outs = fn.normalize_many(p, xs)
+    lens = fn.norm_many(p, xs)
+    for x, o, r in zip(xs, outs, lens):
+        w = fn.normalize3(p, x)
+        assert oracle.same(o.length.cpu().numpy(), w.length.cpu().numpy()).all()
+        assert oracle.same(o.unit.cpu().numpy(), w.unit.cpu().numpy()).all()
+        assert oracle.same(r.cpu().numpy(), w.length.cpu().numpy()).all()
+    # host arrays fall back to one host-path call each
+    hs = [x.cpu().numpy() for x in xs[:3]]
+    for h, o in zip(hs, fn.normalize_many(p, hs)):
+        assert oracle.same(o.unit, fn.normalize3(p, h).unit).all()
+
+
 def test_norm_equals_normalize_length(cuda_dev):
     for prec, dt in (("double", torch.float64), ("single", torch.float32)):
         p = fn.preset(prec)
