@@ -99,9 +99,19 @@ def _torch():
     return torch
 
 
+_torch_types: set = set()  # tensor classes seen so far (the check runs several times per call)
+
+
 def is_torch(x) -> bool:
     t = type(x)
-    return t.__module__.startswith("torch") and t.__name__ in ("Tensor", "Parameter")
+    if t in _torch_types:
+        return True
+    if t is np.ndarray:
+        return False
+    if t.__module__.startswith("torch") and t.__name__ in ("Tensor", "Parameter"):
+        _torch_types.add(t)
+        return True
+    return False
 
 
 def is_array(x) -> bool:
@@ -185,7 +195,16 @@ def _ka_address(ka_arr: np.ndarray) -> int:
 
 
 _stream_of = None
+_device_of = None
 _dcode_of: dict = {}
+
+
+def _current_device(torch) -> int:
+    """torch's current CUDA device (the cheap private accessor when present)."""
+    global _device_of
+    if _device_of is None:
+        _device_of = getattr(torch._C, "_cuda_getDevice", None) or torch.cuda.current_device
+    return _device_of()
 
 
 def _cuda_stream(torch, dev: int) -> int:
@@ -211,6 +230,36 @@ def _overlaps(x, n: int, ldx: int, dim: int, outs) -> bool:
     return False
 
 
+def _run_device_out(op, dim, x, n, ka_arr, out, w0, w1, w2):
+    """The common device call -- dense CUDA rows on torch's current device, valid
+    preallocated outputs, a non-rotation op -- with no further checks; None when any
+    condition fails (the general path then handles the call, including its errors)."""
+    fast = _fast_run()
+    if fast is None or not x.is_cuda or not x.is_contiguous() or op > _lib.OP_NORMALIZE_SQ:
+        return None
+    dt, dev = x.dtype, x.device
+    outs = tuple(out)
+    if len(outs) != 1 + (w1 > 0) + (w2 > 0):
+        return None
+    for o, w in zip(outs, (w0,) + ((w1,) if w1 else ()) + ((w2,) if w2 else ())):
+        if type(o) not in _torch_types or o.dtype is not dt or o.device != dev or not o.is_contiguous() \
+                or o.shape != _shape(n, w):
+            return None
+    torch = _torch()
+    if _current_device(torch) != dev.index:
+        return None
+    dcode = _dcode_of.get(dt)
+    if dcode is None:
+        return None
+    head, body, extra = outs[0], outs[1] if w1 else None, outs[-1] if w2 else None
+    rc = fast.run(op, dim, dcode, x.data_ptr(), n, head.data_ptr(), None if body is None else body.data_ptr(),
+                  None if extra is None else extra.data_ptr(), None if ka_arr is None else _ka_address(ka_arr),
+                  _cuda_stream(torch, dev.index))
+    if rc:
+        _lib.check(rc, "fn_run")
+    return BatchOut(head, body, extra)
+
+
 def run(op: int, dim: int, x, ka_arr: np.ndarray | None, out=None, invalid=None) -> BatchOut:
     """Run kernel family ``op`` over rows ``x[N, dim]``; return (head, body, extra).
 
@@ -220,6 +269,10 @@ def run(op: int, dim: int, x, ka_arr: np.ndarray | None, out=None, invalid=None)
         raise ValueError(f"expected rows of shape [N, {dim}], got {tuple(x.shape)}")
     w0, w1, w2 = widths(op, dim)
     n = int(x.shape[0])
+    if out is not None and invalid is None and type(x) in _torch_types:
+        res = _run_device_out(op, dim, x, n, ka_arr, out, w0, w1, w2)
+        if res is not None:
+            return res
     L = _lib.lib()
     kptr = None if ka_arr is None else _ka_address(ka_arr)
     outs = tuple(out) if out is not None else ()
@@ -260,7 +313,7 @@ def run(op: int, dim: int, x, ka_arr: np.ndarray | None, out=None, invalid=None)
             dev = x.device.index
             # The library launches on the thread's current CUDA device (shared with torch
             # through the driver's current context): switch only when x lives elsewhere.
-            switch = torch.cuda.current_device() != dev
+            switch = _current_device(torch) != dev
             if switch:
                 ctx = torch.cuda.device(dev)
                 ctx.__enter__()
