@@ -45,6 +45,8 @@ METRIC = "normalized vectors/sec and achieved HBM GB/s vs peak (3D fp64), 1/2/4/
 UNIT = "vectors/s"
 CFG = 5
 ROWS_TOTAL = 1 << 30
+WORKLOAD = ("cfg5: 3D f64 normalize3 (scaling algorithm), N=2^30 rows total, "
+            "exponents U[-1020,1020], 0.5% near-DBL_MAX rows, 0.5% all-subnormal rows")
 DIM = 3
 BYTES_PER_ROW = 56  # 24 in + 8 (r) + 24 (unit)
 CPU_SAMPLE_ROWS = 1 << 26
@@ -331,8 +333,9 @@ def run_reference_arm(args):
         "ms_per_step": 1e3 * t_total / max(1, args.steps),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded cfg5 generator, host restatement)",
-        "config": {"workload": "cfg5: 3D f64 normalize (scaling), bounded CPU sample",
-                   "rows_sampled": CPU_SAMPLE_ROWS},
+        "config": {"workload": WORKLOAD, "rows_total": ROWS_TOTAL,
+                   "rows_sampled": CPU_SAMPLE_ROWS,
+                   "sample": "each step: a bounded CPU sample of the workload (rows_sampled rows)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -617,8 +620,7 @@ def run_ours(args):
         "dtype": "f64",
         "data": "synthetic (seeded cfg5 generator in HBM; BASELINE.json configs[4])",
         "config": {
-            "workload": "cfg5: 3D f64 normalize3 (scaling algorithm), N=2^30 rows total, "
-                        "exponents U[-1020,1020], 0.5% near-DBL_MAX rows, 0.5% all-subnormal rows",
+            "workload": WORKLOAD,
             "rows_total": ROWS_TOTAL,
             "rows_per_gpu": rows_rank0,
             "bytes_per_row": BYTES_PER_ROW,
