@@ -13,8 +13,9 @@
 //     tiles in one bulk group; `wait_group.read 1` right after the commit guarantees
 //     that the staging tile written two iterations later has been drained.
 // Every HBM byte is touched exactly once, in 16-byte-aligned bulk transactions.
-// Rows past the last full tile (and arrays that are not 16-byte aligned) use a plain
-// thread-per-row kernel with the same row arithmetic.
+// Rows past the last full tile, outputs that are not 16-byte aligned and irregular row
+// strides use a plain thread-per-row kernel with the same row arithmetic; inputs off the
+// 16-byte grid take the MIS instantiation (each tile loaded from the boundary below it).
 #pragma once
 #include <cuda_runtime.h>
 
