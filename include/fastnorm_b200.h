@@ -127,6 +127,10 @@ int fn_host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head
  * as the AoS kernels, bit for bit.  Ops SCALE..NORMALIZE_SQ, both dtypes. */
 int fn_run_soa(int op, int dim, int dtype, const void* const* xs, int64_t n, void* head,
                void* const* body, void* sq, const double* ka, void* stream);
+/* fn_run_soa for host component arrays: the host pipeline of fn_host_run (page-locked
+ * arrays DMA'd directly, pageable ones staged by the parallel copier), synchronous. */
+int fn_host_run_soa(int op, int dim, int dtype, const void* const* xs, int64_t n, void* head,
+                    void* const* body, void* sq, const double* ka);
 /* Page-locked (portable) host memory for fn_host_run / fn_host_run_multi callers: buffers
  * from here are DMA'd directly instead of through the library's staging copies
  * (1.56 vs 0.64 Gvec/s for 3-D f64 rows).  No reference analogue (the reference is CPU

@@ -516,13 +516,45 @@ def _columns_of_records(xs, dim: int):
     return np.lib.stride_tricks.as_strided(x0, shape=(len(x0), dim), strides=(st, es), writeable=False)
 
 
+def _run_soa_host(op: int, dim: int, xs, ka_arr: np.ndarray | None):
+    """Host component arrays (numpy or CPU tensors) through fn_host_run_soa: the chunked
+    host pipeline, no torch transfers.  Outputs are arrays of the inputs' kind."""
+    import ctypes
+
+    as_tensor = is_torch(xs[0])
+    arrs = [np.ascontiguousarray(v.numpy() if is_torch(v) else np.asarray(v)) for v in xs]
+    n = arrs[0].shape[0]
+    dt = arrs[0].dtype
+    if any(a.dtype != dt or a.ndim != 1 for a in arrs):
+        raise TypeError("component arrays must be 1-D and share a dtype")
+    dcode = _dtype_code(str(dt))
+    w0, w1, w2 = widths(op, dim)
+    head = np.empty(n, dtype=dt)
+    body = [np.empty(n, dtype=dt) for _ in range(dim)] if w1 else None
+    extra = np.empty(n, dtype=dt) if w2 else None
+    xp = (ctypes.c_void_p * dim)(*[a.ctypes.data for a in arrs])
+    bp = (ctypes.c_void_p * dim)(*[b.ctypes.data for b in body]) if body else None
+    kptr = None if ka_arr is None else _ka_address(ka_arr)
+    rc = _lib.lib().fn_host_run_soa(op, dim, dcode, ctypes.addressof(xp), n, head.ctypes.data,
+                                    None if bp is None else ctypes.addressof(bp),
+                                    None if extra is None else extra.ctypes.data, kptr)
+    if rc:
+        _lib.check(rc, "fn_host_run_soa")
+    if as_tensor:
+        torch = _torch()
+        conv = torch.from_numpy
+        return conv(head), None if body is None else tuple(conv(b) for b in body), \
+            None if extra is None else conv(extra)
+    return head, None if body is None else tuple(body), extra
+
+
 def run_soa(op: int, dim: int, xs, ka_arr: np.ndarray | None):
     """Structure-of-arrays rows: component arrays xs[k][N] -> (head[N], body tuple of
     dim arrays or None, extra[N] or None), through fn_run_soa on the device.
 
-    CUDA tensors are used in place.  Host arrays (numpy, CPU tensors) are moved to the
-    current CUDA device and the results copied back by torch -- plumbing only, the
-    arithmetic runs in the kernel."""
+    CUDA tensors are used in place.  Host arrays (numpy, CPU tensors) go through the
+    host pipeline (fn_host_run_soa).  Consecutive columns of one record array run the
+    AoS kernels on the records in place."""
     import ctypes
 
     n = int(xs[0].shape[0])
@@ -535,14 +567,11 @@ def run_soa(op: int, dim: int, xs, ka_arr: np.ndarray | None):
         res = run(op, dim, aos, ka_arr)
         body = None if res.body is None else tuple(res.body[:, k] for k in range(dim))
         return res.head, body, res.sq
+    if not (is_torch(xs[0]) and xs[0].is_cuda):
+        return _run_soa_host(op, dim, xs, ka_arr)
     torch = _torch()
-    host = not (is_torch(xs[0]) and xs[0].is_cuda)
-    if host:
-        dev = torch.device("cuda", torch.cuda.current_device())
-        ts = [torch.as_tensor(v).to(dev) for v in xs]
-    else:
-        ts = [v.contiguous() for v in xs]
-        dev = ts[0].device
+    ts = [v.contiguous() for v in xs]
+    dev = ts[0].device
     dt = ts[0].dtype
     if any(t.dtype != dt or t.device != dev for t in ts):
         raise TypeError("component arrays must share dtype and device")
@@ -561,9 +590,4 @@ def run_soa(op: int, dim: int, xs, ka_arr: np.ndarray | None):
                                    _cuda_stream(torch, dev.index))
     if rc:
         _lib.check(rc, "fn_run_soa")
-    if host:
-        numpy_in = isinstance(xs[0], np.ndarray)
-        conv = (lambda t: t.cpu().numpy()) if numpy_in else (lambda t: t.cpu())
-        return conv(head), None if body is None else tuple(conv(t) for t in body), \
-            None if extra is None else conv(extra)
     return head, None if body is None else tuple(body), extra

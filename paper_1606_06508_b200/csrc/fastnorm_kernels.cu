@@ -1060,6 +1060,126 @@ int host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, v
 }
 
 // ---------------------------------------------------------------------------------
+// Host structure-of-arrays rows (fn_host_run_soa): the reference's scalar signatures
+// called with host component arrays.  The same chunked pipeline as host_run_impl --
+// per chunk, every component array goes H2D (through page-locked staging filled by the
+// parallel copier when the caller's memory is pageable), the SoA kernels run, every
+// output array comes back -- over `pipes` streams, so transfers and kernels of
+// different chunks overlap.
+// ---------------------------------------------------------------------------------
+int host_run_soa(int op, int dim, int dtype, const void* const* xs, int64_t n, void* head, void* const* body,
+                 void* sq, const double* ka) {
+    if (op < FN_OP_SCALE || op > FN_OP_NORMALIZE_SQ) return fail(FN_EINVAL, "unknown op for the SoA entry");
+    if (dim < 2 || dim > 4) return fail(FN_EINVAL, "dim must be 2, 3 or 4");
+    if (dtype != FN_F32 && dtype != FN_F64) return fail(FN_EINVAL, "dtype must be FN_F32/FN_F64");
+    if (n < 0) return fail(FN_EINVAL, "n must be >= 0");
+    if (n == 0) return FN_OK;
+    const Widths wd = op_widths(op, dim);
+    if (!xs || !head) return fail(FN_EINVAL, "xs and head must not be NULL");
+    for (int c = 0; c < dim; ++c)
+        if (!xs[c]) return fail(FN_EINVAL, "component array is NULL");
+    if (wd.w1) {
+        if (!body) return fail(FN_EINVAL, "body arrays must not be NULL");
+        for (int c = 0; c < dim; ++c)
+            if (!body[c]) return fail(FN_EINVAL, "body array is NULL");
+    }
+    if (wd.w2 && !sq) return fail(FN_EINVAL, "sq output must not be NULL");
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    const size_t w = dtype == FN_F64 ? 8 : 4;
+    // output arrays: head, body[0..dim), sq -- each one element per row
+    const int nout = 1 + (wd.w1 ? dim : 0) + (wd.w2 ? 1 : 0);
+    char* outs[6];
+    outs[0] = static_cast<char*>(head);
+    for (int c = 0; c < (wd.w1 ? dim : 0); ++c) outs[1 + c] = static_cast<char*>(body[c]);
+    if (wd.w2) outs[nout - 1] = static_cast<char*>(sq);
+    bool stage_in = false, stage_out = false;
+    for (int c = 0; c < dim; ++c) stage_in = stage_in || !is_page_locked(xs[c]);
+    for (int k = 0; k < nout; ++k) stage_out = stage_out || !is_page_locked(outs[k]);
+    const bool staged = stage_in || stage_out;
+    const int64_t row_in = (int64_t)(dim * w), in_total = n * row_in;
+    int64_t chunk_bytes;
+    if (getenv("FASTNORM_B200_HOST_CHUNK_MB")) {
+        chunk_bytes = (int64_t)env_int("FASTNORM_B200_HOST_CHUNK_MB", 48, 1, 1024) << 20;
+    } else if (staged) {
+        chunk_bytes = std::max<int64_t>((int64_t)8 << 20, std::min<int64_t>((int64_t)16 << 20, in_total / 3));
+    } else {
+        chunk_bytes = std::max<int64_t>((int64_t)4 << 20, std::min<int64_t>((int64_t)48 << 20, in_total / 8));
+    }
+    const int64_t rows = std::min<int64_t>(n, std::max<int64_t>(4096, chunk_bytes / row_in));
+    const size_t arr = align256(rows * w);  // one array's chunk
+    const size_t per_pipe = arr * (size_t)(dim + nout);
+    std::lock_guard<std::mutex> lk(device_mutex(dev));
+    Staging* st = nullptr;
+    int rc = staging_get(dev, per_pipe, &st);
+    if (rc != FN_OK) return rc;
+    if (staged) {
+        rc = host_staging_get(st, per_pipe);
+        if (rc != FN_OK) return rc;
+    }
+    struct Pending {
+        bool live = false;
+        int64_t r0 = 0, m = 0;
+    } pending[Staging::kMaxPipes];
+    auto drain = [&](int p) -> int {
+        if (!pending[p].live) return FN_OK;
+        cudaError_t ee = cudaEventSynchronize(st->done[p]);
+        if (ee != cudaSuccess) return cuda_fail(ee, "cudaEventSynchronize");
+        if (stage_out) {
+            const char* hb = static_cast<const char*>(st->hbuf[p]);
+            for (int k = 0; k < nout; ++k)
+                copy_pool().copy(outs[k] + pending[p].r0 * w, hb + (size_t)(dim + k) * arr, pending[p].m * w);
+        }
+        pending[p].live = false;
+        return FN_OK;
+    };
+    int64_t chunk = 0;
+    for (int64_t r0 = 0; r0 < n; r0 += rows, ++chunk) {
+        const int p = (int)(chunk % st->pipes);
+        const int64_t m = std::min<int64_t>(rows, n - r0);
+        cudaStream_t s = st->streams[p];
+        rc = drain(p);
+        if (rc != FN_OK) return rc;
+        char* base = static_cast<char*>(st->buf[p]);
+        char* hbase = static_cast<char*>(st->hbuf[p]);
+        const void* dx[4];
+        for (int c = 0; c < dim; ++c) {
+            const char* src = static_cast<const char*>(xs[c]) + r0 * w;
+            if (stage_in) {
+                copy_pool().copy(hbase + (size_t)c * arr, src, m * w);
+                src = hbase + (size_t)c * arr;
+            }
+            e = cudaMemcpyAsync(base + (size_t)c * arr, src, m * w, cudaMemcpyHostToDevice, s);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync H2D");
+            dx[c] = base + (size_t)c * arr;
+        }
+        void* dout[6];
+        for (int k = 0; k < nout; ++k) dout[k] = base + (size_t)(dim + k) * arr;
+        rc = run_soa(op, dim, dtype, dx, m, dout[0], wd.w1 ? &dout[1] : nullptr, wd.w2 ? dout[nout - 1] : nullptr, ka,
+                     s);
+        if (rc != FN_OK) return rc;
+        for (int k = 0; k < nout && e == cudaSuccess; ++k) {
+            char* dst = stage_out ? hbase + (size_t)(dim + k) * arr : outs[k] + r0 * w;
+            e = cudaMemcpyAsync(dst, dout[k], m * w, cudaMemcpyDeviceToHost, s);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync D2H");
+        e = cudaEventRecord(st->done[p], s);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+        pending[p] = {true, r0, m};
+    }
+    for (int64_t c = std::max<int64_t>(0, chunk - st->pipes); c < chunk; ++c) {
+        rc = drain((int)(c % st->pipes));
+        if (rc != FN_OK) return rc;
+    }
+    for (int p = 0; p < st->pipes; ++p) {
+        e = cudaStreamSynchronize(st->streams[p]);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+    }
+    return FN_OK;
+}
+
+// ---------------------------------------------------------------------------------
 // One row, low latency (the reference's scalar signatures).  The row travels inside the
 // kernel's parameter block (no device read of host memory); one thread computes it with
 // the same RowOp as the batched kernels, stores the results into a per-thread,
@@ -1332,6 +1452,11 @@ int fn_host_run_multi_ld(int op, int dim, int dtype, const void* x, int64_t n, i
                          void* body, void* sq, const double* ka, const int* devices, int ndev) {
     if (ldx < 1) return fnb::set_error(FN_EINVAL, "ldx must be >= dim");
     return fnb::host_run_multi(op, dim, dtype, x, n, head, body, sq, ka, devices, ndev, ldx);
+}
+
+int fn_host_run_soa(int op, int dim, int dtype, const void* const* xs, int64_t n, void* head, void* const* body,
+                    void* sq, const double* ka) {
+    return fnb::host_run_soa(op, dim, dtype, xs, n, head, body, sq, ka);
 }
 
 int fn_run_soa(int op, int dim, int dtype, const void* const* xs, int64_t n, void* head,

@@ -820,6 +820,34 @@ def test_structure_of_arrays_misaligned_bulk_path(cuda_dev, prec):
                         assert oracle.same(a.cpu().numpy(), b.cpu().numpy()).all(), (prec, dim, n, name)
 
 
+@pytest.mark.parametrize("pinned", [False, True])
+def test_structure_of_arrays_host_pipeline(cuda_dev, pinned):
+    """Host component arrays through fn_host_run_soa (several pipeline chunks, pageable or
+    page-locked, numpy and CPU tensors, both precisions): the AoS results bit for bit."""
+    for prec, single in (("double", False), ("single", True)):
+        p = fn.preset(prec)
+        n = 3_000_001
+        x = _random_rows(n, 3, single, seed=31 + single)
+        comps = []
+        for k in range(3):
+            a = fn.host_empty((n,), dtype=x.dtype) if pinned else np.empty(n, dtype=x.dtype)
+            a[:] = x[:, k]
+            comps.append(a)
+        want = fn.normalize3(p, torch.from_numpy(x).to(cuda_dev))
+        wl, wu = want.length.cpu().numpy(), want.unit.cpu().numpy()
+        got = fn.normalize3(p, *comps)
+        assert oracle.same(got.length, wl).all()
+        assert all(oracle.same(got.unit[k], wu[:, k]).all() for k in range(3))
+        sq = fn.normalize3_sq(p, *comps)
+        assert oracle.same(sq.length, wl).all()
+        assert oracle.same(fn.norm3(p, *comps), wl).all()
+        sc = fn.scale3(p, *comps)
+        wsc = fn.scale3(p, torch.from_numpy(x).to(cuda_dev))
+        assert oracle.same(sc.inv_sigma, wsc.inv_sigma.cpu().numpy()).all()
+        t = fn.normalize3(p, *[torch.from_numpy(c) for c in comps])  # CPU tensors
+        assert isinstance(t.length, torch.Tensor) and oracle.same(t.length.numpy(), wl).all()
+
+
 def test_structure_of_arrays_unaligned_and_tails(cuda_dev):
     """Component arrays at an 8-byte offset (scalar SoA kernel) and lengths that leave a
     partial 16-byte vector (vector kernel + scalar tail) give the AoS results."""
