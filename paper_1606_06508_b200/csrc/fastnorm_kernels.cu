@@ -1067,6 +1067,44 @@ int host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, v
 // output array comes back -- over `pipes` streams, so transfers and kernels of
 // different chunks overlap.
 // ---------------------------------------------------------------------------------
+// Small host SoA batches: the zero-copy route of host_run_small (components copied into
+// a per-thread page-locked buffer mapped into the device, the per-row SoA kernel run on
+// it in place, one synchronisation, results copied out).
+static int host_run_soa_small(int op, int dim, int dtype, const void* const* xs, int64_t n, char* const* outs,
+                              int nout, bool has_body, bool has_sq, const double* ka, int dev) {
+    static thread_local std::vector<SmallCtx> ctxs;
+    if ((int)ctxs.size() <= dev) ctxs.resize(dev + 1);
+    SmallCtx& c = ctxs[dev];
+    cudaError_t e;
+    if (c.dev < 0) {
+        e = cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
+        e = cudaHostAlloc(reinterpret_cast<void**>(&c.host), kSmallHostBytes + 16 * 256, cudaHostAllocMapped);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaHostAlloc");
+        e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c.dptr), c.host, 0);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaHostGetDevicePointer");
+        c.dev = dev;
+    }
+    const size_t w = dtype == FN_F64 ? 8 : 4;
+    const size_t arr = align256(n * w);
+    const void* dx[4];
+    for (int k = 0; k < dim; ++k) {
+        memcpy(c.host + k * arr, xs[k], n * w);
+        dx[k] = c.dptr + k * arr;
+    }
+    void* dout[6];
+    for (int k = 0; k < nout; ++k) dout[k] = c.dptr + (dim + k) * arr;
+    tl_direct = true;
+    const int rc = run_soa(op, dim, dtype, dx, n, dout[0], has_body ? &dout[1] : nullptr,
+                           has_sq ? dout[nout - 1] : nullptr, ka, c.stream);
+    tl_direct = false;
+    if (rc != FN_OK) return rc;
+    e = cudaStreamSynchronize(c.stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+    for (int k = 0; k < nout; ++k) memcpy(outs[k], c.host + (dim + k) * arr, n * w);
+    return FN_OK;
+}
+
 int host_run_soa(int op, int dim, int dtype, const void* const* xs, int64_t n, void* head, void* const* body,
                  void* sq, const double* ka) {
     if (op < FN_OP_SCALE || op > FN_OP_NORMALIZE_SQ) return fail(FN_EINVAL, "unknown op for the SoA entry");
@@ -1094,6 +1132,8 @@ int host_run_soa(int op, int dim, int dtype, const void* const* xs, int64_t n, v
     outs[0] = static_cast<char*>(head);
     for (int c = 0; c < (wd.w1 ? dim : 0); ++c) outs[1 + c] = static_cast<char*>(body[c]);
     if (wd.w2) outs[nout - 1] = static_cast<char*>(sq);
+    if ((size_t)(dim + nout) * align256(n * w) <= kSmallHostBytes && env_int("FASTNORM_B200_HOST_SMALL", 1, 0, 1))
+        return host_run_soa_small(op, dim, dtype, xs, n, outs, nout, wd.w1 != 0, wd.w2 != 0, ka, dev);
     bool stage_in = false, stage_out = false;
     for (int c = 0; c < dim; ++c) stage_in = stage_in || !is_page_locked(xs[c]);
     for (int k = 0; k < nout; ++k) stage_out = stage_out || !is_page_locked(outs[k]);

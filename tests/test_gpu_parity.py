@@ -846,6 +846,13 @@ def test_structure_of_arrays_host_pipeline(cuda_dev, pinned):
         assert oracle.same(sc.inv_sigma, wsc.inv_sigma.cpu().numpy()).all()
         t = fn.normalize3(p, *[torch.from_numpy(c) for c in comps])  # CPU tensors
         assert isinstance(t.length, torch.Tensor) and oracle.same(t.length.numpy(), wl).all()
+        for m in (1, 100, 5000):  # the zero-copy route for small batches
+            sub = [np.ascontiguousarray(c[:m]) for c in comps]
+            got = fn.normalize3(p, *sub)
+            assert oracle.same(got.length, wl[:m]).all()
+            assert all(oracle.same(got.unit[k], wu[:m, k]).all() for k in range(3))
+            q = fn.normalize3_sq(p, *sub)
+            assert oracle.same(q.length, wl[:m]).all() and oracle.same(q.squared_length, sq.squared_length[:m]).all()
 
 
 def test_structure_of_arrays_unaligned_and_tails(cuda_dev):
