@@ -1,4 +1,16 @@
-import cProfile, pstats, time, torch, paper_1606_06508_b200 as fn
+"""Host cost of one public device call, fn.normalize3(p, X, out=(r, u)) on 1000 rows:
+microseconds per call over 20000 calls, then a cProfile of the same loop."""
+import cProfile
+import os
+import pstats
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+import torch  # noqa: E402
+
+import paper_1606_06508_b200 as fn  # noqa: E402
+
 p = fn.preset("double")
 X = torch.zeros((1000, 3), dtype=torch.float64, device="cuda")
 r = torch.empty(1000, dtype=torch.float64, device="cuda"); u = torch.empty((1000, 3), dtype=torch.float64, device="cuda")
