@@ -27,6 +27,28 @@ import numpy as np
 from paper_1606_06508_b200 import _lib
 
 
+class _Rows:
+    """Default of the trailing components ``x2..xn`` in the public wrappers.  The
+    reference's parameters (``normalize3(p, x1, x2, x3)``, normalize.py:58) keep their
+    names and order; leaving ``x2..xn`` out is the batched overload, where ``x1`` is an
+    ``[N, n]`` array of rows."""
+
+    __slots__ = ()
+
+    def __repr__(self) -> str:
+        return "ROWS"
+
+
+ROWS = _Rows()
+
+
+def components(*xs) -> tuple:
+    """The components a wrapper was called with (``x1`` alone for one row array)."""
+    if xs[-1] is not ROWS:
+        return xs
+    return tuple(v for v in xs if v is not ROWS)
+
+
 def widths(op: int, dim: int) -> tuple[int, int, int]:
     """Elements per row of the (head, body, extra) outputs of a kernel family."""
     if op == _lib.OP_NORM:

@@ -28,6 +28,7 @@ import csv
 import hashlib
 import io
 import json
+import math
 import platform
 import statistics
 from dataclasses import asdict, dataclass, field
@@ -39,7 +40,7 @@ from paper_1606_06508_b200.params import preset
 from paper_1606_06508_b200.scale import kernel_args_array
 
 __all__ = ["REGIMES", "BenchConfig", "BenchConfigError", "BenchRow", "RatioRow", "BenchReport",
-           "generate_inputs", "run_bench"]
+           "generate_inputs", "generate_regime_rows", "run_bench"]
 
 REGIMES = workloads.REGIMES
 _PREC_DTYPE = {"double": "float64", "single": "float32"}
@@ -118,12 +119,63 @@ class BenchReport:
         return buf.getvalue()
 
 
-def generate_inputs(regime: str, dimension: int, precision: str, count: int, seed=0) -> np.ndarray:
-    """A deterministic ``(count, dimension)`` host batch of the reference regimes
-    (bench.py:146-207): ``normal``, ``subnormal``, ``huge``, ``mixed``, ``unit-ish``.
-    Drawn by the counter-based generator the device uses (workloads.regime_rows), so
-    the same seed gives the same rows on the host and in HBM; ``seed`` may be an int or
-    a tuple of ints."""
+# Binade exponents per format: least subnormal, least normal, largest (bench.py:49).
+_BINADES = {"double": (-1074, -1022, 1023), "single": (-149, -126, 127)}
+
+
+def generate_inputs(regime: str, dimension: int, precision: str, count: int, seed) -> np.ndarray:
+    """The reference's deterministic ``(count, dimension)`` host batch of nonzero finite
+    vectors, bit for bit (bench.py:146-207): the same PCG64 stream seeded through
+    ``SeedSequence(seed)`` (``seed``: an int or a tuple of ints), drawn in the same order
+    (signs, mantissas, then the regime's exponents or normals).
+
+    ``normal``: magnitudes in [tau_min, tau_max]; ``subnormal``: in [alpha, nu);
+    ``huge``: above tau_max; ``mixed``: exponents uniform over the whole range,
+    subnormals included; ``unit-ish``: norms within 2^-10 of one.
+
+    The GPU ratio harness (:func:`run_bench`) draws its HBM-sized batches with the
+    counter generator instead (:func:`generate_regime_rows`), which any shard or device
+    reproduces without drawing the rows before it."""
+    if regime not in REGIMES:
+        raise ValueError(f"unknown regime {regime!r}; choices: {REGIMES}")
+    if dimension not in (2, 3, 4):
+        raise ValueError(f"dimension must be 2, 3 or 4, got {dimension}")
+    if precision not in _PREC_DTYPE:
+        raise ValueError(f"unknown precision {precision!r}")
+    if count <= 0:
+        raise ValueError("count must be positive")
+    gen = np.random.Generator(np.random.PCG64(np.random.SeedSequence(seed)))
+    fmt = preset(precision)
+    dtype = np.dtype(_PREC_DTYPE[precision])
+    least_sub, least_normal, top = _BINADES[precision]
+    lo_band, hi_band = int(math.log2(fmt.tau_min)), int(math.log2(fmt.tau_max))
+    shape = (count, dimension)
+    signs = 2.0 * gen.integers(0, 2, size=shape).astype(np.float64) - 1.0
+    mantissas = gen.random(shape) + 1.0
+    if regime == "unit-ish":
+        g = gen.standard_normal(shape)
+        lengths = np.sqrt(np.sum(g * g, axis=1, keepdims=True))
+        g[:, 0] = np.where(lengths[:, 0] == 0.0, 1.0, g[:, 0])
+        lengths = np.maximum(lengths, np.finfo(np.float64).tiny)
+        stretch = 1.0 + (2.0 * gen.random((count, 1)) - 1.0) * 2.0 ** -10
+        return np.ascontiguousarray(((g / lengths) * stretch).astype(dtype))
+    exp_range = {"normal": (lo_band, hi_band), "subnormal": (least_sub, least_normal),
+                 "huge": (hi_band + 1, top - 1), "mixed": (least_sub, top)}[regime]
+    mags = np.ldexp(mantissas, gen.integers(*exp_range, size=shape))
+    if regime == "subnormal":  # rounding can lift the top of the range onto nu
+        mags = np.minimum(mags, fmt.nu - fmt.alpha)
+    vals = (mags * signs).astype(dtype)
+    if regime == "subnormal" and precision == "single":
+        cap = np.float32(fmt.nu - fmt.alpha)
+        np.clip(vals, -cap, cap, out=vals)
+    return np.ascontiguousarray(vals)
+
+
+def generate_regime_rows(regime: str, dimension: int, precision: str, count: int, seed=0) -> np.ndarray:
+    """Rows of a reference regime from the counter generator the device uses
+    (workloads.regime_rows): the same seed gives the same rows on the host and in HBM,
+    and any row range can be drawn alone.  Not the reference's stream -- that is
+    :func:`generate_inputs`."""
     if regime not in REGIMES:
         raise ValueError(f"unknown regime {regime!r}; choices: {REGIMES}")
     if dimension not in (2, 3, 4):

@@ -1,8 +1,10 @@
 """Scaling normalization (reference: pkg/src/fastnorm/normalize.py).
 
 Scalar calls keep the reference signatures (``normalize3(p, x1, x2, x3)`` ->
-``NormalizeOutcome(length, unit)``, normalize.py:51-89).  Passing one ``[N, n]`` array
-(CUDA tensor: device path; numpy / CPU tensor: host path) selects the batched overload,
+``NormalizeOutcome(length, unit)``, normalize.py:51-89): same parameter names, order and
+annotations, so keyword calls work.  Passing one ``[N, n]`` array as ``x1`` and leaving
+``x2..xn`` out (their default is the ``ROWS`` marker) selects the batched overload (CUDA
+tensor: device path; numpy / CPU tensor: host path),
 which returns ``NormalizeOutcome(length=[N], unit=[N, n])`` computed by the B200 kernel
 bit-identically to the reference (Appendix A of SURVEY.md).  ``out=(length, unit)``
 writes into preallocated arrays.
@@ -17,6 +19,7 @@ from __future__ import annotations
 from typing import Any, NamedTuple
 
 from paper_1606_06508_b200 import _backend, _lib, batch
+from paper_1606_06508_b200.batch import ROWS, components
 from paper_1606_06508_b200.params import FpParams
 from paper_1606_06508_b200.scale import check_precision, kernel_args, kernel_args_array
 
@@ -102,49 +105,53 @@ def _norm(p: FpParams, dim: int, xs, out):
     return k(*kernel_args(p), *_scalars(f"norm{dim}", dim, xs))
 
 
-def normalize2(p: FpParams, *xs, out=None) -> NormalizeOutcome:
+def normalize2(p: FpParams, x1: float, x2: float = ROWS, *, out=None) -> NormalizeOutcome:
     """Length and unit direction of a 2-vector; zero input gives (0, (0, 0))."""
-    return _normalize(p, 2, xs, out)
+    return _normalize(p, 2, components(x1, x2), out)
 
 
-def normalize3(p: FpParams, *xs, out=None) -> NormalizeOutcome:
+def normalize3(p: FpParams, x1: float, x2: float = ROWS, x3: float = ROWS, *, out=None) -> NormalizeOutcome:
     """Length and unit direction of a 3-vector; zero input gives (0, (0, 0, 0))."""
-    return _normalize(p, 3, xs, out)
+    return _normalize(p, 3, components(x1, x2, x3), out)
 
 
-def normalize4(p: FpParams, *xs, out=None) -> NormalizeOutcome:
+def normalize4(p: FpParams, x1: float, x2: float = ROWS, x3: float = ROWS, x4: float = ROWS, *,
+               out=None) -> NormalizeOutcome:
     """Length and unit quaternion; the zero quaternion maps to (0, (0, 0, 0, 1))."""
-    return _normalize(p, 4, xs, out)
+    return _normalize(p, 4, components(x1, x2, x3, x4), out)
 
 
-def normalize2_sq(p: FpParams, *xs, out=None) -> NormalizeSqOutcome:
+def normalize2_sq(p: FpParams, x1: float, x2: float = ROWS, *, out=None) -> NormalizeSqOutcome:
     """normalize2 plus the squared length; ``out=(squared_length, length, unit)``."""
-    return _normalize_sq(p, 2, xs, out)
+    return _normalize_sq(p, 2, components(x1, x2), out)
 
 
-def normalize3_sq(p: FpParams, *xs, out=None) -> NormalizeSqOutcome:
+def normalize3_sq(p: FpParams, x1: float, x2: float = ROWS, x3: float = ROWS, *,
+                  out=None) -> NormalizeSqOutcome:
     """normalize3 plus the squared length; ``out=(squared_length, length, unit)``."""
-    return _normalize_sq(p, 3, xs, out)
+    return _normalize_sq(p, 3, components(x1, x2, x3), out)
 
 
-def normalize4_sq(p: FpParams, *xs, out=None) -> NormalizeSqOutcome:
+def normalize4_sq(p: FpParams, x1: float, x2: float = ROWS, x3: float = ROWS, x4: float = ROWS, *,
+                  out=None) -> NormalizeSqOutcome:
     """normalize4 plus the squared length (BASELINE config 3)."""
-    return _normalize_sq(p, 4, xs, out)
+    return _normalize_sq(p, 4, components(x1, x2, x3, x4), out)
 
 
-def norm2(p: FpParams, *xs, out=None):
+def norm2(p: FpParams, x1: float, x2: float = ROWS, *, out=None) -> float:
     """Length only; identical to ``normalize2(...).length`` bit for bit."""
-    return _norm(p, 2, xs, out)
+    return _norm(p, 2, components(x1, x2), out)
 
 
-def norm3(p: FpParams, *xs, out=None):
+def norm3(p: FpParams, x1: float, x2: float = ROWS, x3: float = ROWS, *, out=None) -> float:
     """Length only; identical to ``normalize3(...).length`` bit for bit."""
-    return _norm(p, 3, xs, out)
+    return _norm(p, 3, components(x1, x2, x3), out)
 
 
-def norm4(p: FpParams, *xs, out=None):
+def norm4(p: FpParams, x1: float, x2: float = ROWS, x3: float = ROWS, x4: float = ROWS, *,
+          out=None) -> float:
     """Length only; identical to ``normalize4(...).length`` bit for bit."""
-    return _norm(p, 4, xs, out)
+    return _norm(p, 4, components(x1, x2, x3, x4), out)
 
 
 def normalize_many(p: FpParams, xs, out=None) -> list:
@@ -156,7 +163,8 @@ def normalize_many(p: FpParams, xs, out=None) -> list:
     xs = list(xs)
     if not xs:
         return []
-    check_precision(p, xs[0])
+    for x in xs:  # every batch, not just the first: the kernel constants are per precision
+        check_precision(p, x)
     dim = int(xs[0].shape[1])
     outs = None if out is None else [tuple(o) for o in out]
     return [NormalizeOutcome(r.head, r.body)
@@ -168,7 +176,8 @@ def norm_many(p: FpParams, xs, out=None) -> list:
     xs = list(xs)
     if not xs:
         return []
-    check_precision(p, xs[0])
+    for x in xs:  # every batch, not just the first: the kernel constants are per precision
+        check_precision(p, x)
     dim = int(xs[0].shape[1])
     outs = None if out is None else [(o,) for o in out]
     return [r.head for r in batch.run_many(_lib.OP_NORM, dim, xs, kernel_args_array(p), outs)]

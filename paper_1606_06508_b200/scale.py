@@ -15,6 +15,7 @@ from typing import Any, NamedTuple
 import numpy as np
 
 from paper_1606_06508_b200 import _backend, _lib, batch
+from paper_1606_06508_b200.batch import ROWS, components
 from paper_1606_06508_b200.params import FpParams, require_valid
 
 __all__ = ["ScaleOutcome", "kernel_args", "scale2", "scale3", "scale4"]
@@ -63,16 +64,17 @@ def _scale(p: FpParams, dim: int, xs, out):
     return ScaleOutcome(inv, tuple(s))
 
 
-def scale2(p: FpParams, *xs, out=None) -> ScaleOutcome:
+def scale2(p: FpParams, x1: float, x2: float = ROWS, *, out=None) -> ScaleOutcome:
     """Scale a 2-vector (or [N, 2] rows) so max |x_k| lands in [tau_min, tau_max]."""
-    return _scale(p, 2, xs, out)
+    return _scale(p, 2, components(x1, x2), out)
 
 
-def scale3(p: FpParams, *xs, out=None) -> ScaleOutcome:
+def scale3(p: FpParams, x1: float, x2: float = ROWS, x3: float = ROWS, *, out=None) -> ScaleOutcome:
     """Scale a 3-vector (or [N, 3] rows) so its largest magnitude lands in the band."""
-    return _scale(p, 3, xs, out)
+    return _scale(p, 3, components(x1, x2, x3), out)
 
 
-def scale4(p: FpParams, *xs, out=None) -> ScaleOutcome:
+def scale4(p: FpParams, x1: float, x2: float = ROWS, x3: float = ROWS, x4: float = ROWS, *,
+           out=None) -> ScaleOutcome:
     """Scale a quaternion (or [N, 4] rows) so its largest magnitude lands in the band."""
-    return _scale(p, 4, xs, out)
+    return _scale(p, 4, components(x1, x2, x3, x4), out)

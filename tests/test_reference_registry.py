@@ -78,3 +78,50 @@ def test_reference_kernel_args_feed_our_abi(ref_pkg):
 
     for fmt in ("single", "double"):
         assert ref_pkg["scale"].kernel_args(ref_pkg["params"].preset(fmt)) == fn.kernel_args(fn.preset(fmt))
+
+
+_WRAPPERS = {
+    "normalize": ("normalize2", "normalize3", "normalize4", "norm2", "norm3", "norm4"),
+    "scale": ("scale2", "scale3", "scale4"),
+    "baselines": ("naive_normalize2", "naive_normalize3", "naive_normalize4", "quotient2",
+                  "quotient3_robust", "quotient3_fast", "quotient4"),
+}
+
+
+def test_public_wrapper_signatures_match_reference(ref_pkg):
+    """Every public scalar wrapper keeps the reference's parameters exactly: names, kinds,
+    order, annotations and defaults (normalize.py:51-89, scale.py:33-51,
+    baselines.py:30-76), and the same return annotation.  The only additions are the
+    ROWS default on x2..xn (leaving them out is the [N, n] overload) and keyword-only
+    ``out``."""
+    import paper_1606_06508_b200 as fn
+    from paper_1606_06508_b200.batch import ROWS
+
+    for mod, names in _WRAPPERS.items():
+        for name in names:
+            ref = inspect.signature(getattr(ref_pkg[mod], name))
+            ours = inspect.signature(getattr(fn, name))
+            assert ours.return_annotation == ref.return_annotation, name
+            rp, op = list(ref.parameters.values()), list(ours.parameters.values())
+            assert [q.name for q in op[: len(rp)]] == [q.name for q in rp], name
+            for r, o in zip(rp, op):
+                assert o.kind == r.kind and o.annotation == r.annotation, (name, r, o)
+                if r.default is inspect.Parameter.empty:
+                    # x1 (and p) stay required; x2..xn gain only the ROWS marker
+                    assert o.default is inspect.Parameter.empty or (o.default is ROWS and r.name not in ("p", "x1")), (name, o)
+                else:
+                    assert o.default == r.default and type(o.default).__mro__[-2] is type(r.default), (name, o)
+            extra = op[len(rp):]
+            assert [(q.name, q.kind, q.default) for q in extra] == [("out", inspect.Parameter.KEYWORD_ONLY, None)], name
+
+
+def test_public_wrappers_accept_reference_keyword_calls():
+    """Keyword calls written against the reference work unchanged (the GPU computes them;
+    here only the argument binding is checked)."""
+    import paper_1606_06508_b200 as fn
+
+    p = fn.preset("double")
+    inspect.signature(fn.normalize3).bind(p, x1=3.0, x2=4.0, x3=12.0)
+    inspect.signature(fn.quotient3_robust).bind(x1=1.0, x2=2.0, x3=3.0, precision="single")
+    inspect.signature(fn.scale4).bind(p, 1.0, 2.0, x3=3.0, x4=4.0)
+    inspect.signature(fn.naive_normalize2).bind(1.0, 2.0, "single")
