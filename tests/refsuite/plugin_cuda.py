@@ -36,6 +36,7 @@ if MODE != "none":
         dropin = types.ModuleType("fastnorm._kernels")
         dropin.__dict__.update({k: v for k, v in vars(_cuda_kernels).items() if not k.startswith("__")})
         dropin.BACKEND_NAME = "compiled"
+        dropin.BUILD_FLAGS = _cuda_kernels.BUILD_FLAGS  # a lazy module attribute there
         _backend._MODULES["compiled"] = dropin
         if _backend._DEFAULT != "compiled":
             raise RuntimeError("the reference's default backend is not the compiled slot")
@@ -47,3 +48,10 @@ def pytest_report_header(config):
     mods = {k: getattr(v, "BACKEND_NAME", "?") + " @ " + getattr(v, "__name__", "?")
             for k, v in _backend._MODULES.items()}
     return [f"refsuite mode: {MODE}; registry: {mods}; default: {_backend.backend_name()}"]
+
+
+def pytest_terminal_summary(terminalreporter):
+    with open("/proc/self/maps") as f:
+        libs = sorted({line.split()[-1] for line in f if line.rstrip().endswith(".so")
+                       and ("fastnorm" in line or "_kernels" in line)})
+    terminalreporter.write_line(f"refsuite mode {MODE}: libraries mapped: {libs}")
