@@ -15,6 +15,9 @@ normalize3 (scaling algorithm: r[N] and unit[N, 3]) over every rank's shard.
 * e2e    -- the same metric through the public API with HOST buffers
             (fn.normalize3(p, pinned_numpy, out=...) -> fn_host_run): every step copies
             the shard's input H2D and r + unit D2H inside the timed region.
+* e2e_default_api -- the default drop-in call, fn.normalize3(p, numpy_rows): pageable
+            input, no out= (outputs from the library's page-locked pool), each step's
+            result dropped before the next, as a caller's loop over batches does.
 * roofline -- algorithmic bytes per launch (56 B/row x rows) / mean launch duration,
             against MEASURED_PEAKS.json hbm_gbs.
 * cpu_baseline -- (rank 0, N = 1 only) the reference's own compiled timing loop
@@ -23,6 +26,10 @@ normalize3 (scaling algorithm: r[N] and unit[N, 3]) over every rank's shard.
 
 `--impl reference` times only that CPU reference path (rank 0; other ranks exit 0).
 Run: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                     [--rows R] [--dist-backend nccl|gloo]
+--gpus N > 1 without a torchrun environment launches N ranks itself (torch.distributed.run
+on 127.0.0.1) and refuses to put two NCCL ranks on one GPU.  --rows changes the total
+(default 2^30); --dist-backend gloo lets test ranks share a GPU.
 """
 
 from __future__ import annotations
@@ -47,6 +54,14 @@ CFG = 5
 ROWS_TOTAL = 1 << 30
 WORKLOAD = ("cfg5: 3D f64 normalize3 (scaling algorithm), N=2^30 rows total, "
             "exponents U[-1020,1020], 0.5% near-DBL_MAX rows, 0.5% all-subnormal rows")
+
+
+def _workload(rows: int) -> str:
+    if rows == ROWS_TOTAL:
+        return WORKLOAD
+    return WORKLOAD.replace("N=2^30 rows total", f"N={rows} rows total (--rows; BASELINE config 5 is 2^30)")
+
+
 DIM = 3
 BYTES_PER_ROW = 56  # 24 in + 8 (r) + 24 (unit)
 CPU_SAMPLE_ROWS = 1 << 26
@@ -186,6 +201,12 @@ def _dist_env():
 
 
 from paper_1606_06508_b200.multigpu import shard_range  # noqa: E402
+
+
+def _lib_handle():
+    from paper_1606_06508_b200 import _lib
+
+    return _lib.lib()
 
 
 # --------------------------------------------------------------------------------------
@@ -333,7 +354,7 @@ def run_reference_arm(args):
         "ms_per_step": 1e3 * t_total / max(1, args.steps),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded cfg5 generator, host restatement)",
-        "config": {"workload": WORKLOAD, "rows_total": ROWS_TOTAL,
+        "config": {"workload": _workload(args.rows), "rows_total": args.rows,
                    "rows_sampled": CPU_SAMPLE_ROWS,
                    "sample": "each step: a bounded CPU sample of the workload (rows_sampled rows)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
@@ -499,26 +520,35 @@ def run_ours(args):
     from paper_1606_06508_b200 import multigpu, workloads
 
     rank, world, local = _dist_env()
-    if args.gpus != world and world > 1:
+    if args.gpus != world:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    # under torchrun (RANK set) the NCCL group is created even for a single rank, so the
-    # same barrier / max-reduce / counter-reduce code runs at every N
+    ndev = torch.cuda.device_count()
+    if args.dist_backend == "nccl" and world > ndev:
+        raise SystemExit(f"{world} NCCL ranks need {world} GPUs, {ndev} visible")
+    torch.cuda.set_device(local % ndev)
+    dev = torch.device("cuda", local % ndev)
+    # under torchrun (RANK set) the process group is created even for a single rank, so
+    # the same barrier / max-reduce / counter-reduce code runs at every N.  NCCL on the
+    # B200 box; gloo (collectives on host tensors) when a test puts ranks on one GPU.
     distributed = "RANK" in os.environ and "MASTER_ADDR" in os.environ
     if distributed:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+    cdev = dev if args.dist_backend == "nccl" else torch.device("cpu")  # collective tensors live here
+    rows_total = args.rows
 
     def barrier():
         if distributed:
             dist.barrier()
 
     def max_over_ranks(v: float) -> float:
-        return multigpu.max_over_ranks(v, device=dev)
+        return multigpu.max_over_ranks(v, device=cdev)
 
     p = fn.preset("double")
     ka = fn.kernel_args(p)
-    lo, hi = shard_range(ROWS_TOTAL, rank, world)
+    lo, hi = shard_range(rows_total, rank, world)
     n = hi - lo
 
     x = torch.empty((n, DIM), dtype=torch.float64, device=dev)
@@ -544,13 +574,13 @@ def run_ours(args):
     barrier()
     torch.cuda.synchronize(dev)
     t_dev = max_over_ranks(ev0.elapsed_time(ev1) / 1e3)
-    value = ROWS_TOTAL * args.steps / t_dev
+    value = rows_total * args.steps / t_dev
     per_launch_s = t_dev / args.steps  # one kernel launch per step per rank
     achieved_gbs = (n * BYTES_PER_ROW) / per_launch_s / 1e9 if world == 1 else \
-        (ROWS_TOTAL // world * BYTES_PER_ROW) / per_launch_s / 1e9
+        (rows_total // world * BYTES_PER_ROW) / per_launch_s / 1e9
 
     # ---------------- validation counters: one small NCCL all-reduce ----------------
-    counts_h = multigpu.reduce_counts(multigpu.shard_counts_device(x, ka))
+    counts_h = multigpu.reduce_counts(multigpu.shard_counts_device(x, ka).to(cdev))
     torch.cuda.synchronize(dev)
 
     # ---------------- end to end through the public API, host buffers ----------------
@@ -560,43 +590,82 @@ def run_ours(args):
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
     e2e_rows = min(n, _host_rows_that_fit(world))
     if distributed:
-        t = torch.tensor([e2e_rows], dtype=torch.int64, device=dev)
+        t = torch.tensor([e2e_rows], dtype=torch.int64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
         e2e_rows = int(t.item())
     e2e_error = None
     numa = multigpu.numa_local(local)  # pin + copy from the GPU's own socket
     numa.__enter__()
-    try:
-        xh = torch.empty((e2e_rows, DIM), dtype=torch.float64, pin_memory=True)
-        xh.copy_(x[:e2e_rows])
-        rh = torch.empty((e2e_rows,), dtype=torch.float64, pin_memory=True)
-        uh = torch.empty((e2e_rows, DIM), dtype=torch.float64, pin_memory=True)
+    try:  # page-locked through the library (released to the OS as soon as they are dropped)
+        xn = fn.host_empty((e2e_rows, DIM))
+        torch.from_numpy(xn).copy_(x[:e2e_rows])
+        rn = fn.host_empty((e2e_rows,))
+        un = fn.host_empty((e2e_rows, DIM))
     except Exception as exc:  # pragma: no cover - host-dependent
         e2e_error = f"pinned allocation failed: {exc}"
     if distributed:  # every rank skips the e2e pass if any rank could not pin
-        flag = torch.tensor([0 if e2e_error is None else 1], dtype=torch.int64, device=dev)
+        flag = torch.tensor([0 if e2e_error is None else 1], dtype=torch.int64, device=cdev)
         dist.all_reduce(flag, op=dist.ReduceOp.MAX)
         if int(flag.item()) and e2e_error is None:
             e2e_error = "another rank could not pin its e2e buffers"
     del x, r, u
     torch.cuda.empty_cache()
     t_e2e = float("nan")
+    L = _lib_handle()
+    e2e_launches = None
     if e2e_error is None:
-        xn, rn, un = xh.numpy(), rh.numpy(), uh.numpy()
         w = min(e2e_rows, 1 << 20)
         fn.normalize3(p, xn[:w], out=(rn[:w], un[:w]))  # warm the staging pool
         barrier()
+        k0 = L.fn_launch_count()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
             fn.normalize3(p, xn, out=(rn, un))
         t1 = time.perf_counter()
+        e2e_launches = int(L.fn_launch_count() - k0)  # counted by the library itself
         barrier()
         t_e2e = max_over_ranks(t1 - t0)
-        del xh, rh, uh, xn, rn, un
+    # ---------------- end to end, the default call: fn.normalize3(p, numpy_rows) ----------------
+    # Pageable numpy input, outputs allocated by the library (page-locked pool), the result
+    # dropped after each step as a caller's loop over batches would.
+    default_api = None
+    if not args.no_default_api and e2e_error is None:
+        try:
+            del rn, un  # the caller-provided outputs go; the library allocates its own
+            xp = np.empty((e2e_rows, DIM), dtype=np.float64)  # plain pageable numpy rows
+            np.copyto(xp, xn)
+            del xn
+            res = fn.normalize3(p, xp)  # warm-up: pins the output blocks once
+            del res
+            barrier()
+            k0 = L.fn_launch_count()
+            pool0 = (fn.batch.pinned_pool.allocs, fn.batch.pinned_pool.reuses)
+            t0 = time.perf_counter()
+            for _ in range(e2e_steps):
+                res = fn.normalize3(p, xp)
+                del res
+            t1 = time.perf_counter()
+            launches_d = int(L.fn_launch_count() - k0)
+            barrier()
+            t_def = max_over_ranks(t1 - t0)
+            default_api = {
+                "value": e2e_rows * world * e2e_steps / t_def, "unit": UNIT,
+                "h2d_bytes_per_step": e2e_rows * world * DIM * 8,
+                "d2h_bytes_per_step": e2e_rows * world * (DIM + 1) * 8,
+                "rows_per_gpu": e2e_rows, "steps": e2e_steps, "ms_per_step": 1e3 * t_def / e2e_steps,
+                "api": "paper_1606_06508_b200.normalize3(p, numpy [N,3]) with pageable input and no out= "
+                       "-> fn_host_run (outputs from the library's page-locked pool)",
+                "gpu_launches": launches_d,
+                "pool_blocks_pinned_in_timed_region": fn.batch.pinned_pool.allocs - pool0[0],
+                "pool_blocks_reused_in_timed_region": fn.batch.pinned_pool.reuses - pool0[1],
+            }
+            del xp
+        except Exception as exc:  # informational: never lose the headline line
+            default_api = {"value": None, "error": str(exc)}
+    else:
+        xn = rn = un = None
     numa.__exit__(None, None, None)
     e2e_value = e2e_rows * world * e2e_steps / t_e2e if e2e_error is None else None
-    chunk_rows = (48 << 20) // (DIM * 8)
-    e2e_launches = e2e_steps * ((e2e_rows + chunk_rows - 1) // chunk_rows)
 
     if distributed:
         dist.destroy_process_group()
@@ -620,8 +689,8 @@ def run_ours(args):
         "dtype": "f64",
         "data": "synthetic (seeded cfg5 generator in HBM; BASELINE.json configs[4])",
         "config": {
-            "workload": WORKLOAD,
-            "rows_total": ROWS_TOTAL,
+            "workload": _workload(rows_total),
+            "rows_total": rows_total,
             "rows_per_gpu": rows_rank0,
             "bytes_per_row": BYTES_PER_ROW,
             "l2": "no flush: each step streams 24 GiB/world of input + 32 GiB/world of outputs >> 126 MB L2",
@@ -652,8 +721,10 @@ def run_ours(args):
             "error": e2e_error,
             "api": "paper_1606_06508_b200.normalize3(p, pinned numpy [N,3], out=(r, unit)) -> fn_host_run",
             "gpu_launches": e2e_launches,
+            "gpu_launches_source": "fn_launch_count() difference around the timed loop",
             "host_cpus": "NUMA-local to the GPU" if numa.cpus else "all (topology unknown)",
         },
+        "e2e_default_api": default_api,
         "validation": {
             "row_classes": dict(zip(multigpu.COUNTER_NAMES, counts_h)),
             "rows_counted": int(sum(counts_h)),
@@ -689,6 +760,42 @@ def run_ours(args):
     return 0
 
 
+def _rows_arg(text: str) -> int:
+    t = text.strip().replace(" ", "")
+    if "^" in t:
+        b, e = t.split("^")
+        v = int(b) ** int(e)
+    elif "<<" in t:
+        b, e = t.split("<<")
+        v = int(b) << int(e)
+    else:
+        v = int(float(t)) if "e" in t.lower() else int(t)
+    if v < 1:
+        raise argparse.ArgumentTypeError("--rows must be positive")
+    return v
+
+
+def _self_launch(args) -> int:
+    """`bench.py --gpus N` (N > 1) run without torchrun: launch N ranks the way the driver
+    does (torch.distributed.run, one process per GPU, 127.0.0.1) and return their exit
+    code.  Refuses to share GPUs between NCCL ranks."""
+    import socket
+
+    import torch
+
+    ndev = torch.cuda.device_count()
+    if args.dist_backend == "nccl" and ndev < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} CUDA devices for NCCL ranks, "
+              f"{ndev} visible (use --dist-backend gloo to share devices in a test)", file=sys.stderr)
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
@@ -699,7 +806,15 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-configs", action="store_true",
                     help="skip the informational per-config measurements (configs 1-4)")
+    ap.add_argument("--no-default-api", action="store_true",
+                    help="skip the e2e_default_api leg (pageable numpy in, library-allocated outputs)")
+    ap.add_argument("--rows", type=_rows_arg, default=ROWS_TOTAL,
+                    help="total rows over all ranks (default 2^30, BASELINE config 5); e.g. 2^26")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="process-group backend for N > 1 (gloo lets several ranks share one GPU in tests)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _self_launch(args)
     if args.warmup < 3 and args.impl == "ours":
         print("note: --warmup raised to 3 (timing rule)", file=sys.stderr)
         args.warmup = 3

@@ -157,6 +157,16 @@ int fn_host_run_ld(int op, int dim, int dtype, const void* x, int64_t n, int64_t
 int fn_host_run_multi_ld(int op, int dim, int dtype, const void* x, int64_t n, int64_t ldx,
                          void* head, void* body, void* sq, const double* ka, const int* devices,
                          int ndev);
+/* fn_host_run_soa over several devices of one process, sharded like fn_host_run_multi
+ * (every component and output array split at the same row boundaries). */
+int fn_host_run_soa_multi(int op, int dim, int dtype, const void* const* xs, int64_t n, void* head,
+                          void* const* body, void* sq, const double* ka, const int* devices, int ndev);
+/* Kernels this library has launched so far, process-wide (all threads and devices; the
+ * scalar path included).  Callers difference it around a region to count its launches. */
+int64_t fn_launch_count(void);
+/* Diagnostics: zero-copy contexts created so far for small host batches (each holds a
+ * mapped page-locked buffer and a stream; they are pooled per device and reused). */
+int64_t fn_small_contexts(void);
 /* fn_run for the rotation ops, with a device counter (uint64, accumulated; may be NULL)
  * of rows the reference would reject. */
 int fn_run_rot(int op, const double* q, int64_t n, double* head, double* body, double* extra,

@@ -86,6 +86,12 @@ def _declare(L: ctypes.CDLL) -> None:
     L.fn_host_free.argtypes = [_vp]
     L.fn_host_run_soa.restype = _int
     L.fn_host_run_soa.argtypes = [_int, _int, _int, _vp, _i64, _vp, _vp, _vp, _vp]
+    L.fn_host_run_soa_multi.restype = _int
+    L.fn_host_run_soa_multi.argtypes = [_int, _int, _int, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _int]
+    L.fn_launch_count.restype = _i64
+    L.fn_launch_count.argtypes = []
+    L.fn_small_contexts.restype = _i64
+    L.fn_small_contexts.argtypes = []
     L.fn_run_soa.restype = _int
     L.fn_run_soa.argtypes = [_int, _int, _int, _vp, _i64, _vp, _vp, _vp, _vp, _vp]
     L.fn_rotate_rows_f64.restype = _int

@@ -73,8 +73,9 @@ _host = threading.local()
 
 @contextmanager
 def host_devices(devices):
-    """Within the scope (this thread), host-array calls shard their rows over
-    ``devices`` (CUDA ordinals), one host thread per device (fn_host_run_multi)."""
+    """Within the scope (this thread), host-array calls -- ``[N, n]`` rows and component
+    arrays alike -- shard their rows over ``devices`` (CUDA ordinals), one host thread
+    per device (fn_host_run_multi / fn_host_run_soa_multi)."""
     devs = [int(d) for d in devices]
     if not devs:
         raise ValueError("host_devices needs at least one device")
@@ -107,6 +108,100 @@ def host_empty(shape, dtype=np.float64) -> np.ndarray:
     buf = (ctypes.c_char * nbytes).from_address(ptr.value)
     weakref.finalize(buf, L.fn_host_free, ptr.value)
     return np.frombuffer(buf, dtype=dt, count=count).reshape(shape)
+
+
+class _PinnedPool:
+    """Page-locked blocks for the outputs of host-array calls made without ``out=``.
+
+    Results the library allocates itself land in page-locked memory, so the D2H copies
+    go straight into them: no staging copy, no first-touch page faults in a fresh
+    ``np.empty``.  Pinning is slow (``cudaHostAlloc`` zeroes and locks every page), so
+    blocks are recycled: when a result array and all its views are gone, its block goes
+    back to a free list by size class (sizes rounded up by at most 1/8), and the next
+    call of that size class reuses it.  The free lists hold at most
+    FASTNORM_B200_HOST_POOL_MB (default: a quarter of the host's memory); beyond that,
+    blocks are released.  FASTNORM_B200_HOST_POOL_MB=0 turns the pool off (plain
+    ``np.empty`` outputs, staged on the way back)."""
+
+    MIN_BYTES = 128 << 10  # smaller outputs take the zero-copy small-batch route anyway
+
+    def __init__(self):
+        self._lock = threading.Lock()
+        self._free: dict[int, list[int]] = {}
+        self._cached = 0
+        self._limit: int | None = None
+        self.allocs = 0  # blocks pinned so far (fn_host_alloc calls)
+        self.reuses = 0
+
+    def limit(self) -> int:
+        if self._limit is None:
+            import os
+
+            env = os.environ.get("FASTNORM_B200_HOST_POOL_MB")
+            if env is not None:
+                self._limit = max(0, int(env)) << 20
+            else:
+                try:
+                    self._limit = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") // 4
+                except (ValueError, OSError):
+                    self._limit = 8 << 30
+        return self._limit
+
+    @staticmethod
+    def size_class(nbytes: int) -> int:
+        step = max(64 << 10, 1 << max(0, nbytes.bit_length() - 4))
+        return -(-nbytes // step) * step
+
+    def empty(self, shape, dtype: np.dtype) -> np.ndarray:
+        import ctypes
+        import weakref
+
+        count = 1
+        for d in shape:
+            count *= d
+        nbytes = count * dtype.itemsize
+        if nbytes < self.MIN_BYTES or self.limit() == 0:
+            return np.empty(shape, dtype=dtype)
+        cls = self.size_class(nbytes)
+        ptr = None
+        with self._lock:
+            lst = self._free.get(cls)
+            if lst:
+                ptr = lst.pop()
+                self._cached -= cls
+                self.reuses += 1
+        if ptr is None:
+            L = _lib.lib()
+            p = ctypes.c_void_p()
+            if L.fn_host_alloc(cls, ctypes.byref(p)) != 0:
+                return np.empty(shape, dtype=dtype)  # cannot pin more: a pageable result
+            ptr = p.value
+            with self._lock:
+                self.allocs += 1
+        buf = (ctypes.c_char * cls).from_address(ptr)
+        fin = weakref.finalize(buf, self._give, ptr, cls)
+        fin.atexit = False  # at exit the process releases everything anyway
+        return np.frombuffer(buf, dtype=dtype, count=count).reshape(shape)
+
+    def _give(self, ptr: int, cls: int) -> None:
+        with self._lock:
+            if self._cached + cls <= self.limit():
+                self._free.setdefault(cls, []).append(ptr)
+                self._cached += cls
+                return
+        _lib.lib().fn_host_free(ptr)
+
+    def clear(self) -> None:
+        """Release every cached block (results still alive keep theirs)."""
+        with self._lock:
+            blocks = [p for lst in self._free.values() for p in lst]
+            self._free.clear()
+            self._cached = 0
+        for ptr in blocks:
+            _lib.lib().fn_host_free(ptr)
+
+
+pinned_pool = _PinnedPool()
 
 
 class BatchOut(NamedTuple):
@@ -384,7 +479,7 @@ def run(op: int, dim: int, x, ka_arr: np.ndarray | None, out=None, invalid=None)
         if not w:
             return None
         o = _check_out(o, _shape(n, w), x, what)
-        return o if o is not None else np.empty(_shape(n, w), dtype=x.dtype)
+        return o if o is not None else pinned_pool.empty(_shape(n, w), x.dtype)
 
     head, body, extra = alloc_np(o_head, w0, "head"), alloc_np(o_body, w1, "body"), alloc_np(o_extra, w2, "extra")
     if ldx != dim and any(o is not None and np.may_share_memory(x, o) for o in (head, body, extra)):
@@ -503,7 +598,7 @@ def run_rows2(op: int, a, v, ka_arr: np.ndarray | None, out=None, invalid=None):
                         ka_arr, None if out is None else np.asarray(out.numpy() if is_torch(out) else out))
         return _torch().from_numpy(res) if is_torch(v) else res
     a, v = np.ascontiguousarray(a), np.ascontiguousarray(v)
-    o = _check_out(out, (n, 3), v, "out") if out is not None else np.empty((n, 3), dtype=np.float64)
+    o = _check_out(out, (n, 3), v, "out") if out is not None else pinned_pool.empty((n, 3), np.dtype(np.float64))
     rc = L.fn_host_rotate_rows_f64(op, a.ctypes.data, v.ctypes.data, n, o.ctypes.data, kptr)
     _lib.check(rc, "fn_host_rotate_rows_f64")
     return o
@@ -551,15 +646,22 @@ def _run_soa_host(op: int, dim: int, xs, ka_arr: np.ndarray | None):
         raise TypeError("component arrays must be 1-D and share a dtype")
     dcode = _dtype_code(str(dt))
     w0, w1, w2 = widths(op, dim)
-    head = np.empty(n, dtype=dt)
-    body = [np.empty(n, dtype=dt) for _ in range(dim)] if w1 else None
-    extra = np.empty(n, dtype=dt) if w2 else None
+    head = pinned_pool.empty((n,), dt)
+    body = [pinned_pool.empty((n,), dt) for _ in range(dim)] if w1 else None
+    extra = pinned_pool.empty((n,), dt) if w2 else None
     xp = (ctypes.c_void_p * dim)(*[a.ctypes.data for a in arrs])
     bp = (ctypes.c_void_p * dim)(*[b.ctypes.data for b in body]) if body else None
     kptr = None if ka_arr is None else _ka_address(ka_arr)
-    rc = _lib.lib().fn_host_run_soa(op, dim, dcode, ctypes.addressof(xp), n, head.ctypes.data,
-                                    None if bp is None else ctypes.addressof(bp),
-                                    None if extra is None else extra.ctypes.data, kptr)
+    bptr = None if bp is None else ctypes.addressof(bp)
+    eptr = None if extra is None else extra.ctypes.data
+    devs = getattr(_host, "devices", None)
+    if devs:  # shard over the scoped devices, as the AoS host calls do
+        darr = np.array(devs, dtype=np.int32)
+        rc = _lib.lib().fn_host_run_soa_multi(op, dim, dcode, ctypes.addressof(xp), n, head.ctypes.data, bptr,
+                                              eptr, kptr, darr.ctypes.data, len(devs))
+    else:
+        rc = _lib.lib().fn_host_run_soa(op, dim, dcode, ctypes.addressof(xp), n, head.ctypes.data, bptr, eptr,
+                                        kptr)
     if rc:
         _lib.check(rc, "fn_host_run_soa")
     if as_tensor:

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -138,6 +139,10 @@ static int cps_override() {
     return v;
 }
 
+// Kernels this library has launched, process-wide (fn_launch_count): the bench counts
+// its launches inside a timed region from the library itself.
+static std::atomic<int64_t> g_launches{0};
+
 // Programmatic dependent launch for the streaming kernels (FASTNORM_B200_PDL=0 turns it
 // off).  Back-to-back launches on a stream overlap one kernel's drain with the next one's
 // launch and prologue; each kernel still waits (griddepcontrol.wait) for its
@@ -163,7 +168,9 @@ static cudaError_t launch_pdl(void (*kern)(Params...), int grid, int block, size
     cfg.stream = stream;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, kern, args...);
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, args...);
+    if (e == cudaSuccess) g_launches.fetch_add(1, std::memory_order_relaxed);
+    return e;
 }
 
 // CTAs per SM: the measured streaming optimum (CtasPerSm); small batches (few tiles per
@@ -852,6 +859,18 @@ static int staging_get(int dev, size_t bytes_per_pipe, Staging** out) {
 
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
+// Armed once the first chunk is enqueued: an error return would otherwise leave H2D / D2H
+// copies of earlier chunks in flight on the pipe streams, reading or writing caller
+// buffers the caller may free as soon as the call has returned.  Declared after the
+// device lock, so it runs before the lock is released.
+struct PipeDrainGuard {
+    Staging* st = nullptr;
+    ~PipeDrainGuard() {
+        if (!st) return;
+        for (int p = 0; p < st->pipes; ++p) cudaStreamSynchronize(st->streams[p]);
+    }
+};
+
 // Page-locked host staging of bytes_per_pipe per pipe (caller holds device_mutex(dev)).
 static int host_staging_get(Staging* st, size_t bytes_per_pipe) {
     if (st->hbytes >= bytes_per_pipe) return FN_OK;
@@ -886,21 +905,79 @@ struct SmallCtx {
     char* dptr = nullptr;
 };
 
+// Contexts live in a per-device free list, not in thread_local storage: fn_host_run_multi
+// runs each shard on a fresh std::thread, and a thread_local context (a mapped
+// page-locked buffer and a stream) would leak with every such thread.  The pool holds
+// at most as many contexts per device as there were concurrent small calls on it.
+constexpr size_t kSmallCtxBytes = kSmallHostBytes + 16 * 256;
+
+class SmallPool {
+  public:
+    // Takes a context of device `dev` (the caller's current device), creating one if none is free.
+    int acquire(int dev, SmallCtx** out) {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            if ((int)free_.size() <= dev) free_.resize(dev + 1);
+            if (!free_[dev].empty()) {
+                *out = free_[dev].back();
+                free_[dev].pop_back();
+                return FN_OK;
+            }
+        }
+        std::unique_ptr<SmallCtx> c(new SmallCtx());
+        cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
+        e = cudaHostAlloc(reinterpret_cast<void**>(&c->host), kSmallCtxBytes, cudaHostAllocMapped);
+        if (e != cudaSuccess) {
+            cudaStreamDestroy(c->stream);
+            return cuda_fail(e, "cudaHostAlloc");
+        }
+        e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->dptr), c->host, 0);
+        if (e != cudaSuccess) {
+            cudaFreeHost(c->host);
+            cudaStreamDestroy(c->stream);
+            return cuda_fail(e, "cudaHostGetDevicePointer");
+        }
+        c->dev = dev;
+        std::lock_guard<std::mutex> lk(mu_);
+        ++created_;
+        *out = c.release();
+        return FN_OK;
+    }
+    void release(SmallCtx* c) {
+        std::lock_guard<std::mutex> lk(mu_);
+        free_[c->dev].push_back(c);
+    }
+    int64_t created() {
+        std::lock_guard<std::mutex> lk(mu_);
+        return created_;
+    }
+
+  private:
+    std::mutex mu_;
+    std::vector<std::vector<SmallCtx*>> free_;
+    int64_t created_ = 0;
+};
+
+static SmallPool& small_pool() {
+    static SmallPool* pool = new SmallPool();  // never destroyed: contexts outlive static teardown
+    return *pool;
+}
+
+struct SmallLease {
+    SmallCtx* c = nullptr;
+    ~SmallLease() {
+        if (c) small_pool().release(c);
+    }
+};
+
 static int host_run_small(int op, int dim, int dtype, const void* x, const void* x2, int dim2, int64_t n,
                           void* head, void* body, void* sq, const double* ka, int dev, int64_t ldx) {
-    static thread_local std::vector<SmallCtx> ctxs;
-    if ((int)ctxs.size() <= dev) ctxs.resize(dev + 1);
-    SmallCtx& c = ctxs[dev];
+    SmallLease lease;
+    int rc0 = small_pool().acquire(dev, &lease.c);
+    if (rc0 != FN_OK) return rc0;
+    SmallCtx& c = *lease.c;
     cudaError_t e;
-    if (c.dev < 0) {
-        e = cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking);
-        if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
-        e = cudaHostAlloc(reinterpret_cast<void**>(&c.host), kSmallHostBytes + 8 * 256, cudaHostAllocMapped);
-        if (e != cudaSuccess) return cuda_fail(e, "cudaHostAlloc");
-        e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c.dptr), c.host, 0);
-        if (e != cudaSuccess) return cuda_fail(e, "cudaHostGetDevicePointer");
-        c.dev = dev;
-    }
     const size_t w = dtype == FN_F64 ? 8 : 4;
     const Widths wd = op_widths(op, dim);
     const size_t bx = align256(n * ldx * w), bx2 = align256(n * dim2 * w), b0 = align256(n * wd.w0 * w),
@@ -1000,6 +1077,8 @@ static int host_run_impl(int op, int dim, int dtype, const void* x, const void* 
         pending[p].live = false;
         return FN_OK;
     };
+    PipeDrainGuard in_flight;
+    in_flight.st = st;
     int64_t chunk = 0;
     for (int64_t r0 = 0; r0 < n; r0 += rows, ++chunk) {
         const int p = (int)(chunk % st->pipes);
@@ -1051,6 +1130,7 @@ static int host_run_impl(int op, int dim, int dtype, const void* x, const void* 
         e = cudaStreamSynchronize(st->streams[p]);
         if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
     }
+    in_flight.st = nullptr;
     return FN_OK;
 }
 
@@ -1072,19 +1152,11 @@ int host_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, v
 // it in place, one synchronisation, results copied out).
 static int host_run_soa_small(int op, int dim, int dtype, const void* const* xs, int64_t n, char* const* outs,
                               int nout, bool has_body, bool has_sq, const double* ka, int dev) {
-    static thread_local std::vector<SmallCtx> ctxs;
-    if ((int)ctxs.size() <= dev) ctxs.resize(dev + 1);
-    SmallCtx& c = ctxs[dev];
+    SmallLease lease;
+    int rc0 = small_pool().acquire(dev, &lease.c);
+    if (rc0 != FN_OK) return rc0;
+    SmallCtx& c = *lease.c;
     cudaError_t e;
-    if (c.dev < 0) {
-        e = cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking);
-        if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
-        e = cudaHostAlloc(reinterpret_cast<void**>(&c.host), kSmallHostBytes + 16 * 256, cudaHostAllocMapped);
-        if (e != cudaSuccess) return cuda_fail(e, "cudaHostAlloc");
-        e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c.dptr), c.host, 0);
-        if (e != cudaSuccess) return cuda_fail(e, "cudaHostGetDevicePointer");
-        c.dev = dev;
-    }
     const size_t w = dtype == FN_F64 ? 8 : 4;
     const size_t arr = align256(n * w);
     const void* dx[4];
@@ -1174,6 +1246,8 @@ int host_run_soa(int op, int dim, int dtype, const void* const* xs, int64_t n, v
         pending[p].live = false;
         return FN_OK;
     };
+    PipeDrainGuard in_flight;
+    in_flight.st = st;
     int64_t chunk = 0;
     for (int64_t r0 = 0; r0 < n; r0 += rows, ++chunk) {
         const int p = (int)(chunk % st->pipes);
@@ -1216,6 +1290,7 @@ int host_run_soa(int op, int dim, int dtype, const void* const* xs, int64_t n, v
         e = cudaStreamSynchronize(st->streams[p]);
         if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
     }
+    in_flight.st = nullptr;
     return FN_OK;
 }
 
@@ -1268,7 +1343,9 @@ static cudaError_t scalar_launch(const double* xin, const KArgs<T>& ka, const Sc
     for (int k = 0; k < N; ++k) x.v[k] = (T)xin[k];  // f32: the reference's <float> cast
     scalar_kernel<T, N, OP><<<1, 32, 0, c.stream>>>(
         x, ka, reinterpret_cast<T*>(c.dptr), reinterpret_cast<unsigned*>(c.dptr + kScalarFlagOffset), c.seq);
-    return cudaGetLastError();
+    const cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) g_launches.fetch_add(1, std::memory_order_relaxed);
+    return e;
 }
 
 template <typename T, int OP>
@@ -1315,8 +1392,37 @@ static inline void cpu_relax() {
 #endif
 }
 
+// Scalar contexts are cached per thread (no lock on the ~10 us path) and handed back to
+// a process-wide free list when the thread exits, so short-lived caller threads reuse
+// them instead of each leaking a stream and a mapped page-locked buffer.
+static std::mutex g_scalar_free_mu;
+static std::vector<ScalarCtx>* g_scalar_free = new std::vector<ScalarCtx>();  // never destroyed
+
+struct ScalarCtxCache {
+    std::vector<ScalarCtx> ctxs;  // indexed by device
+    ~ScalarCtxCache() {
+        std::lock_guard<std::mutex> lk(g_scalar_free_mu);
+        for (auto& c : ctxs)
+            if (c.dev >= 0) g_scalar_free->push_back(c);
+    }
+    ScalarCtx& get(int dev) {
+        if ((int)ctxs.size() <= dev) ctxs.resize(dev + 1);
+        ScalarCtx& c = ctxs[dev];
+        if (c.dev < 0) {
+            std::lock_guard<std::mutex> lk(g_scalar_free_mu);
+            for (size_t k = 0; k < g_scalar_free->size(); ++k)
+                if ((*g_scalar_free)[k].dev == dev) {
+                    c = (*g_scalar_free)[k];
+                    g_scalar_free->erase(g_scalar_free->begin() + k);
+                    break;
+                }
+        }
+        return c;
+    }
+};
+
 int scalar_run(int op, int dim, int dtype, const double* xin, double* out, const double* ka) {
-    static thread_local std::vector<ScalarCtx> ctxs;
+    static thread_local ScalarCtxCache cache;
     if (!xin || !out) return fail(FN_EINVAL, "xin and out must not be NULL");
     if (op < FN_OP_SCALE || op > FN_OP_ROT_APPLY || dim < 2 || dim > 4)
         return fail(FN_EINVAL, "unknown op or dim");
@@ -1328,8 +1434,7 @@ int scalar_run(int op, int dim, int dtype, const double* xin, double* out, const
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-    if ((int)ctxs.size() <= dev) ctxs.resize(dev + 1);
-    ScalarCtx& c = ctxs[dev];
+    ScalarCtx& c = cache.get(dev);
     if (c.dev < 0) {
         e = cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking);
         if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
@@ -1368,20 +1473,14 @@ int scalar_run(int op, int dim, int dtype, const double* xin, double* out, const
 // Row shards over several devices, one host thread per device, each running the
 // chunked host pipeline above on its own streams and staging buffers.  No data moves
 // between devices (rows are independent, _kernels.pyx:167-412).
-int host_run_multi(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* body,
-                   void* sq, const double* ka, const int* devices, int ndev, int64_t ldx = 0) {
+template <typename ShardFn>
+static int over_devices(int64_t n, const int* devices, int ndev, ShardFn shard) {
     if (ndev < 1 || !devices) return fail(FN_EINVAL, "need at least one device");
-    int rc = check_args(op, dim, dtype, x, n, head, body, sq);
-    if (rc != FN_OK || n == 0) return rc;
-    if (ldx == 0) ldx = dim;
-    if (ldx < dim) return fail(FN_EINVAL, "ldx (elements per input row) must be >= dim");
     int count = 0;
     cudaError_t e = cudaGetDeviceCount(&count);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
     for (int k = 0; k < ndev; ++k)
         if (devices[k] < 0 || devices[k] >= count) return fail(FN_EINVAL, "device index out of range");
-    const size_t w = dtype == FN_F64 ? 8 : 4;
-    const Widths wd = op_widths(op, dim);
     std::vector<int> rcs(ndev, FN_OK);
     std::vector<std::string> errs(ndev);
     std::vector<std::thread> pool;
@@ -1396,10 +1495,7 @@ int host_run_multi(int op, int dim, int dtype, const void* x, int64_t n, void* h
             if (ee != cudaSuccess) {
                 rcs[k] = cuda_fail(ee, "cudaSetDevice");
             } else if (m > 0) {
-                rcs[k] = host_run(op, dim, dtype, static_cast<const char*>(x) + r0 * ldx * w, m,
-                                  static_cast<char*>(head) + r0 * wd.w0 * w,
-                                  wd.w1 ? static_cast<char*>(body) + r0 * wd.w1 * w : nullptr,
-                                  wd.w2 ? static_cast<char*>(sq) + r0 * wd.w2 * w : nullptr, ka, ldx);
+                rcs[k] = shard(r0, m);
             }
             if (rcs[k] != FN_OK) errs[k] = g_last_error;
         });
@@ -1408,6 +1504,49 @@ int host_run_multi(int op, int dim, int dtype, const void* x, int64_t n, void* h
     for (int k = 0; k < ndev; ++k)
         if (rcs[k] != FN_OK) return fail(rcs[k], "device " + std::to_string(devices[k]) + ": " + errs[k]);
     return FN_OK;
+}
+
+int host_run_multi(int op, int dim, int dtype, const void* x, int64_t n, void* head, void* body,
+                   void* sq, const double* ka, const int* devices, int ndev, int64_t ldx = 0) {
+    int rc = check_args(op, dim, dtype, x, n, head, body, sq);
+    if (rc != FN_OK) return rc;
+    if (ndev < 1 || !devices) return fail(FN_EINVAL, "need at least one device");
+    if (n == 0) return FN_OK;
+    if (ldx == 0) ldx = dim;
+    if (ldx < dim) return fail(FN_EINVAL, "ldx (elements per input row) must be >= dim");
+    const size_t w = dtype == FN_F64 ? 8 : 4;
+    const Widths wd = op_widths(op, dim);
+    return over_devices(n, devices, ndev, [&](int64_t r0, int64_t m) {
+        return host_run(op, dim, dtype, static_cast<const char*>(x) + r0 * ldx * w, m,
+                        static_cast<char*>(head) + r0 * wd.w0 * w,
+                        wd.w1 ? static_cast<char*>(body) + r0 * wd.w1 * w : nullptr,
+                        wd.w2 ? static_cast<char*>(sq) + r0 * wd.w2 * w : nullptr, ka, ldx);
+    });
+}
+
+// The structure-of-arrays host call sharded the same way (each component and output
+// array split at the same row boundaries).
+int host_run_soa_multi(int op, int dim, int dtype, const void* const* xs, int64_t n, void* head,
+                       void* const* body, void* sq, const double* ka, const int* devices, int ndev) {
+    if (op < FN_OP_SCALE || op > FN_OP_NORMALIZE_SQ) return fail(FN_EINVAL, "unknown op for the SoA entry");
+    if (dim < 2 || dim > 4) return fail(FN_EINVAL, "dim must be 2, 3 or 4");
+    if (dtype != FN_F32 && dtype != FN_F64) return fail(FN_EINVAL, "dtype must be FN_F32/FN_F64");
+    if (n < 0) return fail(FN_EINVAL, "n must be >= 0");
+    if (ndev < 1 || !devices) return fail(FN_EINVAL, "need at least one device");
+    if (n == 0) return FN_OK;
+    const Widths wd = op_widths(op, dim);
+    if (!xs || !head || (wd.w1 && !body)) return fail(FN_EINVAL, "xs, head and body must not be NULL");
+    const size_t w = dtype == FN_F64 ? 8 : 4;
+    return over_devices(n, devices, ndev, [&](int64_t r0, int64_t m) {
+        const void* xk[4] = {};
+        void* bk[4] = {};
+        for (int c = 0; c < dim; ++c) {
+            xk[c] = xs[c] ? static_cast<const char*>(xs[c]) + r0 * w : nullptr;
+            if (wd.w1) bk[c] = body[c] ? static_cast<char*>(body[c]) + r0 * w : nullptr;
+        }
+        return host_run_soa(op, dim, dtype, xk, m, static_cast<char*>(head) + r0 * w, wd.w1 ? bk : nullptr,
+                            wd.w2 ? static_cast<char*>(sq) + r0 * w : nullptr, ka);
+    });
 }
 
 }  // namespace fnb
@@ -1498,6 +1637,15 @@ int fn_host_run_soa(int op, int dim, int dtype, const void* const* xs, int64_t n
                     void* sq, const double* ka) {
     return fnb::host_run_soa(op, dim, dtype, xs, n, head, body, sq, ka);
 }
+
+int fn_host_run_soa_multi(int op, int dim, int dtype, const void* const* xs, int64_t n, void* head,
+                          void* const* body, void* sq, const double* ka, const int* devices, int ndev) {
+    return fnb::host_run_soa_multi(op, dim, dtype, xs, n, head, body, sq, ka, devices, ndev);
+}
+
+int64_t fn_launch_count(void) { return fnb::g_launches.load(std::memory_order_relaxed); }
+
+int64_t fn_small_contexts(void) { return fnb::small_pool().created(); }
 
 int fn_run_soa(int op, int dim, int dtype, const void* const* xs, int64_t n, void* head,
                void* const* body, void* sq, const double* ka, void* stream) {
