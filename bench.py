@@ -728,8 +728,8 @@ def run_ours(args):
         "validation": {
             "row_classes": dict(zip(multigpu.COUNTER_NAMES, counts_h)),
             "rows_counted": int(sum(counts_h)),
-            "reduce": f"NCCL all_reduce(sum) of 6 counters over {world} rank(s)" if distributed
-                      else "single process",
+            "reduce": f"{args.dist_backend} all_reduce(sum) of 6 counters over {world} rank(s)"
+                      if distributed else "single process",
         },
     }
     if world == 1 and not args.no_configs:

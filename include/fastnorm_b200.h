@@ -137,6 +137,9 @@ int fn_host_run_soa(int op, int dim, int dtype, const void* const* xs, int64_t n
  * only).  fn_host_free(NULL) is a no-op. */
 int fn_host_alloc(size_t bytes, void** ptr);
 int fn_host_free(void* ptr);
+/* 1 if ptr is page-locked host memory known to CUDA (fn_host_alloc, cudaHostAlloc,
+ * cudaHostRegister, or the outputs the Python API allocates from its pool), else 0. */
+int fn_host_is_page_locked(const void* ptr);
 /* One row with the reference's scalar semantics, low latency: x[dim] as doubles (the f32
  * families round them to binary32 like the reference's <float> casts), results written
  * to out as doubles in the order head, body..., extra... (e.g. r, u1..un; inv, s1..sn;

@@ -83,6 +83,8 @@ def _declare(L: ctypes.CDLL) -> None:
     L.fn_host_alloc.restype = _int
     L.fn_host_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(_vp)]
     L.fn_host_free.restype = _int
+    L.fn_host_is_page_locked.restype = _int
+    L.fn_host_is_page_locked.argtypes = [_vp]
     L.fn_host_free.argtypes = [_vp]
     L.fn_host_run_soa.restype = _int
     L.fn_host_run_soa.argtypes = [_int, _int, _int, _vp, _i64, _vp, _vp, _vp, _vp]

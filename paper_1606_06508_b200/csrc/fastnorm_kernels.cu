@@ -189,6 +189,53 @@ template <int N> struct PaddedLdx {
     static constexpr int value = N == 3 ? 4 : 0;
 };
 
+// Dynamic tile schedule (tma_stream_kernel): one {next, done} counter pair per (device,
+// stream), allocated on a stream's first small batch and zeroed in stream order.  The
+// kernel's last CTA resets the pair, so consecutive launches on the stream reuse it;
+// launches on different streams never share one.  Used for batches of more than S but
+// at most kDynTilesPerCta tiles per CTA (config 1: 1e6 rows = 3906 tiles over 592 CTAs),
+// where the finish-time spread of a static round-robin is a visible share of the
+// launch; large batches keep the static schedule (no atomics).  Not
+// under stream capture: a graph could be replayed on several streams at once.
+// FASTNORM_B200_DYN=0 / 1 forces static / dynamic (when the batch has > S tiles per CTA).
+constexpr int64_t kDynTilesPerCta = 32;
+
+static int dyn_mode() {
+    static const int v = [] {
+        const char* e = getenv("FASTNORM_B200_DYN");
+        return e ? atoi(e) : -1;
+    }();
+    return v;
+}
+
+static std::mutex g_sched_mu;
+static std::vector<std::pair<std::pair<int, cudaStream_t>, unsigned*>>* g_sched =
+    new std::vector<std::pair<std::pair<int, cudaStream_t>, unsigned*>>();  // never destroyed
+
+static unsigned* sched_pair(int dev, cudaStream_t stream) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cap) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (cap != cudaStreamCaptureStatusNone) return nullptr;
+    std::lock_guard<std::mutex> lk(g_sched_mu);
+    for (auto& kv : *g_sched)
+        if (kv.first.first == dev && kv.first.second == stream) return kv.second;
+    unsigned* p = nullptr;
+    if (cudaMalloc(&p, 2 * sizeof(unsigned)) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;  // static schedule instead
+    }
+    if (cudaMemsetAsync(p, 0, 2 * sizeof(unsigned), stream) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(p);
+        return nullptr;
+    }
+    g_sched->push_back({{dev, stream}, p});
+    return p;
+}
+
 template <typename T, int N, int OP, int LDX, bool MIS>
 static cudaError_t launch_tma_as(const T* x, const T* x2, int64_t n, T* head, T* body, T* extra,
                                  const KArgs<T>& ka, int dev, int sms, cudaStream_t stream) {
@@ -198,8 +245,13 @@ static cudaError_t launch_tma_as(const T* x, const T* x2, int64_t n, T* head, T*
     const int64_t per_sm = std::min<int64_t>(TL::blocks_per_sm(dev), ctas_per_sm_for<OP>(ntiles, sms));
     const int64_t resident = per_sm * sms;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, resident));
+    KArgs<T> kd = ka;
+    kd.sched = nullptr;
+    const int mode = dyn_mode();
+    if (mode != 0 && ntiles > (int64_t)L::S * grid && (mode == 1 || ntiles <= kDynTilesPerCta * grid))
+        kd.sched = sched_pair(dev, stream);
     return launch_pdl(TL::kernel(), grid, Tile<T, N>::kThreads, L::kSmemBytes, stream, x, x2, n, head, body, extra,
-                      ka);
+                      kd);
 }
 
 // MIS: the instantiation for inputs off the 16-byte grid (tma_stream_kernel).
@@ -1599,6 +1651,8 @@ int fn_host_alloc(size_t bytes, void** ptr) {
     }
     return FN_OK;
 }
+
+int fn_host_is_page_locked(const void* ptr) { return ptr && fnb::is_page_locked(ptr) ? 1 : 0; }
 
 int fn_host_free(void* ptr) {
     if (!ptr) return FN_OK;

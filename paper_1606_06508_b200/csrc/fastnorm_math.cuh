@@ -116,6 +116,8 @@ template <typename T> struct KArgs {
     int k_min, k_max;   // log2(sigma_min), log2(sigma_max) when pow2 (validated sets)
     bool pow2;          // sigma_min, sigma_max and their inverses are powers of two
     unsigned long long* invalid;  // rows rejected by the rotations (may be NULL)
+    unsigned* sched;              // tma_stream_kernel's dynamic tile schedule {next, done}
+                                  // (NULL: the static round-robin schedule)
     T rot[9];           // FN_OP_ROT_APPLY: the matrix, row-major
 };
 

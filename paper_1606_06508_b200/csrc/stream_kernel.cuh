@@ -590,11 +590,31 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
     const unsigned char* x2a = reinterpret_cast<const unsigned char*>(x2) - mis2;
     const uint32_t load_bytes = L::kInBytes + (MIS && mis ? 16 : 0);
     const uint32_t load2_bytes = L::kIn2Bytes + (MIS && mis2 ? 16 : 0);
-    const int64_t my_tiles =
-        ntiles > (int64_t)blockIdx.x ? (ntiles - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
+    // Schedule.  Static (the default): CTA b owns tiles b, b + grid, b + 2 grid, ...
+    // Dynamic (ka.sched != NULL; small batches of a few tiles per CTA, where uneven
+    // per-CTA progress leaves a tail of CTAs still working on their last tile while the
+    // others are idle): every CTA's first S tiles are the static ones (no atomic on the
+    // critical start), then its leader claims further tiles from a counter in global
+    // memory as it refills a stage, S tiles ahead of use.  The tile id of each stage
+    // travels to the CTA's threads through s_tile[], written before the stage's
+    // mbarrier arrive (release) and read after its wait (acquire); -1 = no more tiles.
+    // The last CTA to finish resets the counter pair for the next launch on the stream
+    // (the host hands every stream its own pair; launches on one stream run in order,
+    // and a PDL successor's griddepcontrol.wait sees the reset).
+    unsigned* const sched = ka.sched;
+    const bool dyn = sched != nullptr;
+    __shared__ int64_t s_tile[S];
+    const int64_t my_tiles = dyn ? INT64_MAX
+        : (ntiles > (int64_t)blockIdx.x ? (ntiles - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0);
     const bool leader = threadIdx.x == 0;
     uint64_t policy = 0;
     unsigned long long bad = 0;
+    bool claiming = true;  // leader: no -1 claimed yet
+    auto claim = [&](int64_t k) -> int64_t {  // tile of the CTA's k-th stage fill (leader)
+        const int64_t t = k < S ? (int64_t)blockIdx.x + k * gridDim.x
+                                : (int64_t)S * gridDim.x + (int64_t)atomicAdd(&sched[0], 1u);
+        return t < ntiles ? t : -1;
+    };
 
     if (leader) {
         policy = policy_evict_first();
@@ -623,16 +643,33 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
                 bulk_load_plain(s_in2 + st * L::kIn2Bytes, x2 + tile * TR * N2, L::kIn2Bytes, &full[st]);
         }
     };
+    // Dynamic schedule: fill stage st with the CTA's k-th tile, or mark it empty.
+    auto fill_dyn = [&](int st, int64_t k) {
+        if (!claiming) return;
+        const int64_t t = claim(k);
+        s_tile[st] = t;
+        if (t >= 0) {
+            load_stage(st, t);
+        } else {
+            claiming = false;
+            mbar_arrive(&full[st]);  // completes the phase with no bytes: "no tile"
+        }
+    };
     if (leader) {
-        for (int64_t k = 0; k < my_tiles && k < S; ++k) load_stage((int)k, (int64_t)blockIdx.x + k * gridDim.x);
+        if (dyn) {
+            for (int k = 0; k < S; ++k) fill_dyn(k, k);
+        } else {
+            for (int64_t k = 0; k < my_tiles && k < S; ++k) load_stage((int)k, (int64_t)blockIdx.x + k * gridDim.x);
+        }
     }
 
     for (int64_t k = 0; k < my_tiles; ++k) {
         const int s = (int)(k % S);
         const uint32_t parity = (uint32_t)((k / S) & 1);
         const int ob = (int)(k % OB);
-        const int64_t tile = (int64_t)blockIdx.x + k * gridDim.x;
         mbar_wait(&full[s], parity);
+        const int64_t tile = dyn ? s_tile[s] : (int64_t)blockIdx.x + k * gridDim.x;
+        if (tile < 0) break;  // dynamic schedule exhausted (uniform across the CTA)
         if (k == 0) timeline_mark(2);
         timeline_tile(k, 0, threadIdx.x == 0);
 
@@ -677,11 +714,21 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
                 if (W2) bulk_store(extra + row0 * W2, t2, L::kB2);
             }
             bulk_commit();
-            if (k + S < my_tiles) load_stage(s, tile + (int64_t)S * gridDim.x);
+            if (dyn)
+                fill_dyn(s, k + S);
+            else if (k + S < my_tiles)
+                load_stage(s, tile + (int64_t)S * gridDim.x);
             // Threads write staging tile (k+2) % OB after the next __syncthreads, so group
             // k+2-OB must have been read out by then: at most OB-2 groups stay pending.
             bulk_wait_read<OB - 2>();
             timeline_tile(k, 2, true);
+        }
+    }
+    if (dyn && leader) {  // the last CTA out resets the pair for the next launch
+        __threadfence();
+        if (atomicAdd(&sched[1], 1u) == gridDim.x - 1) {
+            atomicExch(&sched[0], 0u);
+            atomicExch(&sched[1], 0u);
         }
     }
 

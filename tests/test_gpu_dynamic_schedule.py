@@ -1,0 +1,123 @@
+"""tma_stream_kernel's dynamic tile schedule (small batches: more than S and at most 32
+tiles per CTA; a {next, done} counter pair per stream, reset by the kernel's last CTA).
+
+The schedule changes which CTA computes a tile, never what is computed: outputs must be
+bit-identical to the oracle and to the static schedule (FASTNORM_B200_DYN=0), across
+back-to-back launches on one stream (the counter is reset between them, PDL included),
+on two streams at once (each stream has its own pair), and in CUDA graphs (captured
+launches take the static schedule)."""
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from gpu_helpers import compare_chunked
+
+import oracle
+import paper_1606_06508_b200 as fn
+from paper_1606_06508_b200 import _lib, workloads
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+SIZES = [1_000_000, 600_001, (1 << 21) + 5, 3_000_017]  # config 1 and neighbours (dynamic range)
+
+
+def _rows(n, cfg=5, dtype=torch.float64, dim=3):
+    x = torch.empty((n, dim), dtype=dtype, device="cuda")
+    workloads.generate_device(cfg, x)
+    return x
+
+
+@pytest.mark.parametrize("n", SIZES)
+def test_dynamic_schedule_matches_oracle(cuda_dev, n):
+    p = fn.preset("double")
+    x = _rows(n)
+    out = fn.normalize3(p, x)
+    torch.cuda.synchronize()
+    bad, first = compare_chunked(_lib.OP_NORMALIZE, x, out.length, out.unit, ka=np.array(fn.kernel_args(p)))
+    assert bad == 0, first
+
+
+@pytest.mark.parametrize("dtype,cfg", [(torch.float32, 4), (torch.float64, 1)])
+def test_back_to_back_launches_reuse_the_counter(cuda_dev, dtype, cfg):
+    p = fn.preset("single" if dtype == torch.float32 else "double")
+    xs = [_rows(n, cfg, dtype) for n in SIZES]
+    want = [fn.normalize3(p, x) for x in xs]
+    torch.cuda.synchronize()
+    want = [(w.length.clone(), w.unit.clone()) for w in want]
+    outs = [(torch.empty_like(w[0]), torch.empty_like(w[1])) for w in want]
+    for _ in range(20):  # 80 launches on one stream, no synchronisation between them
+        for x, o in zip(xs, outs):
+            fn.normalize3(p, x, out=o)
+    torch.cuda.synchronize()
+    for w, o in zip(want, outs):
+        assert torch.equal(w[0].view(torch.int64 if dtype == torch.float64 else torch.int32),
+                           o[0].view(torch.int64 if dtype == torch.float64 else torch.int32))
+        assert torch.equal(w[1].view(torch.int64 if dtype == torch.float64 else torch.int32),
+                           o[1].view(torch.int64 if dtype == torch.float64 else torch.int32))
+
+
+def test_two_streams_at_once(cuda_dev):
+    p = fn.preset("double")
+    xa, xb = _rows(1_000_000, 1), _rows(3_000_017, 5)
+    wa, wb = fn.normalize3(p, xa), fn.normalize3(p, xb)
+    torch.cuda.synchronize()
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    oa = [(torch.empty_like(wa.length), torch.empty_like(wa.unit)) for _ in range(8)]
+    ob = [(torch.empty_like(wb.length), torch.empty_like(wb.unit)) for _ in range(8)]
+    for k in range(8):
+        with torch.cuda.stream(sa):
+            fn.normalize3(p, xa, out=oa[k])
+        with torch.cuda.stream(sb):
+            fn.normalize3(p, xb, out=ob[k])
+    torch.cuda.synchronize()
+    for k in range(8):
+        assert torch.equal(oa[k][1].view(torch.int64), wa.unit.view(torch.int64))
+        assert torch.equal(ob[k][1].view(torch.int64), wb.unit.view(torch.int64))
+        assert torch.equal(ob[k][0].view(torch.int64), wb.length.view(torch.int64))
+
+
+def test_graph_capture_takes_static_schedule(cuda_dev):
+    p = fn.preset("double")
+    x = _rows(1_000_000, 1)
+    want = fn.normalize3(p, x)
+    r, u = torch.empty_like(want.length), torch.empty_like(want.unit)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        fn.normalize3(p, x, out=(r, u))
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(3):
+                fn.normalize3(p, x, out=(r, u))
+    for _ in range(3):
+        r.zero_()
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(u.view(torch.int64), want.unit.view(torch.int64))
+    assert torch.equal(r.view(torch.int64), want.length.view(torch.int64))
+
+
+def test_static_and_dynamic_schedules_agree(cuda_dev, tmp_path):
+    """The same batches under FASTNORM_B200_DYN=0 (static) and =1 (dynamic wherever a
+    batch has more than S tiles per CTA, large ones included), in fresh processes."""
+    code = ("import sys, numpy as np, torch, paper_1606_06508_b200 as fn\n"
+            "from paper_1606_06508_b200 import workloads\n"
+            "p = fn.preset('double'); outs = []\n"
+            "for n in (1_000_000, 3_000_017, 1 << 25):\n"
+            "    x = torch.empty((n, 3), dtype=torch.float64, device='cuda'); workloads.generate_device(5, x)\n"
+            "    o = fn.normalize3(p, x); outs += [o.length.cpu().numpy(), o.unit.cpu().numpy().ravel()]\n"
+            "np.save(sys.argv[1], np.concatenate(outs))\n")
+    res = {}
+    for mode in ("0", "1"):
+        path = str(tmp_path / f"dyn{mode}.npy")
+        env = dict(os.environ, FASTNORM_B200_DYN=mode)
+        out = subprocess.run([sys.executable, "-c", code, path], env=env, capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        res[mode] = np.load(path)
+    assert np.array_equal(res["0"].view(np.uint64), res["1"].view(np.uint64))
