@@ -372,6 +372,7 @@ OTHER_CONFIGS = {  # config -> [(public API call, algorithmic bytes per row)]
     2: [("normalize2", 40), ("quotient2", 40)],
     3: [("normalize4_sq", 80), ("normalize4_rotation", 144)],
     4: [("normalize3", 28), ("quotient3_robust", 28)],
+    5: [("quotient3_robust", 56)],  # the headline's comparison variant (division-bound)
 }
 
 
@@ -465,7 +466,32 @@ def _batch_stream_rate(fn, p, x, bytes_per_row, peak, reps, sets=8, per_set=4):
                                  "frac": n * bytes_per_row / t_eager / 1e9 / peak}}
 
 
-def measure_other_configs(dev, reps: int = 5):
+_ISSUE_KEYS = {("quotient2", 2): "quotient2_f64_cfg2", ("normalize2", 2): "normalize2_f64_cfg2",
+               ("quotient3_robust", 4): "quotient3_f32_cfg4", ("quotient3_robust", 5): "quotient3_f64_cfg5"}
+
+
+def _issue_roofline(name: str, cfg: int, rows: int, t: float, clock_mhz):
+    """Instruction-issue roofline of a kernel: warp instructions per row (from the
+    committed ncu pass, profiles/ncu_issue.json, tools/ncu_issue.sh) x rows over the
+    issue peak -- one warp instruction per SMSP per cycle, 4 SMSPs x 148 SMs at the SM
+    clock sampled during this run -- against the measured launch time."""
+    key = _ISSUE_KEYS.get((name, cfg))
+    try:
+        with open(os.path.join(REPO, "profiles", "ncu_issue.json")) as f:
+            d = json.load(f)[key]
+    except Exception:
+        return None
+    clk = (clock_mhz or 1965.0) * 1e6
+    peak = 148 * 4 * clk  # warp instructions per second
+    achieved = d["warp_inst_per_row"] * rows / t
+    fp64 = d["fp64_warp_inst_per_row"] * rows / t
+    return {"bound": "issue", "achieved": achieved, "peak": peak, "unit": "warp inst/s", "frac": achieved / peak,
+            "warp_inst_per_row": d["warp_inst_per_row"], "fp64_warp_inst_per_row": d["fp64_warp_inst_per_row"],
+            "fp64_pipe_frac": fp64 / (peak / 2),  # the FP64 pipe takes a warp instruction every 2 cycles
+            "clock_mhz": clk / 1e6, "source": d["source"]}
+
+
+def measure_other_configs(dev, reps: int = 5, clocks_mhz=None):
     """Each BASELINE config's kernels through the public API: rows generated in HBM, L2
     evicted (a 512 MiB read) before every timed launch, CUDA events on the launching
     stream, median of `reps`."""
@@ -502,6 +528,9 @@ def measure_other_configs(dev, reps: int = 5):
             out.append({"config": cfg, "kernel": name, "rows": c.rows, "dtype": c.dtype,
                         "vectors_per_s": c.rows / t, "GB_per_s": c.rows * bpr / t / 1e9,
                         "frac": c.rows * bpr / t / 1e9 / peak, "ms": t * 1e3})
+            issue = _issue_roofline(name, cfg, c.rows, t, clocks_mhz)
+            if issue is not None:
+                out[-1]["issue_roofline"] = issue
             if cfg == 1:
                 out[-1]["stream_of_batches"] = _batch_stream_rate(fn, p, x, bpr, peak, reps)
         del x
@@ -734,7 +763,7 @@ def run_ours(args):
     }
     if world == 1 and not args.no_configs:
         try:
-            line["other_configs"] = measure_other_configs(dev)
+            line["other_configs"] = measure_other_configs(dev, clocks_mhz=(line.get("clocks") or {}).get("sm_mhz"))
         except Exception as exc:  # informational only: never lose the headline line
             line["other_configs"] = {"error": str(exc)}
     if world == 1 and not args.no_cpu_baseline:

@@ -189,30 +189,35 @@ template <int N> struct PaddedLdx {
     static constexpr int value = N == 3 ? 4 : 0;
 };
 
-// Dynamic tile schedule (tma_stream_kernel): one {next, done} counter pair per (device,
-// stream), allocated on a stream's first small batch and zeroed in stream order.  The
-// kernel's last CTA resets the pair, so consecutive launches on the stream reuse it;
-// launches on different streams never share one.  Used for batches of more than S but
-// at most kDynTilesPerCta tiles per CTA (config 1: 1e6 rows = 3906 tiles over 592 CTAs),
-// where the finish-time spread of a static round-robin is a visible share of the
-// launch; large batches keep the static schedule (no atomics).  Not
-// under stream capture: a graph could be replayed on several streams at once.
-// FASTNORM_B200_DYN=0 / 1 forces static / dynamic (when the batch has > S tiles per CTA).
-constexpr int64_t kDynTilesPerCta = 32;
-
-static int dyn_mode() {
-    static const int v = [] {
+// Dynamic tile schedule (tma_stream_kernel): two tile counters per (device, stream),
+// zeroed in stream order when the stream first uses them.  Launch i on the stream claims
+// from counter i % 2 and zeroes counter (i + 1) % 2 for launch i + 1 after its
+// griddepcontrol.wait, i.e. after launch i - 1 (the last user of that counter) is
+// complete.  The host takes i and launches under one lock, so the counter order matches
+// the stream order even when several threads launch on the same stream.  Launches on
+// different streams never share counters.  Batches with at most S tiles per CTA (nothing
+// to balance) and launches under stream capture (a graph could be replayed on several
+// streams at once) take the static schedule.  FASTNORM_B200_DYN=0 forces the static
+// schedule everywhere.
+static bool dyn_enabled() {
+    static const bool v = [] {
         const char* e = getenv("FASTNORM_B200_DYN");
-        return e ? atoi(e) : -1;
+        return !(e && strcmp(e, "0") == 0);
     }();
     return v;
 }
 
+struct SchedSlots {
+    int dev;
+    cudaStream_t stream;
+    unsigned* ctr;       // two counters
+    uint64_t launches;   // dynamic launches so far on this stream
+    std::mutex mu;       // held from taking a launch index to the launch itself
+};
 static std::mutex g_sched_mu;
-static std::vector<std::pair<std::pair<int, cudaStream_t>, unsigned*>>* g_sched =
-    new std::vector<std::pair<std::pair<int, cudaStream_t>, unsigned*>>();  // never destroyed
+static std::vector<std::unique_ptr<SchedSlots>>* g_sched = new std::vector<std::unique_ptr<SchedSlots>>();
 
-static unsigned* sched_pair(int dev, cudaStream_t stream) {
+static SchedSlots* sched_slots(int dev, cudaStream_t stream) {
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(stream, &cap) != cudaSuccess) {
         cudaGetLastError();
@@ -220,8 +225,8 @@ static unsigned* sched_pair(int dev, cudaStream_t stream) {
     }
     if (cap != cudaStreamCaptureStatusNone) return nullptr;
     std::lock_guard<std::mutex> lk(g_sched_mu);
-    for (auto& kv : *g_sched)
-        if (kv.first.first == dev && kv.first.second == stream) return kv.second;
+    for (auto& e : *g_sched)
+        if (e->dev == dev && e->stream == stream) return e.get();
     unsigned* p = nullptr;
     if (cudaMalloc(&p, 2 * sizeof(unsigned)) != cudaSuccess) {
         cudaGetLastError();
@@ -232,8 +237,13 @@ static unsigned* sched_pair(int dev, cudaStream_t stream) {
         cudaFree(p);
         return nullptr;
     }
-    g_sched->push_back({{dev, stream}, p});
-    return p;
+    std::unique_ptr<SchedSlots> e(new SchedSlots());
+    e->dev = dev;
+    e->stream = stream;
+    e->ctr = p;
+    e->launches = 0;
+    g_sched->push_back(std::move(e));
+    return g_sched->back().get();
 }
 
 template <typename T, int N, int OP, int LDX, bool MIS>
@@ -246,12 +256,19 @@ static cudaError_t launch_tma_as(const T* x, const T* x2, int64_t n, T* head, T*
     const int64_t resident = per_sm * sms;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, resident));
     KArgs<T> kd = ka;
-    kd.sched = nullptr;
-    const int mode = dyn_mode();
-    if (mode != 0 && ntiles > (int64_t)L::S * grid && (mode == 1 || ntiles <= kDynTilesPerCta * grid))
-        kd.sched = sched_pair(dev, stream);
-    return launch_pdl(TL::kernel(), grid, Tile<T, N>::kThreads, L::kSmemBytes, stream, x, x2, n, head, body, extra,
-                      kd);
+    kd.sched = kd.sched_next = nullptr;
+    SchedSlots* slots = (dyn_enabled() && ntiles > (int64_t)L::S * grid) ? sched_slots(dev, stream) : nullptr;
+    if (!slots)
+        return launch_pdl(TL::kernel(), grid, Tile<T, N>::kThreads, L::kSmemBytes, stream, x, x2, n, head, body,
+                          extra, kd);
+    std::lock_guard<std::mutex> lk(slots->mu);
+    const uint64_t i = slots->launches;
+    kd.sched = slots->ctr + (i & 1);
+    kd.sched_next = slots->ctr + ((i + 1) & 1);
+    const cudaError_t e = launch_pdl(TL::kernel(), grid, Tile<T, N>::kThreads, L::kSmemBytes, stream, x, x2, n,
+                                     head, body, extra, kd);
+    if (e == cudaSuccess) slots->launches = i + 1;
+    return e;
 }
 
 // MIS: the instantiation for inputs off the 16-byte grid (tma_stream_kernel).
@@ -766,15 +783,17 @@ struct Staging {
 // ---------------------------------------------------------------------------------
 // Parallel host memcpy for pageable callers: a small persistent worker pool copies the
 // slices of one job; jobs are serialised (host memory bandwidth is shared anyway).
-// FASTNORM_B200_COPY_THREADS (default min(16, 3/4 of the cores): 0.26 -> 0.68 Gvec/s for
-// pageable 3-D f64 rows on the 16-core B200 host, profiles/r01n_pageable.txt).
+// FASTNORM_B200_COPY_THREADS (default min(8, half the cores)).  On the 16-core B200 host
+// 8 threads copy pageable -> page-locked at 78 GB/s and leave cores to the caller and
+// the CUDA driver: the default call with pageable input runs at 1.17-1.18 G 3-D f64
+// rows/s with 6-8 threads, 1.00 with 12, 0.74 with 16 (profiles/r02e_host_sweep.txt).
 // ---------------------------------------------------------------------------------
 class CopyPool {
   public:
     CopyPool() {
         const int hw = (int)std::thread::hardware_concurrency();
         const char* e = getenv("FASTNORM_B200_COPY_THREADS");
-        nthreads_ = e ? std::max(1, atoi(e)) : std::max(1, std::min(16, hw * 3 / 4));
+        nthreads_ = e ? std::max(1, atoi(e)) : std::max(1, std::min(8, hw / 2));
         for (int k = 1; k < nthreads_; ++k) workers_.emplace_back([this, k] { work(k); });
     }
     ~CopyPool() {
@@ -1083,14 +1102,15 @@ static int host_run_impl(int op, int dim, int dtype, const void* x, const void* 
     // Input bytes per chunk (profiles/r01cs_chunks.txt, 3-D f64 rows):
     //  * page-locked callers: 48 MiB for large arrays, and at least 8 chunks of >= 4 MiB
     //    for mid-size ones so transfers and kernels of different chunks overlap;
-    //  * pageable callers: 8-16 MiB (each staging copy still gets the parallel copier).
+    //  * pageable callers: 8-32 MiB (32 MiB from 192 MiB of input up: 1.18 against 0.88
+    //    G rows/s at 16 MiB with page-locked outputs, profiles/r02e_host_sweep.txt).
     // FASTNORM_B200_HOST_CHUNK_MB fixes the chunk size instead.
     const int64_t row_in = (int64_t)((ldx + dim2) * w), in_total = n * row_in;
     int64_t chunk_bytes;
     if (getenv("FASTNORM_B200_HOST_CHUNK_MB")) {
         chunk_bytes = (int64_t)env_int("FASTNORM_B200_HOST_CHUNK_MB", 48, 1, 1024) << 20;
     } else if (staged) {
-        chunk_bytes = std::max<int64_t>((int64_t)8 << 20, std::min<int64_t>((int64_t)16 << 20, in_total / 3));
+        chunk_bytes = std::max<int64_t>((int64_t)8 << 20, std::min<int64_t>((int64_t)32 << 20, in_total / 6));
     } else {
         chunk_bytes = std::max<int64_t>((int64_t)4 << 20, std::min<int64_t>((int64_t)48 << 20, in_total / 8));
     }
@@ -1267,7 +1287,7 @@ int host_run_soa(int op, int dim, int dtype, const void* const* xs, int64_t n, v
     if (getenv("FASTNORM_B200_HOST_CHUNK_MB")) {
         chunk_bytes = (int64_t)env_int("FASTNORM_B200_HOST_CHUNK_MB", 48, 1, 1024) << 20;
     } else if (staged) {
-        chunk_bytes = std::max<int64_t>((int64_t)8 << 20, std::min<int64_t>((int64_t)16 << 20, in_total / 3));
+        chunk_bytes = std::max<int64_t>((int64_t)8 << 20, std::min<int64_t>((int64_t)32 << 20, in_total / 6));
     } else {
         chunk_bytes = std::max<int64_t>((int64_t)4 << 20, std::min<int64_t>((int64_t)48 << 20, in_total / 8));
     }

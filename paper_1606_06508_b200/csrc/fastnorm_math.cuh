@@ -18,6 +18,7 @@
 // every row holding a NaN; the zero branch is taken iff every component is +-0.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace fnb {
@@ -116,8 +117,9 @@ template <typename T> struct KArgs {
     int k_min, k_max;   // log2(sigma_min), log2(sigma_max) when pow2 (validated sets)
     bool pow2;          // sigma_min, sigma_max and their inverses are powers of two
     unsigned long long* invalid;  // rows rejected by the rotations (may be NULL)
-    unsigned* sched;              // tma_stream_kernel's dynamic tile schedule {next, done}
-                                  // (NULL: the static round-robin schedule)
+    unsigned* sched;              // tma_stream_kernel's dynamic tile counter (NULL: the
+                                  // static round-robin schedule)
+    unsigned* sched_next;         // the counter of the next launch on the stream (zeroed here)
     T rot[9];           // FN_OP_ROT_APPLY: the matrix, row-major
 };
 
@@ -232,9 +234,11 @@ struct MarksteinDivider {
 
 // Quotients that land on the subnormal grid (or flush to zero), computed exactly without
 // the library division's generic slow path.  Preconditions: a finite, b finite normal
-// (biased exponent 1..2046), and the normalised exponent gap ea - eb <= -1024, so
-// |a/b| < 2^-1023 and RN(a/b) = n 2^-1074 with n = RN_int(X), X = (fa / fb) 2^s,
-// fa, fb in [1, 2), s = ea - eb + 1074 <= 50:
+// (biased exponent 1..2046), and the normalised exponent gap ea - eb <= -1023, so
+// |a/b| < 2^-1022 and RN(a/b) = n 2^-1074 with n = RN_int(X), X = (fa / fb) 2^s,
+// fa, fb in [1, 2), s = ea - eb + 1074 <= 51 (for s = 51, X < 2^52, RN(A/fb) is within
+// 2^-2 of X and |r| <= 1.5 stays exact; n = 2^52 is the bit pattern of 2^-1022, the
+// correct result when X rounds up onto the normal range):
 //   s <= -2 : X < 1/2, n = 0;
 //   s == -1 : X in (1/4, 1), n = [fa > fb] (X == 1/2 only if fa == fb: tie -> 0, even);
 //   s >=  0 : n0 = rint(RN(A / fb)), A = fa 2^s; |RN(A/fb) - X| <= 2^-3, so n0 is off by
@@ -260,6 +264,26 @@ __device__ __forceinline__ double tiny_quotient(double a, double b, int ea, unsi
         n = __double2ll_rn(n0);
     }
     return __longlong_as_double((long long)((unsigned long long)n | sign));
+}
+
+// a / b for a finite b >= 2^-1022 whose caller already knows whether the quotient lies
+// on the subnormal grid: tiny lanes (|a| / b < 2^-1022 by exponents, or a == 0) go to
+// tiny_quotient (exact, no library slow path), the rest to __ddiv_rn.  Used by the
+// pivoted quotient rows (FNB_QUOTIENT_TINY).
+__device__ __forceinline__ double div_known_tiny(double a, double b, int eb, bool tiny) {
+    if (tiny) {
+        const unsigned long long ba = (unsigned long long)__double_as_longlong(a) & 0x7FFFFFFFFFFFFFFFull;
+        if (ba == 0) return signed_zero_of_quotient(a, b);
+        int ea = (int)(ba >> 52);
+        unsigned long long ma = ba & 0x000FFFFFFFFFFFFFull;
+        if (ea == 0) {  // subnormal numerator: normalise the significand
+            const int lz = __clzll((long long)ma) - 11;
+            ma = (ma << lz) & 0x000FFFFFFFFFFFFFull;
+            ea = 1 - lz;
+        }
+        return tiny_quotient(a, b, ea, ma, eb);
+    }
+    return __ddiv_rn(a, b);
 }
 
 // IEEE quotient when an operand is zero, infinite or NaN (the cases a library division
@@ -580,6 +604,28 @@ __device__ __forceinline__ void naive_row(const T (&x)[N], T& r, T (&u)[N]) {
 
 // quotient{2,3,4}: _kernels.pyx:288-362 (Alg 1 generalised).  m = max via strict '>',
 // zero row (no NaN) -> all +0 (n = 4: five zeros, no identity quaternion).
+//
+// FNB_QUOTIENT_PIVOT = 1 (default) computes the same IEEE results with n - 1 divisions
+// per stage instead of n.  For a row with finite m > 0, a component with |x_j| == m has
+// x_j / m = +-1 exactly and x_j / m / h = +-RN(1/h) (rounding is sign-symmetric), so only
+// the other n - 1 components are divided, the reciprocal of h is one correctly rounded
+// __drcp_rn / __frcp_rn, and the sum of squares is still formed in the reference's left-
+// to-right order over all n quotients.  Like quotient3_fast_row, the row's operands are
+// selected first (the other components in their original order) so every lane of a warp
+// runs the same n - 1 division sites whichever component is largest: on wide-range rows,
+// where quotients land on the subnormal grid, each site with such a lane costs the warp
+// one pass of the library division's slow path.  Rows with a NaN or an infinity give NaN
+// everywhere (NaN / m, inf / inf), as the reference's arithmetic does; the zero row gives
+// zeros.  FNB_QUOTIENT_PIVOT = 0 is the literal transcription kept for A/B timing.
+#ifndef FNB_QUOTIENT_PIVOT
+#define FNB_QUOTIENT_PIVOT 1
+#endif
+#ifndef FNB_QUOTIENT_H_MARKSTEIN
+#define FNB_QUOTIENT_H_MARKSTEIN 0
+#endif
+#ifndef FNB_QUOTIENT_TINY
+#define FNB_QUOTIENT_TINY 0
+#endif
 template <typename T, int N>
 __device__ __forceinline__ void quotient_row(const T (&x)[N], T& r, T (&u)[N]) {
     using F = Fp<T>;
@@ -592,6 +638,84 @@ __device__ __forceinline__ void quotient_row(const T (&x)[N], T& r, T (&u)[N]) {
     bool anynan = false;
 #pragma unroll
     for (int k = 0; k < N; ++k) anynan = anynan || F::isnan_(x[k]);
+#if FNB_QUOTIENT_PIVOT
+  if constexpr (std::is_same<T, double>::value) {  // binary32 quotients are one binary64
+    // product each (Divider<float>): the pivot's selects cost more than they save there
+    // finite m > 0 and no NaN: every component finite (an infinity would be m)
+    const bool regular = !anynan && m > T(0) && isfinite(m);
+    int j = N - 1;  // first component of magnitude m
+#pragma unroll
+    for (int k = N - 2; k >= 0; --k)
+        if (F::abs(x[k]) == m) j = k;
+    T o[N - 1];  // the other components, original order
+#pragma unroll
+    for (int i = 0; i < N - 1; ++i) o[i] = (i < j) ? x[i] : x[i + 1];
+    T qo[N - 1];
+#if FNB_QUOTIENT_TINY
+    // quotients below 2^-1022 (exponent gap to m of -1023 or less, or a zero component)
+    // take tiny_quotient instead of the library division's slow path
+    const T mm = regular ? m : T(1);
+    const int em = biased_exp(mm);
+#pragma unroll
+    for (int i = 0; i < N - 1; ++i) {
+        const T a = regular ? o[i] : T(0);
+        qo[i] = div_known_tiny(a, mm, em, em >= 1 && biased_exp(a) - em <= -1023);
+    }
+#else
+    const Divider<T> by_m(regular ? m : T(1));
+#pragma unroll
+    for (int i = 0; i < N - 1; ++i) qo[i] = by_m(regular ? o[i] : T(0));
+#endif
+    T sj = x[0];
+#pragma unroll
+    for (int k = 1; k < N; ++k) sj = (k == j) ? x[k] : sj;
+    sj = F::sign1(sj);
+    T q[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        T v = sj;
+        if (k < N - 1) v = (k < j) ? qo[k < N - 1 ? k : 0] : v;
+        if (k > 0) v = (k > j) ? qo[k > 0 ? k - 1 : 0] : v;
+        q[k] = v;
+    }
+    const T h = F::sqrt(sum_squares<T, N>(q));
+    r = F::mul(m, h);
+    const T y = F::rcp(h);
+    T uo[N - 1];
+#if FNB_QUOTIENT_TINY
+    // h in [1, 2]: a subnormal (or zero) q gives a quotient below 2^-1022
+    const int eh = biased_exp(h);
+#pragma unroll
+    for (int i = 0; i < N - 1; ++i) uo[i] = div_known_tiny(qo[i], h, eh, biased_exp(qo[i]) == 0);
+#elif FNB_QUOTIENT_H_MARKSTEIN
+    // h in [1, 2]: the shared-reciprocal Markstein division (y = RN(1/h) is needed for
+    // the pivot anyway), the library division only for tiny numerators
+    const MarksteinDivider by_h(h);
+#pragma unroll
+    for (int i = 0; i < N - 1; ++i) uo[i] = by_h(qo[i]);
+#else
+    const Divider<T> by_h(h);
+#pragma unroll
+    for (int i = 0; i < N - 1; ++i) uo[i] = by_h(qo[i]);
+#endif
+    const T uj = F::mul(sj, y);
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        T v = uj;
+        if (k < N - 1) v = (k < j) ? uo[k < N - 1 ? k : 0] : v;
+        if (k > 0) v = (k > j) ? uo[k > 0 ? k - 1 : 0] : v;
+        u[k] = v;
+    }
+    if (!regular) {
+        const T fill = anynan || m > T(0) ? T(NAN) : T(0);  // NaN / infinity rows, zero row
+        r = fill;
+#pragma unroll
+        for (int k = 0; k < N; ++k) u[k] = fill;
+    }
+    return;
+  }
+#endif
+    {  // the literal transcription: binary32, or FNB_QUOTIENT_PIVOT = 0
     if (m == T(0) && !anynan) {
         r = T(0);
 #pragma unroll
@@ -607,6 +731,7 @@ __device__ __forceinline__ void quotient_row(const T (&x)[N], T& r, T (&u)[N]) {
     const Divider<T> by_h(h);
 #pragma unroll
     for (int k = 0; k < N; ++k) u[k] = by_h(q[k]);
+    }
 }
 
 // Shared body of the pivoted fast quotient (_kernels.pyx:370-377 and siblings):

@@ -590,17 +590,17 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
     const unsigned char* x2a = reinterpret_cast<const unsigned char*>(x2) - mis2;
     const uint32_t load_bytes = L::kInBytes + (MIS && mis ? 16 : 0);
     const uint32_t load2_bytes = L::kIn2Bytes + (MIS && mis2 ? 16 : 0);
-    // Schedule.  Static (the default): CTA b owns tiles b, b + grid, b + 2 grid, ...
-    // Dynamic (ka.sched != NULL; small batches of a few tiles per CTA, where uneven
-    // per-CTA progress leaves a tail of CTAs still working on their last tile while the
-    // others are idle): every CTA's first S tiles are the static ones (no atomic on the
-    // critical start), then its leader claims further tiles from a counter in global
-    // memory as it refills a stage, S tiles ahead of use.  The tile id of each stage
-    // travels to the CTA's threads through s_tile[], written before the stage's
+    // Schedule.  Static: CTA b owns tiles b, b + grid, b + 2 grid, ...
+    // Dynamic (ka.sched != NULL): every CTA's first S tiles are the static ones (no atomic
+    // on the critical start), then its leader claims further tiles from a counter in
+    // global memory, one claim ahead of use so the atomic's round trip overlaps a tile of
+    // work; CTAs that run ahead take more tiles and all finish together.  The tile id of
+    // each stage travels to the CTA's threads through s_tile[], written before the stage's
     // mbarrier arrive (release) and read after its wait (acquire); -1 = no more tiles.
-    // The last CTA to finish resets the counter pair for the next launch on the stream
-    // (the host hands every stream its own pair; launches on one stream run in order,
-    // and a PDL successor's griddepcontrol.wait sees the reset).
+    // Counters: the host gives every (device, stream) a pair and alternates launches
+    // between them; each launch zeroes the other one (the next launch's) once its
+    // griddepcontrol.wait has returned, so no launch ends with atomics and a successor
+    // (stream order, PDL included) always starts from zero.
     unsigned* const sched = ka.sched;
     const bool dyn = sched != nullptr;
     __shared__ int64_t s_tile[S];
@@ -610,9 +610,16 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
     uint64_t policy = 0;
     unsigned long long bad = 0;
     bool claiming = true;  // leader: no -1 claimed yet
+    unsigned ahead = 0;    // leader: the counter value for the next dynamic fill, claimed one
+                           // fill early so the atomic's round trip overlaps a tile of work
     auto claim = [&](int64_t k) -> int64_t {  // tile of the CTA's k-th stage fill (leader)
-        const int64_t t = k < S ? (int64_t)blockIdx.x + k * gridDim.x
-                                : (int64_t)S * gridDim.x + (int64_t)atomicAdd(&sched[0], 1u);
+        int64_t t;
+        if (k < S) {
+            t = (int64_t)blockIdx.x + k * gridDim.x;
+        } else {
+            t = (int64_t)S * gridDim.x + (int64_t)ahead;
+            if (t < ntiles) ahead = atomicAdd(&sched[0], 1u);
+        }
         return t < ntiles ? t : -1;
     };
 
@@ -625,6 +632,7 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
     __syncthreads();
     grid_dependency_wait();
     grid_launch_dependents();
+    if (dyn && blockIdx.x == 0 && threadIdx.x == 0) *ka.sched_next = 0u;
     timeline_mark(1);
     // One stage = the tile's input records (and its second-input records), one mbarrier.
     auto load_stage = [&](int st, int64_t tile) {
@@ -658,6 +666,7 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
     if (leader) {
         if (dyn) {
             for (int k = 0; k < S; ++k) fill_dyn(k, k);
+            if (claiming) ahead = atomicAdd(&sched[0], 1u);
         } else {
             for (int64_t k = 0; k < my_tiles && k < S; ++k) load_stage((int)k, (int64_t)blockIdx.x + k * gridDim.x);
         }
@@ -722,13 +731,6 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
             // k+2-OB must have been read out by then: at most OB-2 groups stay pending.
             bulk_wait_read<OB - 2>();
             timeline_tile(k, 2, true);
-        }
-    }
-    if (dyn && leader) {  // the last CTA out resets the pair for the next launch
-        __threadfence();
-        if (atomicAdd(&sched[1], 1u) == gridDim.x - 1) {
-            atomicExch(&sched[0], 0u);
-            atomicExch(&sched[1], 0u);
         }
     }
 
