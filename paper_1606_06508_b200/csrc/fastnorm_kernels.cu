@@ -265,6 +265,9 @@ static cudaError_t launch_tma_as(const T* x, const T* x2, int64_t n, T* head, T*
     const uint64_t i = slots->launches;
     kd.sched = slots->ctr + (i & 1);
     kd.sched_next = slots->ctr + ((i + 1) & 1);
+    // tiles per claim: 1 for a few tiles per CTA (balance matters most), up to 8 for
+    // long runs (at ~2 ns per tile GPU-wide, one claim per tile contends on the counter)
+    kd.sched_batch = (int)std::max<int64_t>(1, std::min<int64_t>(8, ntiles / ((int64_t)grid * 128)));
     const cudaError_t e = launch_pdl(TL::kernel(), grid, Tile<T, N>::kThreads, L::kSmemBytes, stream, x, x2, n,
                                      head, body, extra, kd);
     if (e == cudaSuccess) slots->launches = i + 1;
@@ -783,17 +786,20 @@ struct Staging {
 // ---------------------------------------------------------------------------------
 // Parallel host memcpy for pageable callers: a small persistent worker pool copies the
 // slices of one job; jobs are serialised (host memory bandwidth is shared anyway).
-// FASTNORM_B200_COPY_THREADS (default min(8, half the cores)).  On the 16-core B200 host
-// 8 threads copy pageable -> page-locked at 78 GB/s and leave cores to the caller and
-// the CUDA driver: the default call with pageable input runs at 1.17-1.18 G 3-D f64
-// rows/s with 6-8 threads, 1.00 with 12, 0.74 with 16 (profiles/r02e_host_sweep.txt).
+// The pool has FASTNORM_B200_COPY_THREADS workers (default min(16, cores)); a job may
+// use fewer.  On the 16-core B200 host (2^28 3-D f64 rows, profiles/r02h_host_sweep.txt):
+// with the outputs staged too, all 16 threads do best (0.80 G rows/s, 0.73 with 12);
+// when only the input is staged (page-locked outputs, e.g. the library's own result
+// pool), half of them do best (1.50 G rows/s with 8 of 16, 1.40 with 6 of 12, 1.22
+// with 4 of 8, 0.97 with all 12) -- more copy threads compete with the concurrent DMA
+// traffic and the driver's threads.
 // ---------------------------------------------------------------------------------
 class CopyPool {
   public:
     CopyPool() {
         const int hw = (int)std::thread::hardware_concurrency();
         const char* e = getenv("FASTNORM_B200_COPY_THREADS");
-        nthreads_ = e ? std::max(1, atoi(e)) : std::max(1, std::min(8, hw / 2));
+        nthreads_ = e ? std::max(1, atoi(e)) : std::max(1, std::min(16, hw));
         for (int k = 1; k < nthreads_; ++k) workers_.emplace_back([this, k] { work(k); });
     }
     ~CopyPool() {
@@ -804,8 +810,11 @@ class CopyPool {
         cv_.notify_all();
         for (auto& t : workers_) t.join();
     }
-    void copy(void* dst, const void* src, size_t bytes) {
-        if (bytes < ((size_t)4 << 20) || nthreads_ == 1) {
+    int threads() const { return nthreads_; }
+    // Copies with at most max_threads threads (the caller's included).
+    void copy(void* dst, const void* src, size_t bytes, int max_threads = 1 << 30) {
+        const int use = std::max(1, std::min(nthreads_, max_threads));
+        if (bytes < ((size_t)4 << 20) || use == 1) {
             memcpy(dst, src, bytes);
             return;
         }
@@ -815,7 +824,8 @@ class CopyPool {
             dst_ = static_cast<char*>(dst);
             src_ = static_cast<const char*>(src);
             bytes_ = bytes;
-            pending_ = nthreads_ - 1;
+            active_ = use;
+            pending_ = use - 1;
             ++gen_;
         }
         cv_.notify_all();
@@ -826,7 +836,7 @@ class CopyPool {
 
   private:
     void slice(int k) {
-        const size_t per = (bytes_ / nthreads_ + 63) & ~(size_t)63;
+        const size_t per = (bytes_ / active_ + 63) & ~(size_t)63;
         const size_t lo = std::min(bytes_, per * k), hi = std::min(bytes_, per * (k + 1));
         if (hi > lo) memcpy(dst_ + lo, src_ + lo, hi - lo);
     }
@@ -838,6 +848,7 @@ class CopyPool {
                 cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
                 if (stop_) return;
                 seen = gen_;
+                if (k >= active_) continue;  // not part of this job
             }
             slice(k);
             std::lock_guard<std::mutex> lk(mu_);
@@ -851,15 +862,26 @@ class CopyPool {
     char* dst_ = nullptr;
     const char* src_ = nullptr;
     size_t bytes_ = 0;
+    int active_ = 1;
     int pending_ = 0;
     uint64_t gen_ = 0;
     bool stop_ = false;
 };
 
+static int copy_pool_threads();
+
+// Threads for one staging copy: every worker when the call stages its outputs too,
+// about half of them (6 of 12) when only the input is staged.
+static int copy_threads(bool stage_out) {
+    return stage_out ? 1 << 30 : std::max(1, (copy_pool_threads() + 1) / 2);
+}
+
 static CopyPool& copy_pool() {
     static CopyPool pool;
     return pool;
 }
+
+static int copy_pool_threads() { return copy_pool().threads(); }
 
 static bool is_page_locked(const void* p) {
     if (!p) return true;
@@ -1165,7 +1187,7 @@ static int host_run_impl(int op, int dim, int dtype, const void* x, const void* 
         const char* src = static_cast<const char*>(x) + r0 * ldx * w;
         const size_t in_bytes = ((m - 1) * ldx + dim) * w;
         if (stage_in) {
-            copy_pool().copy(hbase, src, in_bytes);
+            copy_pool().copy(hbase, src, in_bytes, copy_threads(stage_out));
             src = hbase;
         }
         e = cudaMemcpyAsync(dx, src, in_bytes, cudaMemcpyHostToDevice, s);
@@ -1174,7 +1196,7 @@ static int host_run_impl(int op, int dim, int dtype, const void* x, const void* 
             void* dx2 = base + bx;
             const char* src2 = static_cast<const char*>(x2) + r0 * dim2 * w;
             if (stage_in2) {
-                copy_pool().copy(hbase + bx, src2, m * dim2 * w);
+                copy_pool().copy(hbase + bx, src2, m * dim2 * w, copy_threads(stage_out));
                 src2 = hbase + bx;
             }
             e = cudaMemcpyAsync(dx2, src2, m * dim2 * w, cudaMemcpyHostToDevice, s);
@@ -1333,7 +1355,7 @@ int host_run_soa(int op, int dim, int dtype, const void* const* xs, int64_t n, v
         for (int c = 0; c < dim; ++c) {
             const char* src = static_cast<const char*>(xs[c]) + r0 * w;
             if (stage_in) {
-                copy_pool().copy(hbase + (size_t)c * arr, src, m * w);
+                copy_pool().copy(hbase + (size_t)c * arr, src, m * w, copy_threads(stage_out));
                 src = hbase + (size_t)c * arr;
             }
             e = cudaMemcpyAsync(base + (size_t)c * arr, src, m * w, cudaMemcpyHostToDevice, s);

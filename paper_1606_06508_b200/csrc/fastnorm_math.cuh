@@ -120,6 +120,7 @@ template <typename T> struct KArgs {
     unsigned* sched;              // tma_stream_kernel's dynamic tile counter (NULL: the
                                   // static round-robin schedule)
     unsigned* sched_next;         // the counter of the next launch on the stream (zeroed here)
+    int sched_batch;              // tiles per claim of the dynamic schedule
     T rot[9];           // FN_OP_ROT_APPLY: the matrix, row-major
 };
 
@@ -264,26 +265,6 @@ __device__ __forceinline__ double tiny_quotient(double a, double b, int ea, unsi
         n = __double2ll_rn(n0);
     }
     return __longlong_as_double((long long)((unsigned long long)n | sign));
-}
-
-// a / b for a finite b >= 2^-1022 whose caller already knows whether the quotient lies
-// on the subnormal grid: tiny lanes (|a| / b < 2^-1022 by exponents, or a == 0) go to
-// tiny_quotient (exact, no library slow path), the rest to __ddiv_rn.  Used by the
-// pivoted quotient rows (FNB_QUOTIENT_TINY).
-__device__ __forceinline__ double div_known_tiny(double a, double b, int eb, bool tiny) {
-    if (tiny) {
-        const unsigned long long ba = (unsigned long long)__double_as_longlong(a) & 0x7FFFFFFFFFFFFFFFull;
-        if (ba == 0) return signed_zero_of_quotient(a, b);
-        int ea = (int)(ba >> 52);
-        unsigned long long ma = ba & 0x000FFFFFFFFFFFFFull;
-        if (ea == 0) {  // subnormal numerator: normalise the significand
-            const int lz = __clzll((long long)ma) - 11;
-            ma = (ma << lz) & 0x000FFFFFFFFFFFFFull;
-            ea = 1 - lz;
-        }
-        return tiny_quotient(a, b, ea, ma, eb);
-    }
-    return __ddiv_rn(a, b);
 }
 
 // IEEE quotient when an operand is zero, infinite or NaN (the cases a library division
@@ -617,15 +598,17 @@ __device__ __forceinline__ void naive_row(const T (&x)[N], T& r, T (&u)[N]) {
 // one pass of the library division's slow path.  Rows with a NaN or an infinity give NaN
 // everywhere (NaN / m, inf / inf), as the reference's arithmetic does; the zero row gives
 // zeros.  FNB_QUOTIENT_PIVOT = 0 is the literal transcription kept for A/B timing.
+// Measured (tools/ab_quotient.sh, profiles/r02e_ab_quotient.txt, r02f_ab_quotient.txt):
+// quotient2 config 2 2226 -> 3260 GB/s, quotient3 config 5 2134 -> 2624, quotient4
+// config 3 5812 -> 6042, quotient3 config 1 5761 -> 5885.  Binary32 keeps the literal
+// form (pivot: 4655 -> 4424 GB/s on config 4).  Also measured and dropped: the Markstein
+// division by h with the shared reciprocal (-4 % on configs 2 and 5), and routing the
+// quotients below 2^-1022 to tiny_quotient by exponent gap (-11 % on config 2, -13 % on
+// config 5: the extra path is longer than the library's slow path it replaces).
 #ifndef FNB_QUOTIENT_PIVOT
 #define FNB_QUOTIENT_PIVOT 1
 #endif
-#ifndef FNB_QUOTIENT_H_MARKSTEIN
-#define FNB_QUOTIENT_H_MARKSTEIN 0
-#endif
-#ifndef FNB_QUOTIENT_TINY
-#define FNB_QUOTIENT_TINY 0
-#endif
+
 template <typename T, int N>
 __device__ __forceinline__ void quotient_row(const T (&x)[N], T& r, T (&u)[N]) {
     using F = Fp<T>;
@@ -651,21 +634,9 @@ __device__ __forceinline__ void quotient_row(const T (&x)[N], T& r, T (&u)[N]) {
 #pragma unroll
     for (int i = 0; i < N - 1; ++i) o[i] = (i < j) ? x[i] : x[i + 1];
     T qo[N - 1];
-#if FNB_QUOTIENT_TINY
-    // quotients below 2^-1022 (exponent gap to m of -1023 or less, or a zero component)
-    // take tiny_quotient instead of the library division's slow path
-    const T mm = regular ? m : T(1);
-    const int em = biased_exp(mm);
-#pragma unroll
-    for (int i = 0; i < N - 1; ++i) {
-        const T a = regular ? o[i] : T(0);
-        qo[i] = div_known_tiny(a, mm, em, em >= 1 && biased_exp(a) - em <= -1023);
-    }
-#else
     const Divider<T> by_m(regular ? m : T(1));
 #pragma unroll
     for (int i = 0; i < N - 1; ++i) qo[i] = by_m(regular ? o[i] : T(0));
-#endif
     T sj = x[0];
 #pragma unroll
     for (int k = 1; k < N; ++k) sj = (k == j) ? x[k] : sj;
@@ -682,22 +653,9 @@ __device__ __forceinline__ void quotient_row(const T (&x)[N], T& r, T (&u)[N]) {
     r = F::mul(m, h);
     const T y = F::rcp(h);
     T uo[N - 1];
-#if FNB_QUOTIENT_TINY
-    // h in [1, 2]: a subnormal (or zero) q gives a quotient below 2^-1022
-    const int eh = biased_exp(h);
-#pragma unroll
-    for (int i = 0; i < N - 1; ++i) uo[i] = div_known_tiny(qo[i], h, eh, biased_exp(qo[i]) == 0);
-#elif FNB_QUOTIENT_H_MARKSTEIN
-    // h in [1, 2]: the shared-reciprocal Markstein division (y = RN(1/h) is needed for
-    // the pivot anyway), the library division only for tiny numerators
-    const MarksteinDivider by_h(h);
-#pragma unroll
-    for (int i = 0; i < N - 1; ++i) uo[i] = by_h(qo[i]);
-#else
     const Divider<T> by_h(h);
 #pragma unroll
     for (int i = 0; i < N - 1; ++i) uo[i] = by_h(qo[i]);
-#endif
     const T uj = F::mul(sj, y);
 #pragma unroll
     for (int k = 0; k < N; ++k) {

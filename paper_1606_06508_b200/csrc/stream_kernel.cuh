@@ -593,8 +593,9 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
     // Schedule.  Static: CTA b owns tiles b, b + grid, b + 2 grid, ...
     // Dynamic (ka.sched != NULL): every CTA's first S tiles are the static ones (no atomic
     // on the critical start), then its leader claims further tiles from a counter in
-    // global memory, one claim ahead of use so the atomic's round trip overlaps a tile of
-    // work; CTAs that run ahead take more tiles and all finish together.  The tile id of
+    // global memory, ka.sched_batch consecutive tiles per claim and one claim ahead of
+    // use, so the atomic's round trip overlaps tiles of work; CTAs that run ahead take
+    // more tiles and all finish within a batch of each other.  The tile id of
     // each stage travels to the CTA's threads through s_tile[], written before the stage's
     // mbarrier arrive (release) and read after its wait (acquire); -1 = no more tiles.
     // Counters: the host gives every (device, stream) a pair and alternates launches
@@ -610,15 +611,21 @@ __global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x,
     uint64_t policy = 0;
     unsigned long long bad = 0;
     bool claiming = true;  // leader: no -1 claimed yet
-    unsigned ahead = 0;    // leader: the counter value for the next dynamic fill, claimed one
-                           // fill early so the atomic's round trip overlaps a tile of work
+    unsigned ahead = 0;    // leader: the next batch of the dynamic schedule, claimed one
+                           // batch early so the atomic's round trip overlaps tiles of work
+    int64_t cur = 0, end = 0;  // leader: the batch being handed out, [cur, end)
+    const int batch = dyn ? ka.sched_batch : 1;  // tiles per claim (fewer atomics on big runs)
     auto claim = [&](int64_t k) -> int64_t {  // tile of the CTA's k-th stage fill (leader)
         int64_t t;
         if (k < S) {
             t = (int64_t)blockIdx.x + k * gridDim.x;
         } else {
-            t = (int64_t)S * gridDim.x + (int64_t)ahead;
-            if (t < ntiles) ahead = atomicAdd(&sched[0], 1u);
+            if (cur == end) {
+                cur = (int64_t)S * gridDim.x + (int64_t)ahead * batch;
+                end = cur + batch;
+                if (cur < ntiles) ahead = atomicAdd(&sched[0], 1u);
+            }
+            t = cur++;
         }
         return t < ntiles ? t : -1;
     };

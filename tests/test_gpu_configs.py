@@ -113,6 +113,31 @@ def test_cfg2_scaling_and_quotient_full(cuda_dev):
     assert st[3] > 0 and st[4] > 0 and st[5] > 0        # all three scaling classes occur
 
 
+def _two_prod_sq(a):
+    """a*a as hi + lo exactly (Dekker's split; |a| far from overflow)."""
+    p = a * a
+    c = 134217729.0 * a
+    ah = c - (c - a)
+    al = a - ah
+    return p, ((ah * ah - p) + 2.0 * ah * al) + al * al
+
+
+def _two_sum(a, b):
+    s = a + b
+    bb = s - a
+    return s, (a - (s - bb)) + (b - bb)
+
+
+def _dd_sum_squares(x):
+    """Double-double sum of squares of each row of x (float64 [n, k])."""
+    hi, lo = _two_prod_sq(x[:, 0])
+    for k in range(1, x.shape[1]):
+        p, e = _two_prod_sq(x[:, k])
+        hi, t = _two_sum(hi, p)
+        lo = lo + t + e
+    return _two_sum(hi, lo)
+
+
 def test_cfg3_quaternion_sq_full(cuda_dev):
     p = fn.preset("double")
     ka = np.array(fn.kernel_args(p))
@@ -133,6 +158,17 @@ def test_cfg3_quaternion_sq_full(cuda_dev):
     for row, s in zip(xs.tolist(), sq.tolist()):
         exact = sum(Fraction(v) ** 2 for v in row)
         assert abs(Fraction(s) - exact) <= 5 * u * exact
+    # ... and on every row of the config (2^27) against a double-double sum of squares
+    # (Dekker products, two-sum accumulation: relative error ~2^-100, far inside 5u)
+    worst = 0.0
+    for lo in range(0, x.shape[0], 1 << 23):
+        xr = to_np(x[lo:lo + (1 << 23)])
+        sr = to_np(res.squared_length[lo:lo + (1 << 23)])
+        hi_s, lo_s = _dd_sum_squares(xr)
+        d = (sr - hi_s) - lo_s  # sr - hi_s is exact (Sterbenz)
+        rel = np.abs(d) / hi_s
+        worst = max(worst, float(rel.max()))
+    assert worst <= 5 * 2.0 ** -53 * (1 + 2.0 ** -40), worst
 
 
 def test_cfg4_f32_full(cuda_dev):

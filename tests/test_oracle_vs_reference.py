@@ -126,3 +126,34 @@ def test_hypothesis_rows_vs_reference(dim, prec, data):
                               min_size=1, max_size=8))
     x = np.array(vals, dtype=np.float64 if prec == "f64" else np.float32)
     _rows_vs_reference(x, prec, dim)
+
+
+def _sample_vs_reference(x: np.ndarray, prec: str, dim: int, fam: str):
+    """Vectorised form of _rows_vs_reference for large samples: the reference's compiled
+    export called row by row, compared with the oracle as arrays (the _same rule)."""
+    ka = KA[prec]
+    f = getattr(REF, kernel_name(fam, dim, prec))
+    rows = x.astype(np.float64).tolist()
+    want = np.array([f(*ka, *row) for row in rows] if fam in SCALING else [f(*row) for row in rows],
+                    dtype=np.float64).reshape(len(rows), -1)
+    h, b, _ = oracle.run(oracle.BASE_OPS[fam], x, ka if fam in SCALING else None)
+    got = h[:, None].astype(np.float64) if b is None else np.concatenate([h[:, None], b], axis=1).astype(np.float64)
+    both_nan = np.isnan(got) & np.isnan(want)
+    same = both_nan | ((got == want) & (np.signbit(got) == np.signbit(want)))
+    bad = np.flatnonzero(~same.all(axis=1))
+    assert bad.size == 0, (fam, prec, bad[:5], x[bad[:5]], got[bad[:5]], want[bad[:5]])
+
+
+@pytest.mark.parametrize("cfg,rows", [(1, 1 << 20), (2, 1 << 20), (3, 1 << 20), (4, 1 << 22), (5, 1 << 22)])
+def test_workload_sample_vs_reference(cfg, rows):
+    """A 4-million-row sample of configs 4 and 5 (whose full-size parity reaches the
+    reference only through the oracle: their NaN / infinity / overflowing rows make the
+    reference's loop checksums uninformative) and 2^20 rows of configs 1-3, normalize
+    family, plus the quotient variant the config runs: the oracle equals the reference's
+    compiled exports on every row."""
+    c = workloads.CONFIGS[cfg]
+    prec = "f64" if c.dtype == "float64" else "f32"
+    x = workloads.host_rows(cfg, 777 * cfg, rows)
+    _sample_vs_reference(x, prec, c.dim, "normalize")
+    if cfg in (2, 4):
+        _sample_vs_reference(x[: rows // 4], prec, c.dim, "quotient")

@@ -34,7 +34,7 @@ def run_one(a):
 
     from paper_1606_06508_b200 import batch, workloads
 
-    L = ctypes.CDLL(a.libs[0])
+    L = ctypes.CDLL(a.libs[0].split("@")[0])
     L.fn_run.restype = ctypes.c_int
     L.fn_run.argtypes = [ctypes.c_int] * 3 + [ctypes.c_void_p, ctypes.c_int64] + [ctypes.c_void_p] * 5
     n = 1 << a.log2_rows
@@ -79,9 +79,15 @@ def main():
         rest = [f"--op={a.op}", f"--dim={a.dim}", f"--cfg={a.cfg}", f"--log2-rows={a.log2_rows}",
                 f"--reps={a.reps}", f"--rounds={a.rounds}"] + (["--f32"] if a.f32 else []) + \
             ([f"--regime={a.regime}"] if a.regime else [])
+        import os
+
         for _ in range(3):
-            for path in a.libs:
-                subprocess.run([sys.executable, __file__, path] + rest, check=True)
+            for spec in a.libs:
+                # "lib.so@VAR=VAL,VAR2=VAL2": the same library under other settings
+                path, _, envs = spec.partition("@")
+                env = dict(os.environ)
+                env.update(dict(kv.split("=", 1) for kv in envs.split(",") if kv))
+                subprocess.run([sys.executable, __file__, spec] + rest, check=True, env=env)
         return
     run_one(a)
 

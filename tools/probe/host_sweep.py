@@ -67,8 +67,7 @@ if __name__ == "__main__":
         child(int(sys.argv[2]))
     else:
         log2 = int(sys.argv[1]) if len(sys.argv) > 1 else 28
-        settings = [{}, {"FASTNORM_B200_COPY_THREADS": "12"}, {"FASTNORM_B200_COPY_THREADS": "6"},
-                    {"FASTNORM_B200_HOST_PIPES": "4"}]
+        settings = [{}, {"FASTNORM_B200_COPY_THREADS": "16"}, {"FASTNORM_B200_COPY_THREADS": "8"}]
         for st in settings:
             env = dict(os.environ, **st)
             subprocess.run([sys.executable, __file__, "child", str(log2)], env=env, timeout=300)
