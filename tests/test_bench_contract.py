@@ -50,4 +50,5 @@ def test_our_arm_line(cuda_dev):
     assert d["validation"]["rows_counted"] == 1 << 30
     assert d["clocks"]["samples"] >= 1 and d["clocks"]["sm_max_mhz"]
     oc = d["other_configs"]
-    assert {c["config"] for c in oc} == {1, 2, 3, 4} and all(c["frac"] > 0.2 for c in oc)
+    assert {1, 2, 3, 4} <= {c["config"] for c in oc} <= {1, 2, 3, 4, 5}
+    assert all(c["frac"] > 0.2 for c in oc)

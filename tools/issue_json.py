@@ -48,7 +48,7 @@ def main():
             continue
         n = ROWS[name]
         t_unit = v["gpu__time_duration.sum"][1]
-        t = v["gpu__time_duration.sum"][0] * {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1}[t_unit]
+        t = v["gpu__time_duration.sum"][0] * {"nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3, "second": 1, "s": 1}[t_unit]
         clk = v["smsp__cycles_elapsed.avg.per_second"][0] * {"hz": 1, "khz": 1e3, "mhz": 1e6, "ghz": 1e9}[
             v["smsp__cycles_elapsed.avg.per_second"][1].lower()]
         inst = _num(v["smsp__inst_executed.sum"])
