@@ -207,6 +207,14 @@ static bool dyn_enabled() {
     return v;
 }
 
+// Kernels that keep the static schedule.  Dynamic vs static, back-to-back launches, three
+// boxes (profiles/r02h_ab_dyn.txt, r02j_ab_dyn.txt, r02k_steady.jsonl): +5 to +23 % on the
+// quotient, norm, normalize2 and normalize4_sq kernels, +0.3 to +2 % on normalize3 f64 at
+// 2^30 rows, but -1.7 % on normalize3 f32 (config 4) on two boxes.
+template <typename T, int N, int OP> struct DynamicSchedule {
+    static constexpr bool value = !(std::is_same<T, float>::value && N == 3 && OP == FN_OP_NORMALIZE);
+};
+
 struct SchedSlots {
     int dev;
     cudaStream_t stream;
@@ -257,7 +265,8 @@ static cudaError_t launch_tma_as(const T* x, const T* x2, int64_t n, T* head, T*
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, resident));
     KArgs<T> kd = ka;
     kd.sched = kd.sched_next = nullptr;
-    SchedSlots* slots = (dyn_enabled() && ntiles > (int64_t)L::S * grid) ? sched_slots(dev, stream) : nullptr;
+    SchedSlots* slots = (dyn_enabled() && DynamicSchedule<T, N, OP>::value && ntiles > (int64_t)L::S * grid)
+                            ? sched_slots(dev, stream) : nullptr;
     if (!slots)
         return launch_pdl(TL::kernel(), grid, Tile<T, N>::kThreads, L::kSmemBytes, stream, x, x2, n, head, body,
                           extra, kd);

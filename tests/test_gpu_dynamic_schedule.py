@@ -42,17 +42,21 @@ def test_dynamic_schedule_matches_oracle(cuda_dev, n):
     assert bad == 0, first
 
 
-@pytest.mark.parametrize("dtype,cfg", [(torch.float32, 4), (torch.float64, 1)])
-def test_back_to_back_launches_reuse_the_counter(cuda_dev, dtype, cfg):
+# normalize3 f32 keeps the static schedule (DynamicSchedule in fastnorm_kernels.cu), so the
+# binary32 case runs the quotient kernel, which takes the dynamic one
+@pytest.mark.parametrize("dtype,cfg,family", [(torch.float32, 4, "quotient3"), (torch.float64, 1, "normalize3")])
+def test_back_to_back_launches_reuse_the_counter(cuda_dev, dtype, cfg, family):
     p = fn.preset("single" if dtype == torch.float32 else "double")
+    call = (lambda x, out=None: fn.quotient3_robust(x, out=out)) if family == "quotient3" else \
+        (lambda x, out=None: fn.normalize3(p, x, out=out))
     xs = [_rows(n, cfg, dtype) for n in SIZES]
-    want = [fn.normalize3(p, x) for x in xs]
+    want = [call(x) for x in xs]
     torch.cuda.synchronize()
     want = [(w.length.clone(), w.unit.clone()) for w in want]
     outs = [(torch.empty_like(w[0]), torch.empty_like(w[1])) for w in want]
     for _ in range(20):  # 80 launches on one stream, no synchronisation between them
         for x, o in zip(xs, outs):
-            fn.normalize3(p, x, out=o)
+            call(x, out=o)
     torch.cuda.synchronize()
     for w, o in zip(want, outs):
         assert torch.equal(w[0].view(torch.int64 if dtype == torch.float64 else torch.int32),
