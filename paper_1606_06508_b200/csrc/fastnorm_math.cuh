@@ -287,105 +287,6 @@ __device__ __forceinline__ double special_quotient(double a, double b) {
                : __longlong_as_double((long long)(sign | (inf ? 0x7ff0000000000000ull : 0ull)));
 }
 
-// ---------------------------------------------------------------------------------
-// Warp-uniform exact binary64 division (the quotient families on wide-range rows).
-//
-// The library division (__ddiv_rn) has a short inline path, valid when the numerator is
-// >= 2^-967, the divisor is normal and below 2^1017, and the quotient is normal, and a
-// long subroutine for everything else.  On configs 2 and 5 about a third of the quotients
-// x_k / m and q_k / h are tiny (zero or subnormal results), so nearly every warp runs the
-// subroutine once per division site with a few lanes active: 65 % of quotient2's warp
-// instructions on config 2 (round-1 ncu), 18.7 warp instructions per row for quotient3 on
-// config 5 against 8.1 on unit-range rows (profiles/ncu_issue.json).
-//
-// WideDivider computes RN(a / b) for EVERY operand pair with one instruction stream:
-//   a = fa 2^ea, b = fb 2^eb with fa, fb in [1, 2) (subnormals normalised), so
-//   a / b = (fa / fb) 2^d, d = ea - eb, and t = RN(fa / fb) in (1/2, 2) is one Markstein
-//   division with the divisor's reciprocal y = RN(1/fb) (always inside its validity range).
-//   * t 2^d >= 2^-1022 (normal or overflowing result): RN(a / b) = t 2^d, an exact
-//     scaling by two powers of two (the IEEE product overflows to infinity exactly when
-//     the unbounded-exponent result exceeds the largest double).
-//   * t 2^d < 2^-1022 (the subnormal grid): RN(a / b) = n 2^-1074, n = RN_int(X),
-//     X = (fa / fb) 2^s, s = d + 1074 <= 52.  s <= -2: X < 1/2, n = 0; s = -1: X in
-//     (1/4, 1), n = [fa > fb] (X = 1/2 only for fa == fb: tie to even, 0); 0 <= s <= 52:
-//     n0 = rint(t 2^s), |t 2^s - X| <= 2^(s-53) <= 1/2, so |n0 - X| <= 1; the remainder
-//     r = fa 2^s - n0 fb is exact (a multiple of 2^-52 below 2 in magnitude) and 2|r| > fb
-//     moves n0 one step towards X.  A tie (2|r| == fb) means X = n0 +- 1/2 is a 53-bit
-//     number, so t 2^s = X and rint already chose the even neighbour.  n <= 2^52 (2^52 is
-//     the bit pattern of 2^-1022, the right answer when X rounds up onto the normal range).
-//   * zero, infinite or NaN operands: special_quotient (IEEE).
-// The result sign is sign(a) xor sign(b).  Every path is selected, not branched, so a warp
-// with mixed lanes runs it once.  fn_selftest_div checks it bit for bit against __ddiv_rn
-// (full range, subnormal operands and results, midpoints of the subnormal grid, boundary
-// exponent gaps, IEEE specials).
-//
-// lib_div_fast(a, Eb) is the library division's inline-path condition (conservative):
-// kernels vote on it per row and run __ddiv_rn when the whole warp qualifies (unit-range
-// rows never pay for WideDivider) and WideDivider otherwise.
-// ---------------------------------------------------------------------------------
-__device__ __forceinline__ double pow2_normal(int k) {  // 2^k, -1022 <= k <= 1023
-    return __longlong_as_double((long long)(k + 1023) << 52);
-}
-
-__device__ __forceinline__ bool lib_div_fast(double a, int eb_biased) {
-    const int ea = biased_exp(a);
-    const int d = ea - eb_biased;
-    return ea >= 56 && ea <= 2046 && eb_biased >= 1 && eb_biased <= 2039 && d >= -1021 && d <= 1022;
-}
-
-struct WideDivider {
-    double b, fb, y;
-    int eb;
-    unsigned long long sgnb;
-    bool bspecial;
-    __device__ __forceinline__ explicit WideDivider(double b_) : b(b_) {
-        const unsigned long long kMant = 0x000FFFFFFFFFFFFFull, kOne = 1023ull << 52;
-        const unsigned long long bb = (unsigned long long)__double_as_longlong(b_);
-        sgnb = bb & 0x8000000000000000ull;
-        const unsigned long long ab = bb & 0x7FFFFFFFFFFFFFFFull;
-        const int E = (int)(ab >> 52);
-        const unsigned long long M = ab & kMant;
-        bspecial = E == 2047 || ab == 0;
-        const int lz = E == 0 ? __clzll((long long)M) - 11 : 0;
-        eb = E == 0 ? -1022 - lz : E - 1023;
-        fb = bspecial ? 1.0 : __longlong_as_double((long long)(((M << lz) & kMant) | kOne));
-        y = __drcp_rn(fb);
-    }
-    __device__ __forceinline__ double operator()(double a) const {
-        const unsigned long long kMant = 0x000FFFFFFFFFFFFFull, kOne = 1023ull << 52;
-        const unsigned long long ba = (unsigned long long)__double_as_longlong(a);
-        const unsigned long long sign = (ba & 0x8000000000000000ull) ^ sgnb;
-        const unsigned long long aa = ba & 0x7FFFFFFFFFFFFFFFull;
-        const int E = (int)(aa >> 52);
-        const unsigned long long M = aa & kMant;
-        const bool special = bspecial || E == 2047 || aa == 0;
-        const int lz = E == 0 ? __clzll((long long)M) - 11 : 0;
-        const int ea = E == 0 ? -1022 - lz : E - 1023;
-        const double fa = __longlong_as_double((long long)(((M << lz) & kMant) | kOne));
-        const double t = div_markstein(fa, fb, y);  // RN(fa / fb), in (1/2, 2)
-        const int d = ea - eb;
-        const bool normal = d + (t >= 1.0 ? 0 : -1) >= -1022;
-        // normal / overflow: t 2^d as two exact power-of-two products
-        const int dc = d > 1100 ? 1100 : (d < -1022 ? -1022 : d);
-        const int d1 = dc >> 1;
-        const double big = __dmul_rn(__dmul_rn(t, pow2_normal(d1)), pow2_normal(dc - d1));
-        // subnormal grid: n = RN_int((fa / fb) 2^s)
-        const int s = d + 1074;
-        const double ps = pow2_normal(s < 0 ? 0 : (s > 52 ? 52 : s));
-        double n = rint(__dmul_rn(t, ps));
-        const double r = __fma_rn(-n, fb, __dmul_rn(fa, ps));
-        if (fabs(__dadd_rn(r, r)) > fb) n = __dadd_rn(n, r > 0.0 ? 1.0 : -1.0);
-        n = s >= 0 ? n : (s == -1 && fa > fb ? 1.0 : 0.0);
-        // n + 2^52 holds n in its low significand bits (n <= 2^52; n = 2^52 gives 2^53,
-        // whose bits minus those of 2^52 are again 2^52)
-        const unsigned long long tiny =
-            (unsigned long long)__double_as_longlong(__dadd_rn(n, 4503599627370496.0)) - 0x4330000000000000ull;
-        const unsigned long long mag = normal ? (unsigned long long)__double_as_longlong(big) : tiny;
-        const double res = __longlong_as_double((long long)(mag | sign));
-        return special ? special_quotient(a, b) : res;
-    }
-};
-
 #if !FNB_F64_DIV_MARKSTEIN
 // Plain IEEE division per numerator (__ddiv_rn).  Measured alternatives, all exact and
 // checked by fn_selftest_div, all slower on unit-range rows (configs 1, 3):
@@ -671,35 +572,6 @@ __device__ __forceinline__ void scale_row(const T (&x)[4], const KArgs<T>& ka, T
     s[2] = F::mul(sigma, x[2]); s[3] = F::mul(sigma, x[3]);
 }
 
-// K binary64 numerators over one divisor (the quotient families' division sites).
-// FNB_F64_WIDE_DIV = 1: the warp votes on the library division's inline-path condition
-// and runs __ddiv_rn when every lane qualifies, WideDivider otherwise (one instruction
-// stream, no per-site subroutine); 0: Divider<double> per numerator.
-#ifndef FNB_F64_WIDE_DIV
-#define FNB_F64_WIDE_DIV 1
-#endif
-template <int K>
-__device__ __forceinline__ void divide_shared(const double (&a)[K], double b, double (&q)[K]) {
-#if FNB_F64_WIDE_DIV
-    const int eb = biased_exp(b);
-    bool ok = true;
-#pragma unroll
-    for (int k = 0; k < K; ++k) ok = ok && lib_div_fast(a[k], eb);
-    if (__all_sync(__activemask(), ok)) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) q[k] = __ddiv_rn(a[k], b);
-    } else {
-        const WideDivider w(b);
-#pragma unroll
-        for (int k = 0; k < K; ++k) q[k] = w(a[k]);
-    }
-#else
-    const Divider<double> by(b);
-#pragma unroll
-    for (int k = 0; k < K; ++k) q[k] = by(a[k]);
-#endif
-}
-
 // naive{2,3,4}: _kernels.pyx:262-285.  r = sqrt(sum x^2), u = x / r (true divisions).
 template <typename T, int N>
 __device__ __forceinline__ void naive_row(const T (&x)[N], T& r, T (&u)[N]) {
@@ -761,10 +633,10 @@ __device__ __forceinline__ void quotient_row(const T (&x)[N], T& r, T (&u)[N]) {
     T o[N - 1];  // the other components, original order
 #pragma unroll
     for (int i = 0; i < N - 1; ++i) o[i] = (i < j) ? x[i] : x[i + 1];
-    T qo[N - 1], on[N - 1];
+    T qo[N - 1];
+    const Divider<T> by_m(regular ? m : T(1));
 #pragma unroll
-    for (int i = 0; i < N - 1; ++i) on[i] = regular ? o[i] : T(1);  // irregular rows are refilled below
-    divide_shared<N - 1>(on, regular ? m : T(1), qo);
+    for (int i = 0; i < N - 1; ++i) qo[i] = by_m(regular ? o[i] : T(0));
     T sj = x[0];
 #pragma unroll
     for (int k = 1; k < N; ++k) sj = (k == j) ? x[k] : sj;
@@ -781,7 +653,9 @@ __device__ __forceinline__ void quotient_row(const T (&x)[N], T& r, T (&u)[N]) {
     r = F::mul(m, h);
     const T y = F::rcp(h);
     T uo[N - 1];
-    divide_shared<N - 1>(qo, h, uo);
+    const Divider<T> by_h(h);
+#pragma unroll
+    for (int i = 0; i < N - 1; ++i) uo[i] = by_h(qo[i]);
     const T uj = F::mul(sj, y);
 #pragma unroll
     for (int k = 0; k < N; ++k) {
@@ -823,18 +697,9 @@ __device__ __forceinline__ void quotient_row(const T (&x)[N], T& r, T (&u)[N]) {
 template <typename T>
 __device__ __forceinline__ void qf_pivot(T p, T a, T b, T& r, T& t, T& ua, T& ub) {
     using F = Fp<T>;
-    T qa, qb;
-    if constexpr (std::is_same<T, double>::value) {
-        const double ab[2] = {a, b};
-        double q[2];
-        divide_shared<2>(ab, p, q);
-        qa = q[0];
-        qb = q[1];
-    } else {
-        const Divider<T> by_p(p);
-        qa = by_p(a);
-        qb = by_p(b);
-    }
+    const Divider<T> by_p(p);
+    const T qa = by_p(a);
+    const T qb = by_p(b);
     const T h = F::sqrt(F::add(F::add(T(1), F::mul(qa, qa)), F::mul(qb, qb)));
     t = F::div(F::sign1(p), h);
     r = F::mul(F::abs(p), h);
