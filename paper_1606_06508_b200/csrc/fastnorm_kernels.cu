@@ -91,7 +91,7 @@ static bool is_rotation(int op) {
 template <typename T, int N, int OP, int LDX = 0, bool MIS = false> struct TmaLaunch {
     using L = TileLayout<T, N, OP, OpRows<T, N, OP>::value, OpStages<T, N, OP>::value, OutTiles<OP>::value, LDX, MIS>;
     static constexpr auto kernel() {
-        return tma_stream_kernel<T, N, OP, OpRows<T, N, OP>::value, OpStages<T, N, OP>::value, Tile<T, N>::kThreads,
+        return tma_stream_kernel<T, N, OP, OpRows<T, N, OP>::value, OpStages<T, N, OP>::value, OpThreads<T, N, OP>::value,
                                  Tile<T, N>::kHints, OutTiles<OP>::value, LDX, MIS>;
     }
     static int blocks_per_sm(int dev) {
@@ -103,7 +103,7 @@ template <typename T, int N, int OP, int LDX = 0, bool MIS = false> struct TmaLa
             auto kern = kernel();
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemBytes);
             int nb = 0;
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, Tile<T, N>::kThreads,
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, OpThreads<T, N, OP>::value,
                                                               L::kSmemBytes) != cudaSuccess ||
                 nb < 1)
                 nb = 1;
@@ -268,7 +268,7 @@ static cudaError_t launch_tma_as(const T* x, const T* x2, int64_t n, T* head, T*
     SchedSlots* slots = (dyn_enabled() && DynamicSchedule<T, N, OP>::value && ntiles > (int64_t)L::S * grid)
                             ? sched_slots(dev, stream) : nullptr;
     if (!slots)
-        return launch_pdl(TL::kernel(), grid, Tile<T, N>::kThreads, L::kSmemBytes, stream, x, x2, n, head, body,
+        return launch_pdl(TL::kernel(), grid, OpThreads<T, N, OP>::value, L::kSmemBytes, stream, x, x2, n, head, body,
                           extra, kd);
     std::lock_guard<std::mutex> lk(slots->mu);
     const uint64_t i = slots->launches;
@@ -277,7 +277,7 @@ static cudaError_t launch_tma_as(const T* x, const T* x2, int64_t n, T* head, T*
     // tiles per claim: 1 for a few tiles per CTA (balance matters most), up to 8 for
     // long runs (at ~2 ns per tile GPU-wide, one claim per tile contends on the counter)
     kd.sched_batch = (int)std::max<int64_t>(1, std::min<int64_t>(8, ntiles / ((int64_t)grid * 128)));
-    const cudaError_t e = launch_pdl(TL::kernel(), grid, Tile<T, N>::kThreads, L::kSmemBytes, stream, x, x2, n,
+    const cudaError_t e = launch_pdl(TL::kernel(), grid, OpThreads<T, N, OP>::value, L::kSmemBytes, stream, x, x2, n,
                                      head, body, extra, kd);
     if (e == cudaSuccess) slots->launches = i + 1;
     return e;

@@ -403,6 +403,29 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
 // 2 CTAs x 4 stages x 6 KiB reaches the cudaMemcpy bandwidth.  L2 policy hints measured
 // neutral (within noise) -> off.  The division-bound comparison variants (naive,
 // quotient) are FP64-issue bound instead and prefer full occupancy (kCtasPerSm below).
+// The binary64 division-bound kernels (quotient, quotient3_fast, naive) are latency
+// bound at 3-4 CTAs per SM (24-32 warps): ncu on quotient2 / config 2 shows "wait" and
+// barrier stalls on top, 1.6 eligible warps per scheduler, shared memory limiting the CTA
+// count to 3 (profiles/r02o_quotient2_stalls.txt).  FNB_DIV_ROWS_SHIFT halves their tile
+// (rows per stage) that many times and FNB_DIV_STAGES sets their ring depth, so more
+// CTAs fit per SM; FNB_DIV_MIN_BLOCKS is the launch-bounds minimum (register cap).
+#ifndef FNB_DIV_ROWS_SHIFT
+#define FNB_DIV_ROWS_SHIFT 0
+#endif
+#ifndef FNB_DIV_STAGES
+#define FNB_DIV_STAGES 0
+#endif
+#ifndef FNB_DIV_MIN_BLOCKS
+#define FNB_DIV_MIN_BLOCKS 1
+#endif
+template <typename T, int OP> struct DivBound {
+    static constexpr bool value = std::is_same<T, double>::value &&
+                                  (OP == FN_OP_QUOTIENT || OP == FN_OP_QUOTIENT3_FAST || OP == FN_OP_NAIVE);
+};
+template <typename T, int OP> struct MinBlocks {
+    static constexpr int value = DivBound<T, OP>::value ? FNB_DIV_MIN_BLOCKS : 1;
+};
+
 constexpr int pow2_floor(int v) { return v >= 2 ? 2 * pow2_floor(v / 2) : 1; }
 
 template <typename T, int N> struct Tile {
@@ -418,9 +441,12 @@ template <typename T, int N> struct Tile {
 
 // norm writes 8 B per row against 16-32 B read: read-dominated traffic wants more
 // loads in flight (4 CTAs: 7090 vs 5963 GB/s at 2, profiles/r01i_tune_norm.csv).
+#ifndef FNB_DIV_CTAS
+#define FNB_DIV_CTAS 8
+#endif
 template <int OP> struct CtasPerSm {
     static constexpr int value =
-        (OP == FN_OP_NAIVE || OP == FN_OP_QUOTIENT || OP == FN_OP_QUOTIENT3_FAST) ? 8
+        (OP == FN_OP_NAIVE || OP == FN_OP_QUOTIENT || OP == FN_OP_QUOTIENT3_FAST) ? FNB_DIV_CTAS
         : (OP == FN_OP_NORM ? 4 : 2);
 };
 
@@ -473,7 +499,8 @@ struct TileLayout {
 // would exceed 64 KiB (rotations write 72-112 B per row).
 template <typename T, int N, int OP> struct OpRows {
     static constexpr int kOutRow = (RowOp<T, N, OP>::W0 + RowOp<T, N, OP>::W1 + RowOp<T, N, OP>::W2) * (int)sizeof(T);
-    static constexpr int value = (3 * kOutRow * Tile<T, N>::kRows > 65536) ? Tile<T, N>::kRows / 2 : Tile<T, N>::kRows;
+    static constexpr int kBase = (3 * kOutRow * Tile<T, N>::kRows > 65536) ? Tile<T, N>::kRows / 2 : Tile<T, N>::kRows;
+    static constexpr int value = DivBound<T, OP>::value ? kBase >> FNB_DIV_ROWS_SHIFT : kBase;
 };
 
 // Per-row matrices are 72 B records: the default 8 KiB stage would hold only 64 of them
@@ -501,7 +528,23 @@ template <typename T> struct Tile<T, 9> {
 // library (profiles/r01ca_nrot.txt): 128 x 3 (default) 6267 GB/s, 256 x 2 6308,
 // 128 x 4 5994, 256 x 3 5880 -- the tuner's ranking (r01bz_rot.csv) does not carry over.
 template <typename T, int N, int OP> struct OpStages {
-    static constexpr int value = Tile<T, N>::kStages;
+    static constexpr int value = (DivBound<T, OP>::value && FNB_DIV_STAGES > 0) ? FNB_DIV_STAGES : Tile<T, N>::kStages;
+};
+// quotient2 f64: two stages of 512 rows fit 4 CTAs per SM instead of 3 (+9 % on config 2,
+// profiles/r02p_ab_div_geometry.txt; the other geometries measured within +-2 % or lost on
+// the HBM-bound unit-range configs).
+#ifndef FNB_QUOT2_STAGES
+#define FNB_QUOT2_STAGES 2
+#endif
+template <> struct OpStages<double, 2, FN_OP_QUOTIENT> {
+    static constexpr int value = FNB_DIV_STAGES > 0 ? FNB_DIV_STAGES : FNB_QUOT2_STAGES;
+};
+
+// Threads per CTA: one row per thread at least (a division-bound tile shrunk below 256
+// rows gets as many threads as rows).
+template <typename T, int N, int OP> struct OpThreads {
+    static constexpr int value =
+        OpRows<T, N, OP>::value < Tile<T, N>::kThreads ? OpRows<T, N, OP>::value : Tile<T, N>::kThreads;
 };
 #ifdef FNB_NROT_STAGES
 template <typename T, int N> struct OpStages<T, N, FN_OP_NORMALIZE_ROT> {
@@ -547,7 +590,7 @@ __device__ __forceinline__ void timeline_tile(int64_t, int, bool = true) {}
 template <typename T, int N, int OP, int TR_ = OpRows<T, N, OP>::value, int S_ = OpStages<T, N, OP>::value,
           int NT = Tile<T, N>::kThreads, int HINTS = Tile<T, N>::kHints, int OB_ = OutTiles<OP>::value,
           int LDX_ = 0, bool MIS = false>
-__global__ void __launch_bounds__(NT) tma_stream_kernel(const T* __restrict__ x, const T* __restrict__ x2,
+__global__ void __launch_bounds__(NT, MinBlocks<T, OP>::value) tma_stream_kernel(const T* __restrict__ x, const T* __restrict__ x2,
                                                         int64_t nrows, T* __restrict__ head,
                                                         T* __restrict__ body, T* __restrict__ extra,
                                                         KArgs<T> ka) {
