@@ -7,11 +7,11 @@ import sys
 d = collections.OrderedDict()
 order = []
 for line in open(sys.argv[1]):
-    m = re.search(r"(\S+?)(?:@(\S+))?: op=(\d) dim=(\d) cfg=(\d) (f\d\d) ([\d.]+) ms/launch, ([\d.]+) GB/s", line)
+    m = re.search(r"(\S+?)(?:@(\S+))?: op=(\d) dim=(\d) (?:cfg|regime)=(\S+) (f\d\d) ([\d.]+) ms/launch, ([\d.]+) GB/s", line)
     if not m:
         continue
     lib = m.group(1).split("/")[-1] + ("@" + m.group(2) if m.group(2) else "")
-    key = "op%s dim%s cfg%s %s" % m.group(3, 4, 5, 6)
+    key = "op%s dim%s %s %s" % m.group(3, 4, 5, 6)
     d.setdefault(key, collections.OrderedDict()).setdefault(lib, []).append(float(m.group(8)))
     if lib not in order:
         order.append(lib)
