@@ -530,15 +530,10 @@ template <typename T> struct Tile<T, 9> {
 template <typename T, int N, int OP> struct OpStages {
     static constexpr int value = (DivBound<T, OP>::value && FNB_DIV_STAGES > 0) ? FNB_DIV_STAGES : Tile<T, N>::kStages;
 };
-// quotient2 f64: two stages of 512 rows fit 4 CTAs per SM instead of 3 (+9 % on config 2,
-// profiles/r02p_ab_div_geometry.txt; the other geometries measured within +-2 % or lost on
-// the HBM-bound unit-range configs).
-#ifndef FNB_QUOT2_STAGES
-#define FNB_QUOT2_STAGES 2
-#endif
-template <> struct OpStages<double, 2, FN_OP_QUOTIENT> {
-    static constexpr int value = FNB_DIV_STAGES > 0 ? FNB_DIV_STAGES : FNB_QUOT2_STAGES;
-};
+// quotient2 f64 with two 512-row stages (4 CTAs per SM instead of 3) gained 9 % on
+// config 2 but ran bimodal on unit-range 2-D rows (0.388 or 0.493 ms per 2^26 rows from
+// one process to the next: a two-stage ring is too shallow for HBM-bound rows), so every
+// division-bound kernel keeps the default ring (profiles/r02q_ab_quotient2_stages_table.txt).
 
 // Threads per CTA: one row per thread at least (a division-bound tile shrunk below 256
 // rows gets as many threads as rows).
