@@ -139,6 +139,15 @@ static int cps_override() {
     return v;
 }
 
+// FASTNORM_B200_SCHED_BATCH=<k>: tiles per claim of the dynamic schedule (experiments).
+static int sched_batch_override() {
+    static const int v = [] {
+        const char* e = getenv("FASTNORM_B200_SCHED_BATCH");
+        return e ? atoi(e) : -1;
+    }();
+    return v;
+}
+
 // Kernels this library has launched, process-wide (fn_launch_count): the bench counts
 // its launches inside a timed region from the library itself.
 static std::atomic<int64_t> g_launches{0};
@@ -274,9 +283,12 @@ static cudaError_t launch_tma_as(const T* x, const T* x2, int64_t n, T* head, T*
     const uint64_t i = slots->launches;
     kd.sched = slots->ctr + (i & 1);
     kd.sched_next = slots->ctr + ((i + 1) & 1);
-    // tiles per claim: 1 for a few tiles per CTA (balance matters most), up to 8 for
-    // long runs (at ~2 ns per tile GPU-wide, one claim per tile contends on the counter)
-    kd.sched_batch = (int)std::max<int64_t>(1, std::min<int64_t>(8, ntiles / ((int64_t)grid * 128)));
+    // tiles per claim: 2.  Measured against 1, 4, 8 and 16 on nine kernel / config pairs
+    // (profiles/r02t_sched_batch_table.txt): one tile per claim loses up to 25 % where
+    // many CTAs claim short tiles (the counter's round trip is on every tile's path),
+    // larger batches lose balance (normalize3 config 5: +3.7 % at 2, +2.3 % at 8 over
+    // the static schedule).
+    kd.sched_batch = sched_batch_override() > 0 ? sched_batch_override() : 2;
     const cudaError_t e = launch_pdl(TL::kernel(), grid, OpThreads<T, N, OP>::value, L::kSmemBytes, stream, x, x2, n,
                                      head, body, extra, kd);
     if (e == cudaSuccess) slots->launches = i + 1;
@@ -506,6 +518,8 @@ static int launch_many(int nseg, const void* const* xs, const int64_t* ns, void*
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
     const int sms = device_sms(dev);
     SegmentTable<T> tab;
+    tab.nseg = 0;
+    tab.ntiles = 0;
     auto flush = [&]() -> int {
         if (tab.nseg == 0) return FN_OK;
         const int64_t work = std::max<int64_t>(tab.ntiles, 1);
@@ -518,8 +532,6 @@ static int launch_many(int nseg, const void* const* xs, const int64_t* ns, void*
         tab.ntiles = 0;
         return FN_OK;
     };
-    tab.nseg = 0;
-    tab.ntiles = 0;
     for (int j = 0; j < nseg; ++j) {
         const int64_t n = ns[j];
         if (n == 0) continue;
