@@ -220,8 +220,12 @@ static bool dyn_enabled() {
 // boxes (profiles/r02h_ab_dyn.txt, r02j_ab_dyn.txt, r02k_steady.jsonl): +5 to +23 % on the
 // quotient, norm, normalize2 and normalize4_sq kernels, +0.3 to +2 % on normalize3 f64 at
 // 2^30 rows, but -1.7 % on normalize3 f32 (config 4) on two boxes.
+#ifndef FNB_DYN_F32_NORMALIZE3
+#define FNB_DYN_F32_NORMALIZE3 0
+#endif
 template <typename T, int N, int OP> struct DynamicSchedule {
-    static constexpr bool value = !(std::is_same<T, float>::value && N == 3 && OP == FN_OP_NORMALIZE);
+    static constexpr bool value =
+        FNB_DYN_F32_NORMALIZE3 || !(std::is_same<T, float>::value && N == 3 && OP == FN_OP_NORMALIZE);
 };
 
 struct SchedSlots {
