@@ -185,11 +185,11 @@ static cudaError_t launch_pdl(void (*kern)(Params...), int grid, int block, size
 // CTAs per SM: the measured streaming optimum (CtasPerSm); small batches (few tiles per
 // CTA) fill the machine with the occupancy maximum instead, to shorten the pipeline
 // fill / drain.
-template <int OP>
+template <typename T, int N, int OP>
 static int ctas_per_sm_for(int64_t ntiles, int sms) {
     if (cps_override() > 0) return cps_override();
-    const int64_t tiles_per_cta = ntiles / ((int64_t)CtasPerSm<OP>::value * sms);
-    return tiles_per_cta < 32 ? 64 : CtasPerSm<OP>::value;
+    const int64_t tiles_per_cta = ntiles / ((int64_t)CtasPerSm<T, N, OP>::value * sms);
+    return tiles_per_cta < 32 ? 64 : CtasPerSm<T, N, OP>::value;
 }
 
 // Input records of LDX elements, N of them read per row (LDX > N only for N = 3, LDX = 4,
@@ -273,7 +273,7 @@ static cudaError_t launch_tma_as(const T* x, const T* x2, int64_t n, T* head, T*
     using TL = TmaLaunch<T, N, OP, LDX, MIS>;
     using L = typename TL::L;
     const int64_t ntiles = n / L::TR;
-    const int64_t per_sm = std::min<int64_t>(TL::blocks_per_sm(dev), ctas_per_sm_for<OP>(ntiles, sms));
+    const int64_t per_sm = std::min<int64_t>(TL::blocks_per_sm(dev), ctas_per_sm_for<T, N, OP>(ntiles, sms));
     const int64_t resident = per_sm * sms;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, resident));
     KArgs<T> kd = ka;
@@ -527,7 +527,7 @@ static int launch_many(int nseg, const void* const* xs, const int64_t* ns, void*
     auto flush = [&]() -> int {
         if (tab.nseg == 0) return FN_OK;
         const int64_t work = std::max<int64_t>(tab.ntiles, 1);
-        const int64_t per_sm = std::min<int64_t>(SL::blocks_per_sm(dev), ctas_per_sm_for<OP>(tab.ntiles, sms));
+        const int64_t per_sm = std::min<int64_t>(SL::blocks_per_sm(dev), ctas_per_sm_for<T, N, OP>(tab.ntiles, sms));
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(work, tab.nseg), per_sm * sms));
         const cudaError_t le = launch_pdl(tma_segments_kernel<T, N, OP>, grid, Tile<T, N>::kThreads, L::kSmemBytes,
                                           stream, tab, ka);

@@ -439,15 +439,28 @@ template <typename T, int N> struct Tile {
     static constexpr int kHints = 0;
 };
 
-// norm writes 8 B per row against 16-32 B read: read-dominated traffic wants more
-// loads in flight (4 CTAs: 7090 vs 5963 GB/s at 2, profiles/r01i_tune_norm.csv).
+// CTAs per SM of the streaming kernel.
+// * norm writes 8 B per row against 16-32 B read: read-dominated traffic wants more loads
+//   in flight (4 CTAs: 7090 vs 5963 GB/s at 2, profiles/r01i_tune_norm.csv).
+// * The other families: 2 CTAs under round 1's static schedule (profiles/r01_tune*.csv);
+//   with the dynamic schedule 3 CTAs measure better (profiles/r02w_ab_ctas_table.txt,
+//   2 -> 3: normalize2 f64 +8.8 %, normalize4_sq +4.1 %, normalize4 +2.4 %, scale3
+//   +2.6 %, normalize4_rotation +1.3 %, normalize3 f64 at 2^30 rows -0.7 to +2.8 %
+//   over three rounds, normalize2 f32 +7.9 %, normalize4 f32 +2.3 %), except 3-D
+//   binary32 rows (-8 % for normalize3 f32, which keeps the static schedule).
+// * The division-bound comparison kernels want full occupancy (FNB_DIV_CTAS).
 #ifndef FNB_DIV_CTAS
 #define FNB_DIV_CTAS 8
 #endif
-template <int OP> struct CtasPerSm {
+#ifndef FNB_STREAM_CTAS
+#define FNB_STREAM_CTAS 3
+#endif
+template <typename T, int N, int OP> struct CtasPerSm {
     static constexpr int value =
         (OP == FN_OP_NAIVE || OP == FN_OP_QUOTIENT || OP == FN_OP_QUOTIENT3_FAST) ? FNB_DIV_CTAS
-        : (OP == FN_OP_NORM ? 4 : 2);
+        : OP == FN_OP_NORM                            ? 4
+        : (std::is_same<T, float>::value && N == 3)   ? 2
+                                                      : FNB_STREAM_CTAS;
 };
 
 // Output staging tiles: 3 (one bulk-store group reading behind the current one).  A
