@@ -426,15 +426,21 @@ template <typename T, int OP> struct MinBlocks {
     static constexpr int value = DivBound<T, OP>::value ? FNB_DIV_MIN_BLOCKS : 1;
 };
 
+#ifndef FNB_STREAM_STAGES
+#define FNB_STREAM_STAGES 0  // experiments: ring depth of every (T, N) default tile
+#endif
+#ifndef FNB_STREAM_TILE_BYTES
+#define FNB_STREAM_TILE_BYTES 8192  // experiments: input bytes per stage (upper bound)
+#endif
 constexpr int pow2_floor(int v) { return v >= 2 ? 2 * pow2_floor(v / 2) : 1; }
 
 template <typename T, int N> struct Tile {
     // largest power of two with at most 8 KiB of input per stage
-    static constexpr int kRows = pow2_floor(8192 / (N * (int)sizeof(T)));
+    static constexpr int kRows = pow2_floor(FNB_STREAM_TILE_BYTES / (N * (int)sizeof(T)));
     static constexpr int kStageBytes = kRows * N * (int)sizeof(T);
     // measured (profiles/r01j_tune_all.csv): 4 stages for n = 2, 3; 3 for quaternions,
     // whose wider output staging already keeps more bytes in flight per CTA.
-    static constexpr int kStages = N == 4 ? 3 : 4;
+    static constexpr int kStages = FNB_STREAM_STAGES > 0 ? FNB_STREAM_STAGES : (N == 4 ? 3 : 4);
     static constexpr int kThreads = 256;
     static constexpr int kHints = 0;
 };
