@@ -516,9 +516,25 @@ struct TileLayout {
 
 // Rows per tile for an op: the default, halved while the three output staging tiles
 // would exceed 64 KiB (rotations write 72-112 B per row).
+// 3-D rows of the scaling families under the dynamic schedule (round 2): binary64 takes
+// 512-row stages (12 KiB) in a 3-deep ring, 2 CTAs per SM by shared memory (72 KiB of
+// loads in flight per SM, as before): at 2^30 rows the 256-row tiles ran 6500 GB/s and
+// these 6978, stable over three rounds, with 2^28 rows unchanged (6935 vs 6949;
+// profiles/r02z_ab_tiles.txt).  binary32 keeps 512-row stages in a 5-deep ring (+2.8 %
+// on config 4, profiles/r02y_ab_stages_table.txt).
+#ifndef FNB_BIG_TILES
+#define FNB_BIG_TILES 1
+#endif
+template <typename T, int N, int OP> struct Rows3 {
+    static constexpr bool scaling = OP == FN_OP_NORMALIZE || OP == FN_OP_NORMALIZE_SQ || OP == FN_OP_SCALE;
+    static constexpr bool f64 = FNB_BIG_TILES && N == 3 && scaling && std::is_same<T, double>::value;
+    static constexpr bool f32 = FNB_BIG_TILES && N == 3 && OP == FN_OP_NORMALIZE && std::is_same<T, float>::value;
+};
+
 template <typename T, int N, int OP> struct OpRows {
     static constexpr int kOutRow = (RowOp<T, N, OP>::W0 + RowOp<T, N, OP>::W1 + RowOp<T, N, OP>::W2) * (int)sizeof(T);
-    static constexpr int kBase = (3 * kOutRow * Tile<T, N>::kRows > 65536) ? Tile<T, N>::kRows / 2 : Tile<T, N>::kRows;
+    static constexpr int kTile = Rows3<T, N, OP>::f64 ? 512 : Tile<T, N>::kRows;
+    static constexpr int kBase = (3 * kOutRow * kTile > 65536) ? kTile / 2 : kTile;
     static constexpr int value = DivBound<T, OP>::value ? kBase >> FNB_DIV_ROWS_SHIFT : kBase;
 };
 
@@ -547,7 +563,10 @@ template <typename T> struct Tile<T, 9> {
 // library (profiles/r01ca_nrot.txt): 128 x 3 (default) 6267 GB/s, 256 x 2 6308,
 // 128 x 4 5994, 256 x 3 5880 -- the tuner's ranking (r01bz_rot.csv) does not carry over.
 template <typename T, int N, int OP> struct OpStages {
-    static constexpr int value = (DivBound<T, OP>::value && FNB_DIV_STAGES > 0) ? FNB_DIV_STAGES : Tile<T, N>::kStages;
+    static constexpr int value = (DivBound<T, OP>::value && FNB_DIV_STAGES > 0) ? FNB_DIV_STAGES
+                                 : Rows3<T, N, OP>::f64                        ? 3
+                                 : Rows3<T, N, OP>::f32                        ? 5
+                                                                               : Tile<T, N>::kStages;
 };
 // quotient2 f64 with two 512-row stages (4 CTAs per SM instead of 3) gained 9 % on
 // config 2 but ran bimodal on unit-range 2-D rows (0.388 or 0.493 ms per 2^26 rows from
