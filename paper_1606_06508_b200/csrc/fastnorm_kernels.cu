@@ -88,10 +88,12 @@ static bool is_rotation(int op) {
 }
 
 // Per-instantiation occupancy (computed once per process and device).
-template <typename T, int N, int OP, int LDX = 0, bool MIS = false> struct TmaLaunch {
-    using L = TileLayout<T, N, OP, OpRows<T, N, OP>::value, OpStages<T, N, OP>::value, OutTiles<OP>::value, LDX, MIS>;
+template <typename T, int N, int OP, int LDX = 0, bool MIS = false, bool BIG = true> struct TmaLaunch {
+    static constexpr int kThreads = OpThreads<T, N, OP, BIG>::value;
+    using L = TileLayout<T, N, OP, OpRows<T, N, OP, BIG>::value, OpStages<T, N, OP, BIG>::value, OutTiles<OP>::value,
+                         LDX, MIS>;
     static constexpr auto kernel() {
-        return tma_stream_kernel<T, N, OP, OpRows<T, N, OP>::value, OpStages<T, N, OP>::value, OpThreads<T, N, OP>::value,
+        return tma_stream_kernel<T, N, OP, OpRows<T, N, OP, BIG>::value, OpStages<T, N, OP, BIG>::value, kThreads,
                                  Tile<T, N>::kHints, OutTiles<OP>::value, LDX, MIS>;
     }
     static int blocks_per_sm(int dev) {
@@ -103,7 +105,7 @@ template <typename T, int N, int OP, int LDX = 0, bool MIS = false> struct TmaLa
             auto kern = kernel();
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemBytes);
             int nb = 0;
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, OpThreads<T, N, OP>::value,
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads,
                                                               L::kSmemBytes) != cudaSuccess ||
                 nb < 1)
                 nb = 1;
@@ -267,10 +269,10 @@ static SchedSlots* sched_slots(int dev, cudaStream_t stream) {
     return g_sched->back().get();
 }
 
-template <typename T, int N, int OP, int LDX, bool MIS>
+template <typename T, int N, int OP, int LDX, bool MIS, bool BIG>
 static cudaError_t launch_tma_as(const T* x, const T* x2, int64_t n, T* head, T* body, T* extra,
                                  const KArgs<T>& ka, int dev, int sms, cudaStream_t stream) {
-    using TL = TmaLaunch<T, N, OP, LDX, MIS>;
+    using TL = TmaLaunch<T, N, OP, LDX, MIS, BIG>;
     using L = typename TL::L;
     const int64_t ntiles = n / L::TR;
     const int64_t per_sm = std::min<int64_t>(TL::blocks_per_sm(dev), ctas_per_sm_for<T, N, OP>(ntiles, sms));
@@ -281,7 +283,7 @@ static cudaError_t launch_tma_as(const T* x, const T* x2, int64_t n, T* head, T*
     SchedSlots* slots = (dyn_enabled() && DynamicSchedule<T, N, OP>::value && ntiles > (int64_t)L::S * grid)
                             ? sched_slots(dev, stream) : nullptr;
     if (!slots)
-        return launch_pdl(TL::kernel(), grid, OpThreads<T, N, OP>::value, L::kSmemBytes, stream, x, x2, n, head, body,
+        return launch_pdl(TL::kernel(), grid, TL::kThreads, L::kSmemBytes, stream, x, x2, n, head, body,
                           extra, kd);
     std::lock_guard<std::mutex> lk(slots->mu);
     const uint64_t i = slots->launches;
@@ -293,25 +295,32 @@ static cudaError_t launch_tma_as(const T* x, const T* x2, int64_t n, T* head, T*
     // larger batches lose balance (normalize3 config 5: +3.7 % at 2, +2.3 % at 8 over
     // the static schedule).
     kd.sched_batch = sched_batch_override() > 0 ? sched_batch_override() : 2;
-    const cudaError_t e = launch_pdl(TL::kernel(), grid, OpThreads<T, N, OP>::value, L::kSmemBytes, stream, x, x2, n,
+    const cudaError_t e = launch_pdl(TL::kernel(), grid, TL::kThreads, L::kSmemBytes, stream, x, x2, n,
                                      head, body, extra, kd);
     if (e == cudaSuccess) slots->launches = i + 1;
     return e;
 }
 
 // MIS: the instantiation for inputs off the 16-byte grid (tma_stream_kernel).
+// BIG: the large-batch geometry (Rows3); smaller batches take the default one when it
+// differs (one more instantiation only for the kernels Rows3 changes).
 template <typename T, int N, int OP, int LDX = 0>
 static cudaError_t launch_tma(const T* x, const T* x2, int64_t n, T* head, T* body, T* extra, const KArgs<T>& ka,
                               int dev, int sms, cudaStream_t stream) {
-    if (!aligned16(x) || (x2 && !aligned16(x2)))
-        return launch_tma_as<T, N, OP, LDX, true>(x, x2, n, head, body, extra, ka, dev, sms, stream);
-    return launch_tma_as<T, N, OP, LDX, false>(x, x2, n, head, body, extra, ka, dev, sms, stream);
+    const bool mis = !aligned16(x) || (x2 && !aligned16(x2));
+    if constexpr (Rows3<T, N, OP>::any) {
+        if (n < kBigTileRows)
+            return mis ? launch_tma_as<T, N, OP, LDX, true, false>(x, x2, n, head, body, extra, ka, dev, sms, stream)
+                       : launch_tma_as<T, N, OP, LDX, false, false>(x, x2, n, head, body, extra, ka, dev, sms, stream);
+    }
+    return mis ? launch_tma_as<T, N, OP, LDX, true, true>(x, x2, n, head, body, extra, ka, dev, sms, stream)
+               : launch_tma_as<T, N, OP, LDX, false, true>(x, x2, n, head, body, extra, ka, dev, sms, stream);
 }
 
 template <typename T, int N, int OP>
 static int launch(const void* xv, const void* x2v, int64_t n, void* hv, void* bv, void* qv,
                   const KArgs<T>& ka, cudaStream_t stream, int64_t ldx = N) {
-    using TL = TmaLaunch<T, N, OP>;
+    using TL = TmaLaunch<T, N, OP, 0, false, false>;  // the geometry of the smallest batches it takes
     using L = typename TL::L;
     using Op = typename L::Op;
     const T* x = static_cast<const T*>(xv);
@@ -491,7 +500,7 @@ int run_ex(int op, int dim, int dtype, const void* x, int64_t n, void* head, voi
 // Many independent batches (segments) per launch: fn_run_many.
 // ---------------------------------------------------------------------------------
 template <typename T, int N, int OP> struct SegLaunch {
-    using L = TileLayout<T, N, OP, OpRows<T, N, OP>::value, OpStages<T, N, OP>::value>;
+    using L = TileLayout<T, N, OP, OpRows<T, N, OP, false>::value, OpStages<T, N, OP, false>::value>;
     static int blocks_per_sm(int dev) {
         static std::mutex mu;
         static int cache[64] = {0};

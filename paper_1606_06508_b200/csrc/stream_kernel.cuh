@@ -525,15 +525,20 @@ struct TileLayout {
 #ifndef FNB_BIG_TILES
 #define FNB_BIG_TILES 1
 #endif
-template <typename T, int N, int OP> struct Rows3 {
+// BIG = false selects the default geometry for the same kernel: batches below
+// kBigTileRows rows and the many-batch kernel keep it (1e6-row batches: 0.84 vs 0.80 of
+// the copy peak as a graph-replayed stream, profiles/r02aa_many.txt).
+template <typename T, int N, int OP, bool BIG = true> struct Rows3 {
     static constexpr bool scaling = OP == FN_OP_NORMALIZE || OP == FN_OP_NORMALIZE_SQ || OP == FN_OP_SCALE;
-    static constexpr bool f64 = FNB_BIG_TILES && N == 3 && scaling && std::is_same<T, double>::value;
-    static constexpr bool f32 = FNB_BIG_TILES && N == 3 && OP == FN_OP_NORMALIZE && std::is_same<T, float>::value;
+    static constexpr bool f64 = BIG && FNB_BIG_TILES && N == 3 && scaling && std::is_same<T, double>::value;
+    static constexpr bool f32 = BIG && FNB_BIG_TILES && N == 3 && OP == FN_OP_NORMALIZE && std::is_same<T, float>::value;
+    static constexpr bool any = f64 || f32;
 };
+constexpr int64_t kBigTileRows = int64_t(1) << 24;
 
-template <typename T, int N, int OP> struct OpRows {
+template <typename T, int N, int OP, bool BIG = true> struct OpRows {
     static constexpr int kOutRow = (RowOp<T, N, OP>::W0 + RowOp<T, N, OP>::W1 + RowOp<T, N, OP>::W2) * (int)sizeof(T);
-    static constexpr int kTile = Rows3<T, N, OP>::f64 ? 512 : Tile<T, N>::kRows;
+    static constexpr int kTile = Rows3<T, N, OP, BIG>::f64 ? 512 : Tile<T, N>::kRows;
     static constexpr int kBase = (3 * kOutRow * kTile > 65536) ? kTile / 2 : kTile;
     static constexpr int value = DivBound<T, OP>::value ? kBase >> FNB_DIV_ROWS_SHIFT : kBase;
 };
@@ -548,7 +553,7 @@ template <typename T, int N, int OP> struct OpRows {
 #ifndef FNB_MAT_APPLY_STAGES
 #define FNB_MAT_APPLY_STAGES 3
 #endif
-template <typename T> struct OpRows<T, 9, FN_OP_MAT_APPLY> {
+template <typename T, bool BIG> struct OpRows<T, 9, FN_OP_MAT_APPLY, BIG> {
     static constexpr int value = FNB_MAT_APPLY_ROWS;
 };
 template <typename T> struct Tile<T, 9> {
@@ -562,10 +567,10 @@ template <typename T> struct Tile<T, 9> {
 // 112 B of it written) is tunable through FNB_NROT_ROWS / FNB_NROT_STAGES.  Through the
 // library (profiles/r01ca_nrot.txt): 128 x 3 (default) 6267 GB/s, 256 x 2 6308,
 // 128 x 4 5994, 256 x 3 5880 -- the tuner's ranking (r01bz_rot.csv) does not carry over.
-template <typename T, int N, int OP> struct OpStages {
+template <typename T, int N, int OP, bool BIG = true> struct OpStages {
     static constexpr int value = (DivBound<T, OP>::value && FNB_DIV_STAGES > 0) ? FNB_DIV_STAGES
-                                 : Rows3<T, N, OP>::f64                        ? 3
-                                 : Rows3<T, N, OP>::f32                        ? 5
+                                 : Rows3<T, N, OP, BIG>::f64                   ? 3
+                                 : Rows3<T, N, OP, BIG>::f32                   ? 5
                                                                                : Tile<T, N>::kStages;
 };
 // quotient2 f64 with two 512-row stages (4 CTAs per SM instead of 3) gained 9 % on
@@ -575,17 +580,17 @@ template <typename T, int N, int OP> struct OpStages {
 
 // Threads per CTA: one row per thread at least (a division-bound tile shrunk below 256
 // rows gets as many threads as rows).
-template <typename T, int N, int OP> struct OpThreads {
+template <typename T, int N, int OP, bool BIG = true> struct OpThreads {
     static constexpr int value =
-        OpRows<T, N, OP>::value < Tile<T, N>::kThreads ? OpRows<T, N, OP>::value : Tile<T, N>::kThreads;
+        OpRows<T, N, OP, BIG>::value < Tile<T, N>::kThreads ? OpRows<T, N, OP, BIG>::value : Tile<T, N>::kThreads;
 };
 #ifdef FNB_NROT_STAGES
-template <typename T, int N> struct OpStages<T, N, FN_OP_NORMALIZE_ROT> {
+template <typename T, int N, bool BIG> struct OpStages<T, N, FN_OP_NORMALIZE_ROT, BIG> {
     static constexpr int value = FNB_NROT_STAGES;
 };
 #endif
 #ifdef FNB_NROT_ROWS
-template <typename T, int N> struct OpRows<T, N, FN_OP_NORMALIZE_ROT> {
+template <typename T, int N, bool BIG> struct OpRows<T, N, FN_OP_NORMALIZE_ROT, BIG> {
     static constexpr int value = FNB_NROT_ROWS;
 };
 #endif
@@ -871,8 +876,8 @@ template <typename T> struct SegmentCursor {
     }
 };
 
-template <typename T, int N, int OP, int TR_ = OpRows<T, N, OP>::value, int S_ = OpStages<T, N, OP>::value,
-          int NT = Tile<T, N>::kThreads>
+template <typename T, int N, int OP, int TR_ = OpRows<T, N, OP, false>::value,
+          int S_ = OpStages<T, N, OP, false>::value, int NT = Tile<T, N>::kThreads>
 __global__ void __launch_bounds__(NT) tma_segments_kernel(const __grid_constant__ SegmentTable<T> tab,
                                                           KArgs<T> ka) {
     using L = TileLayout<T, N, OP, TR_, S_>;
