@@ -54,8 +54,8 @@ def main():
 
     rd = as_bytes(*got["dram__bytes_read.sum"])
     wr = as_bytes(*got["dram__bytes_write.sum"])
-    t_us = float(got["gpu__time_duration.sum"][0].replace(",", "")) * (
-        1e-3 if got["gpu__time_duration.sum"][1] == "nsecond" else 1.0)
+    t_us = float(got["gpu__time_duration.sum"][0].replace(",", "")) * {
+        "nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}[got["gpu__time_duration.sum"][1]]
     per_row = (rd + wr) / a.rows
     print(f"dram bytes per row: {per_row:.3f} (algorithmic {a.algo_bytes_per_row})")
     print(f"ncu duration: {t_us:.1f} us -> algorithmic {a.rows * a.algo_bytes_per_row / t_us / 1e3:.1f} GB/s "
