@@ -109,6 +109,20 @@ int fn_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, voi
 int fn_run_many(int op, int dim, int dtype, int nseg, const void* const* xs, const int64_t* ns,
                 void* const* heads, void* const* bodies, void* const* extras, const double* ka,
                 void* stream);
+/* One batch as device-resident row shards on several GPUs of this process, driven by one
+ * host thread (north star (c): one stream per device, no collective on the data path):
+ * shard k is xs[k] [ns[k], dim] on device devices[k] with outputs heads[k] / bodies[k] /
+ * extras[k] on the same device (bodies / extras may be NULL when the op has no such
+ * output).  Every shard's kernel is enqueued on a library-owned stream of its device
+ * before any is waited for, then all are synchronised: the call returns with every output
+ * complete.  after[k] (after may be NULL, and so may any entry) is a stream of device
+ * devices[k] whose already-enqueued work (the producer of xs[k]) the shard waits for.
+ * elapsed_ms[k] (may be NULL) receives shard k's device time by CUDA events on its stream.
+ * A device may be named more than once (one stream per shard).  Ops SCALE..NORMALIZE_SQ.
+ * No reference interface: the reference is CPU only and takes one row per call. */
+int fn_run_sharded(int op, int dim, int dtype, int nshard, const int* devices, const void* const* xs,
+                   const int64_t* ns, void* const* heads, void* const* bodies, void* const* extras,
+                   const double* ka, void* const* after, float* elapsed_ms);
 /* fn_run over rows that are ldx elements apart (ldx >= dim): row i is x[i*ldx .. i*ldx+dim),
  * the other ldx - dim elements of each record are not used.  Padded records such as xyz
  * in xyzw (dim 3, ldx 4; float4-style 16 B / 32 B records) and views like X[:, :3] of a

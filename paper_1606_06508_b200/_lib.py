@@ -58,6 +58,8 @@ def _declare(L: ctypes.CDLL) -> None:
     L.fn_run.argtypes = [_int, _int, _int, _vp, _i64, _vp, _vp, _vp, _vp, _vp]
     L.fn_run_many.restype = _int
     L.fn_run_many.argtypes = [_int, _int, _int, _int, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
+    L.fn_run_sharded.restype = _int
+    L.fn_run_sharded.argtypes = [_int, _int, _int, _int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
     L.fn_run_ld.restype = _int
     L.fn_run_ld.argtypes = [_int, _int, _int, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp]
     L.fn_host_run_ld.restype = _int

@@ -639,6 +639,15 @@ static int soa_path() {
     return v;
 }
 
+// FASTNORM_B200_SOA_DYN=0: the SoA bulk-copy kernel keeps the static tile schedule (A/B).
+static bool soa_dyn_enabled() {
+    static const bool v = [] {
+        const char* e = getenv("FASTNORM_B200_SOA_DYN");
+        return !(e && strcmp(e, "0") == 0);
+    }();
+    return v;
+}
+
 template <typename T, int N, int OP>
 static int launch_soa(const void* const* xs, int64_t n, void* head, void* const* body, void* sq,
                       const KArgs<T>& ka, cudaStream_t stream) {
@@ -687,8 +696,26 @@ static int launch_soa(const void* const* xs, int64_t n, void* head, void* const*
         }
         // whole runs whose loads (and their reach past a misaligned run) stay inside the arrays
         const int64_t ntiles = (n * (int64_t)sizeof(T) - reach) / ST::kArr;
-        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)sms * ST::kCtasPerSm));
-        if (ntiles > 0) e = launch_pdl(kern, grid, ST::NT, (size_t)smem, stream, p, ntiles, ka);
+        const int per_sm = cps_override() > 0 ? std::min(cps_override(), (int)(227 * 1024 / (smem + 1024))) : ST::kCtasPerSm;
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)sms * per_sm));
+        if (ntiles > 0) {
+            // the dynamic tile schedule of launch_tma_as (same counters, same rules)
+            KArgs<T> kd = ka;
+            kd.sched = kd.sched_next = nullptr;
+            SchedSlots* slots = (dyn_enabled() && soa_dyn_enabled() && ntiles > (int64_t)ST::S * grid)
+                                    ? sched_slots(dev, stream) : nullptr;
+            if (!slots) {
+                e = launch_pdl(kern, grid, ST::NT, (size_t)smem, stream, p, ntiles, kd);
+            } else {
+                std::lock_guard<std::mutex> lk(slots->mu);
+                const uint64_t i = slots->launches;
+                kd.sched = slots->ctr + (i & 1);
+                kd.sched_next = slots->ctr + ((i + 1) & 1);
+                kd.sched_batch = sched_batch_override() > 0 ? sched_batch_override() : 2;
+                e = launch_pdl(kern, grid, ST::NT, (size_t)smem, stream, p, ntiles, kd);
+                if (e == cudaSuccess) slots->launches = i + 1;
+            }
+        }
         if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
         const int64_t done = ntiles * ST::TR;
         if (done == n) return FN_OK;
@@ -1677,6 +1704,105 @@ int host_run_soa_multi(int op, int dim, int dtype, const void* const* xs, int64_
     });
 }
 
+// ---------------------------------------------------------------------------------
+// Device-resident shards on several GPUs, driven by one host thread (the north star's
+// single-process multi-GPU driver): shard k of the batch lives on device devices[k]
+// and runs on a stream of its own, so the devices work concurrently; no data moves
+// between devices (rows are independent, _kernels.pyx:167-412) and there is no
+// collective.  A device named more than once gets one stream per shard.
+// ---------------------------------------------------------------------------------
+struct ShardSlot {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t after = nullptr, t0 = nullptr, t1 = nullptr;
+};
+static std::mutex g_shard_mu;
+// g_shard_slots[dev][j]: the j-th shard stream of device dev; never destroyed
+static std::vector<std::vector<ShardSlot>>* g_shard_slots = new std::vector<std::vector<ShardSlot>>();
+
+// Called with the slot's device current.
+static int shard_slot(int dev, int j, ShardSlot* out) {
+    std::lock_guard<std::mutex> lk(g_shard_mu);
+    if ((int)g_shard_slots->size() <= dev) g_shard_slots->resize(dev + 1);
+    auto& v = (*g_shard_slots)[dev];
+    while ((int)v.size() <= j) {
+        ShardSlot s;
+        cudaError_t e = cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&s.after, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreate(&s.t0);
+        if (e == cudaSuccess) e = cudaEventCreate(&s.t1);
+        if (e != cudaSuccess) return cuda_fail(e, "shard stream setup");
+        v.push_back(s);
+    }
+    *out = v[j];
+    return FN_OK;
+}
+
+int run_sharded(int op, int dim, int dtype, int nshard, const int* devices, const void* const* xs,
+                const int64_t* ns, void* const* heads, void* const* bodies, void* const* extras,
+                const double* ka, void* const* after, float* elapsed_ms) {
+    if (nshard < 1) return fail(FN_EINVAL, "need at least one shard");
+    if (!devices || !xs || !ns || !heads) return fail(FN_EINVAL, "devices, xs, ns and heads must not be NULL");
+    if (op < FN_OP_SCALE || op > FN_OP_NORMALIZE_SQ)
+        return fail(FN_EINVAL, "the sharded entry takes the scale / normalize / norm / naive / quotient families");
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+    if (dim < 2 || dim > 4) return fail(FN_EINVAL, "dim must be 2, 3 or 4");
+    const Widths w = op_widths(op, dim);
+    if (w.w1 && !bodies) return fail(FN_EINVAL, "bodies must not be NULL for this op");
+    if (w.w2 && !extras) return fail(FN_EINVAL, "extras must not be NULL for this op");
+    for (int k = 0; k < nshard; ++k) {
+        if (devices[k] < 0 || devices[k] >= count) return fail(FN_EINVAL, "device index out of range");
+        const int rc = check_args(op, dim, dtype, xs[k], ns[k], heads[k], w.w1 ? bodies[k] : nullptr,
+                                  w.w2 ? extras[k] : nullptr);
+        if (rc != FN_OK) return fail(rc, "shard " + std::to_string(k) + ": " + g_last_error);
+    }
+    int home = 0;
+    e = cudaGetDevice(&home);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    std::vector<ShardSlot> slot(nshard);
+    std::vector<int> nth(nshard, 0);
+    int rc = FN_OK, enq = 0;
+    std::string err;
+    // pass 1: enqueue every shard on its device's stream without waiting for any of them
+    for (int k = 0; k < nshard && rc == FN_OK; ++k) {
+        for (int j = 0; j < k; ++j) nth[k] += devices[j] == devices[k];
+        e = cudaSetDevice(devices[k]);
+        if (e != cudaSuccess) { rc = cuda_fail(e, "cudaSetDevice"); break; }
+        rc = shard_slot(devices[k], nth[k], &slot[k]);
+        if (rc != FN_OK) break;
+        enq = k + 1;
+        const ShardSlot& s = slot[k];
+        if (after && after[k]) {  // the producer of xs[k] on this device
+            e = cudaEventRecord(s.after, static_cast<cudaStream_t>(after[k]));
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(s.stream, s.after, 0);
+            if (e != cudaSuccess) { rc = cuda_fail(e, "wait for the shard's producer stream"); break; }
+        }
+        if (elapsed_ms) cudaEventRecord(s.t0, s.stream);
+        if (ns[k] > 0)
+            rc = run(op, dim, dtype, xs[k], ns[k], heads[k], w.w1 ? bodies[k] : nullptr,
+                     w.w2 ? extras[k] : nullptr, ka, s.stream);
+        if (elapsed_ms) cudaEventRecord(s.t1, s.stream);
+        if (rc != FN_OK) err = "shard " + std::to_string(k) + " (device " + std::to_string(devices[k]) + "): " + g_last_error;
+    }
+    if (rc != FN_OK && err.empty()) err = g_last_error;
+    // pass 2: wait for every enqueued shard (also after an error: nothing stays in flight)
+    for (int k = 0; k < enq; ++k) {
+        if (cudaSetDevice(devices[k]) != cudaSuccess) continue;
+        e = cudaStreamSynchronize(slot[k].stream);
+        if (e != cudaSuccess && rc == FN_OK) {
+            rc = cuda_fail(e, "shard synchronise");
+            err = "shard " + std::to_string(k) + " (device " + std::to_string(devices[k]) + "): " + g_last_error;
+        }
+        if (elapsed_ms) {
+            elapsed_ms[k] = 0.f;
+            if (e == cudaSuccess) cudaEventElapsedTime(&elapsed_ms[k], slot[k].t0, slot[k].t1);
+        }
+    }
+    cudaSetDevice(home);
+    return rc == FN_OK ? FN_OK : fail(rc, err);
+}
+
 }  // namespace fnb
 
 // =====================================================================================
@@ -1703,6 +1829,12 @@ int fn_run(int op, int dim, int dtype, const void* x, int64_t n, void* head, voi
 int fn_run_many(int op, int dim, int dtype, int nseg, const void* const* xs, const int64_t* ns, void* const* heads,
                 void* const* bodies, void* const* extras, const double* ka, void* stream) {
     return fnb::run_many(op, dim, dtype, nseg, xs, ns, heads, bodies, extras, ka, stream);
+}
+
+int fn_run_sharded(int op, int dim, int dtype, int nshard, const int* devices, const void* const* xs,
+                   const int64_t* ns, void* const* heads, void* const* bodies, void* const* extras,
+                   const double* ka, void* const* after, float* elapsed_ms) {
+    return fnb::run_sharded(op, dim, dtype, nshard, devices, xs, ns, heads, bodies, extras, ka, after, elapsed_ms);
 }
 
 int fn_run_ld(int op, int dim, int dtype, const void* x, int64_t n, int64_t ldx, void* head, void* body,

@@ -1006,9 +1006,33 @@ __global__ void __launch_bounds__(256) tma_soa_kernel(SoaPtrs<T, N> p, int64_t n
     unsigned char* s_in = smem;
     unsigned char* s_out = smem + S * L::kInBytes;
     uint64_t* full = reinterpret_cast<uint64_t*>(s_out + OB * L::kOutBytes);
-    const int64_t my_tiles =
-        ntiles > (int64_t)blockIdx.x ? (ntiles - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
+    // Tile schedule: static round-robin, or (ka.sched != NULL) tma_stream_kernel's dynamic
+    // one -- the CTA's first S tiles static, then ka.sched_batch tiles per atomic claim,
+    // one claim ahead of use, tile ids handed to the threads through s_tile[].
+    unsigned* const sched = ka.sched;
+    const bool dyn = sched != nullptr;
+    __shared__ int64_t s_tile[S];
+    const int64_t my_tiles = dyn ? INT64_MAX
+        : (ntiles > (int64_t)blockIdx.x ? (ntiles - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0);
     const bool leader = threadIdx.x == 0;
+    bool claiming = true;
+    unsigned ahead = 0;
+    int64_t cur = 0, end = 0;
+    const int batch = dyn ? ka.sched_batch : 1;
+    auto claim = [&](int64_t k) -> int64_t {
+        int64_t t;
+        if (k < S) {
+            t = (int64_t)blockIdx.x + k * gridDim.x;
+        } else {
+            if (cur == end) {
+                cur = (int64_t)S * gridDim.x + (int64_t)ahead * batch;
+                end = cur + batch;
+                if (cur < ntiles) ahead = atomicAdd(&sched[0], 1u);
+            }
+            t = cur++;
+        }
+        return t < ntiles ? t : -1;
+    };
     int mis[N];
     uint32_t tx = 0;
 #pragma unroll
@@ -1024,6 +1048,7 @@ __global__ void __launch_bounds__(256) tma_soa_kernel(SoaPtrs<T, N> p, int64_t n
     __syncthreads();
     grid_dependency_wait();
     grid_launch_dependents();
+    if (dyn && blockIdx.x == 0 && threadIdx.x == 0) *ka.sched_next = 0u;
     auto load_stage = [&](int st, int64_t tile) {
         mbar_arrive_expect_tx(&full[st], tx);
 #pragma unroll
@@ -1032,13 +1057,31 @@ __global__ void __launch_bounds__(256) tma_soa_kernel(SoaPtrs<T, N> p, int64_t n
                             reinterpret_cast<const unsigned char*>(p.x[c]) - mis[c] + tile * L::kArr,
                             L::kArr + (mis[c] ? 16 : 0), &full[st]);
     };
-    if (leader)
-        for (int64_t k = 0; k < my_tiles && k < S; ++k) load_stage((int)k, (int64_t)blockIdx.x + k * gridDim.x);
+    auto fill_dyn = [&](int st, int64_t k) {
+        if (!claiming) return;
+        const int64_t t = claim(k);
+        s_tile[st] = t;
+        if (t >= 0) {
+            load_stage(st, t);
+        } else {
+            claiming = false;
+            mbar_arrive(&full[st]);  // completes the phase with no bytes: "no tile"
+        }
+    };
+    if (leader) {
+        if (dyn) {
+            for (int k = 0; k < S; ++k) fill_dyn(k, k);
+            if (claiming) ahead = atomicAdd(&sched[0], 1u);
+        } else {
+            for (int64_t k = 0; k < my_tiles && k < S; ++k) load_stage((int)k, (int64_t)blockIdx.x + k * gridDim.x);
+        }
+    }
     for (int64_t k = 0; k < my_tiles; ++k) {
         const int st = (int)(k % S);
         const int ob = (int)(k % OB);
-        const int64_t tile = (int64_t)blockIdx.x + k * gridDim.x;
         mbar_wait(&full[st], (uint32_t)((k / S) & 1));
+        const int64_t tile = dyn ? s_tile[st] : (int64_t)blockIdx.x + k * gridDim.x;
+        if (tile < 0) break;  // dynamic schedule exhausted (uniform across the CTA)
         const unsigned char* tin = s_in + st * L::kInBytes;
         T* tout = reinterpret_cast<T*>(s_out + ob * L::kOutBytes);
 #pragma unroll
@@ -1063,7 +1106,10 @@ __global__ void __launch_bounds__(256) tma_soa_kernel(SoaPtrs<T, N> p, int64_t n
             for (int c = 0; c < W1; ++c) bulk_store(p.body[c] + row0, tout + (1 + c) * TR, L::kArr);
             if constexpr (W2 == 1) bulk_store(p.extra + row0, tout + (1 + W1) * TR, L::kArr);
             bulk_commit();
-            if (k + S < my_tiles) load_stage(st, tile + (int64_t)S * gridDim.x);
+            if (dyn)
+                fill_dyn(st, k + S);
+            else if (k + S < my_tiles)
+                load_stage(st, tile + (int64_t)S * gridDim.x);
             bulk_wait_read<OB - 2>();
         }
     }
