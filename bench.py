@@ -613,6 +613,38 @@ def run_ours(args):
     counts_h = multigpu.reduce_counts(multigpu.shard_counts_device(x, ka).to(cdev))
     torch.cuda.synchronize(dev)
 
+    # ---------------- single-process multi-GPU driver (informational, N = 1) ----------------
+    # The same rows as two device-resident shards through fn_run_sharded, both on this
+    # rank's GPU (the rows live here): this measures the driver's overhead against the
+    # one-launch step above, not scaling.  Shards are views of x / r / u: nothing is allocated.
+    sharded = None
+    if world == 1 and not args.no_configs:
+        try:
+            devs = [local % ndev] * 2
+            cuts = [shard_range(n, k, len(devs)) for k in range(len(devs))]
+            xs_sh = multigpu.DeviceShards([x[lo:hi] for lo, hi in cuts])
+            out_sh = (multigpu.DeviceShards([r[lo:hi] for lo, hi in cuts]),
+                      multigpu.DeviceShards([u[lo:hi] for lo, hi in cuts]))
+            for _ in range(2):
+                multigpu.normalize_sharded(p, xs_sh, out=out_sh)
+            k0 = _lib_handle().fn_launch_count()
+            ms, wall = [], []
+            for _ in range(5):
+                torch.cuda.synchronize(dev)
+                t0 = time.perf_counter()
+                res = multigpu.normalize_sharded(p, xs_sh, out=out_sh)
+                wall.append(time.perf_counter() - t0)
+                ms.append(max(res.elapsed_ms))
+            t_sh = statistics.median(ms) / 1e3
+            sharded = {"api": "multigpu.normalize_sharded(p, DeviceShards) -> fn_run_sharded (one stream per shard)",
+                       "devices": devs, "rows": n, "ms_device_max_over_shards": t_sh * 1e3,
+                       "ms_host_wall": statistics.median(wall) * 1e3, "vectors_per_s": n / t_sh,
+                       "GB_per_s": n * BYTES_PER_ROW / t_sh / 1e9,
+                       "gpu_launches": int(_lib_handle().fn_launch_count() - k0)}
+            del xs_sh, out_sh, res
+        except Exception as exc:  # informational only: never lose the headline line
+            sharded = {"error": str(exc)}
+
     # ---------------- end to end through the public API, host buffers ----------------
     # Every rank pins its shard's input and outputs (56 B/row).  If the host cannot hold
     # all ranks' shards with a 30 % margin, the e2e pass runs on the largest prefix of
@@ -760,6 +792,7 @@ def run_ours(args):
             "host_cpus": "NUMA-local to the GPU" if numa.cpus else "all (topology unknown)",
         },
         "e2e_default_api": default_api,
+        "sharded_driver": sharded,
         "validation": {
             "row_classes": dict(zip(multigpu.COUNTER_NAMES, counts_h)),
             "rows_counted": int(sum(counts_h)),

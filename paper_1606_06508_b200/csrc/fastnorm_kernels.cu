@@ -696,7 +696,10 @@ static int launch_soa(const void* const* xs, int64_t n, void* head, void* const*
         }
         // whole runs whose loads (and their reach past a misaligned run) stay inside the arrays
         const int64_t ntiles = (n * (int64_t)sizeof(T) - reach) / ST::kArr;
-        const int per_sm = cps_override() > 0 ? std::min(cps_override(), (int)(227 * 1024 / (smem + 1024))) : ST::kCtasPerSm;
+        // CTAs per SM: 3 where the shared memory holds them (2-D rows: 6433-6553 -> 6873 GB/s,
+        // profiles/r02af_soa_ctas.txt), else what fits (3-D and 4-D rows: 2)
+        const int fit = std::max(1, (int)(227 * 1024 / (smem + 1024)));
+        const int per_sm = std::min(cps_override() > 0 ? cps_override() : ST::kCtasPerSm, fit);
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)sms * per_sm));
         if (ntiles > 0) {
             // the dynamic tile schedule of launch_tma_as (same counters, same rules)

@@ -968,9 +968,11 @@ __global__ void __launch_bounds__(NT) tma_segments_kernel(const __grid_constant_
 // staged per array and written with one bulk store each.  Same ring / mbarrier /
 // store-group protocol as tma_stream_kernel.
 // ---------------------------------------------------------------------------------
-// 4 KiB runs x 3 stages x 2 CTAs per SM: 0.96 of the copy peak for normalize2/3 f64 and
-// normalize3 f32 (2 KiB runs: 0.84-0.94; 8 KiB: 0.90-1.02; more stages or CTAs lose;
-// profiles/r01da_soa.txt).
+// 4 KiB runs x 3 stages: 0.96 of the copy peak for normalize2/3 f64 and normalize3 f32
+// under round 1's static schedule at 2 CTAs per SM (2 KiB runs: 0.84-0.94; 8 KiB:
+// 0.90-1.02; profiles/r01da_soa.txt).  With the dynamic schedule (round 2) the same
+// geometry reaches 6870-6910 GB/s (1.06-1.07; profiles/r02ae_soa_ab.txt) with up to 3
+// CTAs per SM where the shared memory holds them (the host clamps to what fits).
 #ifndef FNB_SOA_RUN_BYTES
 #define FNB_SOA_RUN_BYTES 4096
 #endif
@@ -978,7 +980,7 @@ __global__ void __launch_bounds__(NT) tma_segments_kernel(const __grid_constant_
 #define FNB_SOA_STAGES 3
 #endif
 #ifndef FNB_SOA_CTAS_PER_SM
-#define FNB_SOA_CTAS_PER_SM 2
+#define FNB_SOA_CTAS_PER_SM 3
 #endif
 template <typename T, int N, int OP, bool MIS = false> struct SoaTile {
     using Op = RowOp<T, N, OP>;

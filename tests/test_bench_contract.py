@@ -52,3 +52,6 @@ def test_our_arm_line(cuda_dev):
     oc = d["other_configs"]
     assert {1, 2, 3, 4} <= {c["config"] for c in oc} <= {1, 2, 3, 4, 5}
     assert all(c["frac"] > 0.2 for c in oc)
+    sd = d["sharded_driver"]
+    assert "error" not in sd and len(sd["devices"]) == 2 and sd["rows"] == 1 << 30
+    assert sd["gpu_launches"] == 10 and sd["vectors_per_s"] > 50e9

@@ -62,7 +62,7 @@ def test_normalize_sharded_bit_exact(cfg):
         res = multigpu.normalize_sharded(p, sh)
         assert res.sq is None and len(res.elapsed_ms) == len(devs)
         assert all(ms > 0 for ms in res.elapsed_ms)
-        assert torch.equal(_bits(res.head.gather()), _bits(ref.r))
+        assert torch.equal(_bits(res.head.gather()), _bits(ref.length))
         assert torch.equal(_bits(res.body.gather()), _bits(ref.unit))
         nr = multigpu.norm_sharded(p, sh)
         assert nr.body is None
@@ -136,7 +136,7 @@ def test_sharded_empty_and_ragged_shards():
             whole = torch.empty((rows, 3), dtype=torch.float64, device="cuda:0")
             workloads.generate_device(5, whole)
             ref = fn.normalize3(p, whole)
-            assert torch.equal(_bits(res.head.gather()), _bits(ref.r))
+            assert torch.equal(_bits(res.head.gather()), _bits(ref.length))
             assert torch.equal(_bits(res.body.gather()), _bits(ref.unit))
 
 
