@@ -207,9 +207,9 @@ template <int N> struct PaddedLdx {
 // complete.  The host takes i and launches under one lock, so the counter order matches
 // the stream order even when several threads launch on the same stream.  Launches on
 // different streams never share counters.  Batches with at most S tiles per CTA (nothing
-// to balance) and launches under stream capture (a graph could be replayed on several
-// streams at once) take the static schedule.  FASTNORM_B200_DYN=0 forces the static
-// schedule everywhere.
+// to balance) take the static schedule; launches under stream capture take a counter of
+// their own (capture_pair below).  The streaming, SoA and many-batch kernels share this
+// code (sched_lease).  FASTNORM_B200_DYN=0 forces the static schedule everywhere.
 static bool dyn_enabled() {
     static const bool v = [] {
         const char* e = getenv("FASTNORM_B200_DYN");
@@ -240,14 +240,70 @@ struct SchedSlots {
 static std::mutex g_sched_mu;
 static std::vector<std::unique_ptr<SchedSlots>>* g_sched = new std::vector<std::unique_ptr<SchedSlots>>();
 
-static SchedSlots* sched_slots(int dev, cudaStream_t stream) {
+// Captured launches (CUDA graphs): a graph may be replayed on any stream, so a captured
+// kernel node cannot share a stream's alternating pair.  It gets a {counter, done} pair of
+// its own from a per-device pool, and its last CTA re-zeroes the pair for the node's next
+// replay (sched_report_done).  The pool is allocated and zeroed by the device's first
+// eager dynamic launch (cudaMalloc is not allowed while a stream captures); a capture
+// before that, or after the pool's kCapturePairs pairs are handed out, takes the static
+// schedule.  Two instances of one captured node running at the same time would share the
+// pair -- and already race on their output buffers.  FASTNORM_B200_DYN_CAPTURE=0 keeps
+// captured launches static.
+constexpr int kCapturePairs = 16384;
+struct CapturePool {
+    unsigned* base = nullptr;
+    int next = 0;
+};
+static std::vector<CapturePool>* g_capture = new std::vector<CapturePool>();  // by device, under g_sched_mu
+
+static bool dyn_capture_enabled() {
+    static const bool v = [] {
+        const char* e = getenv("FASTNORM_B200_DYN_CAPTURE");
+        return !(e && strcmp(e, "0") == 0);
+    }();
+    return v;
+}
+
+// Called without a capture in progress on `stream`, g_sched_mu held.
+static void capture_pool_init(int dev, cudaStream_t stream) {
+    if ((int)g_capture->size() <= dev) g_capture->resize(dev + 1);
+    CapturePool& cp = (*g_capture)[dev];
+    if (cp.base || cp.next < 0) return;
+    unsigned* p = nullptr;
+    const size_t bytes = (size_t)kCapturePairs * 2 * sizeof(unsigned);
+    if (cudaMalloc(&p, bytes) != cudaSuccess || cudaMemsetAsync(p, 0, bytes, stream) != cudaSuccess ||
+        cudaStreamSynchronize(stream) != cudaSuccess) {
+        cudaGetLastError();
+        if (p) cudaFree(p);
+        cp.next = -1;  // do not try again
+        return;
+    }
+    cp.base = p;
+}
+
+static unsigned* capture_pair(int dev) {
+    std::lock_guard<std::mutex> lk(g_sched_mu);
+    if (!dyn_capture_enabled() || (int)g_capture->size() <= dev) return nullptr;
+    CapturePool& cp = (*g_capture)[dev];
+    if (!cp.base || cp.next >= kCapturePairs) return nullptr;
+    return cp.base + 2 * (cp.next++);
+}
+
+static bool stream_capturing(cudaStream_t stream, bool* known) {
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(stream, &cap) != cudaSuccess) {
         cudaGetLastError();
-        return nullptr;
+        *known = false;
+        return false;
     }
-    if (cap != cudaStreamCaptureStatusNone) return nullptr;
+    *known = true;
+    return cap != cudaStreamCaptureStatusNone;
+}
+
+// The per-stream pair of an eager launch (not capturing).
+static SchedSlots* sched_slots(int dev, cudaStream_t stream) {
     std::lock_guard<std::mutex> lk(g_sched_mu);
+    capture_pool_init(dev, stream);
     for (auto& e : *g_sched)
         if (e->dev == dev && e->stream == stream) return e.get();
     unsigned* p = nullptr;
@@ -269,6 +325,60 @@ static SchedSlots* sched_slots(int dev, cudaStream_t stream) {
     return g_sched->back().get();
 }
 
+// The tile schedule of one launch.  Fills kd.sched* (all NULL: static schedule) and, for an
+// eager dynamic launch, holds the stream's lock until the launch is made; commit() after a
+// successful launch advances the stream's alternation.
+struct SchedLease {
+    SchedSlots* slots = nullptr;
+    std::unique_lock<std::mutex> lk;
+    uint64_t i = 0;
+    void commit() {
+        if (slots) slots->launches = i + 1;
+    }
+};
+// Tiles per atomic claim.  2 everywhere (measured against 1, 4, 8 and 16 on nine kernel /
+// config pairs, profiles/r02t_sched_batch_table.txt: one tile per claim loses up to 25 %
+// where many CTAs claim short tiles -- the counter's round trip is on every tile's path --
+// and larger batches lose balance: normalize3 config 5 +3.7 % at 2, +2.3 % at 8 over the
+// static schedule) except the norm kernels, which take 4: their tiles are the shortest
+// (24 B in, 8 B out per row) and at 2 tiles per claim they fall into a slow mode on some
+// boxes and builds (norm3 f64, 2^28 rows: 4900-5070 GB/s at 2, 7200 at 4, 7150 at 8, static
+// 6460-6670; profiles/r02ak_norm3_batch.txt), while 4 costs 0.3 % where 2 runs well.
+template <int OP> struct SchedBatch {
+    static constexpr int value = OP == FN_OP_NORM ? 4 : 2;
+};
+
+// `tiles_per_cta`: whole tiles over resident CTAs.  Captured launches with fewer than 32
+// (config-1-sized batches, where the schedule gains nothing in eager mode either) stay
+// static: the report at the end of a self-resetting launch costs them ~1.4 us per launch
+// (7.5 -> 8.9 us, profiles/r02ah_graph_dyn.jsonl).
+template <typename T>
+static SchedLease sched_lease(bool want, int batch, int64_t tiles_per_cta, int dev, cudaStream_t stream,
+                              KArgs<T>& kd) {
+    SchedLease l;
+    kd.sched = kd.sched_next = kd.sched_done = nullptr;
+    if (!want || !dyn_enabled()) return l;
+    kd.sched_batch = sched_batch_override() > 0 ? sched_batch_override() : batch;
+    bool known = false;
+    if (stream_capturing(stream, &known)) {
+        unsigned* pair = tiles_per_cta >= 32 ? capture_pair(dev) : nullptr;
+        if (pair) {
+            kd.sched = pair;
+            kd.sched_done = pair + 1;
+        }
+        return l;
+    }
+    if (!known) return l;
+    SchedSlots* slots = sched_slots(dev, stream);
+    if (!slots) return l;
+    l.slots = slots;
+    l.lk = std::unique_lock<std::mutex>(slots->mu);
+    l.i = slots->launches;
+    kd.sched = slots->ctr + (l.i & 1);
+    kd.sched_next = slots->ctr + ((l.i + 1) & 1);
+    return l;
+}
+
 template <typename T, int N, int OP, int LDX, bool MIS, bool BIG>
 static cudaError_t launch_tma_as(const T* x, const T* x2, int64_t n, T* head, T* body, T* extra,
                                  const KArgs<T>& ka, int dev, int sms, cudaStream_t stream) {
@@ -279,25 +389,11 @@ static cudaError_t launch_tma_as(const T* x, const T* x2, int64_t n, T* head, T*
     const int64_t resident = per_sm * sms;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, resident));
     KArgs<T> kd = ka;
-    kd.sched = kd.sched_next = nullptr;
-    SchedSlots* slots = (dyn_enabled() && DynamicSchedule<T, N, OP>::value && ntiles > (int64_t)L::S * grid)
-                            ? sched_slots(dev, stream) : nullptr;
-    if (!slots)
-        return launch_pdl(TL::kernel(), grid, TL::kThreads, L::kSmemBytes, stream, x, x2, n, head, body,
-                          extra, kd);
-    std::lock_guard<std::mutex> lk(slots->mu);
-    const uint64_t i = slots->launches;
-    kd.sched = slots->ctr + (i & 1);
-    kd.sched_next = slots->ctr + ((i + 1) & 1);
-    // tiles per claim: 2.  Measured against 1, 4, 8 and 16 on nine kernel / config pairs
-    // (profiles/r02t_sched_batch_table.txt): one tile per claim loses up to 25 % where
-    // many CTAs claim short tiles (the counter's round trip is on every tile's path),
-    // larger batches lose balance (normalize3 config 5: +3.7 % at 2, +2.3 % at 8 over
-    // the static schedule).
-    kd.sched_batch = sched_batch_override() > 0 ? sched_batch_override() : 2;
+    SchedLease lease = sched_lease(DynamicSchedule<T, N, OP>::value && ntiles > (int64_t)L::S * grid,
+                                   SchedBatch<OP>::value, ntiles / grid, dev, stream, kd);
     const cudaError_t e = launch_pdl(TL::kernel(), grid, TL::kThreads, L::kSmemBytes, stream, x, x2, n,
                                      head, body, extra, kd);
-    if (e == cudaSuccess) slots->launches = i + 1;
+    if (e == cudaSuccess) lease.commit();
     return e;
 }
 
@@ -499,6 +595,15 @@ int run_ex(int op, int dim, int dtype, const void* x, int64_t n, void* head, voi
 // ---------------------------------------------------------------------------------
 // Many independent batches (segments) per launch: fn_run_many.
 // ---------------------------------------------------------------------------------
+// FASTNORM_B200_MANY_DYN=0: the many-batch kernel keeps the static tile schedule (A/B).
+static bool many_dyn_enabled() {
+    static const bool v = [] {
+        const char* e = getenv("FASTNORM_B200_MANY_DYN");
+        return !(e && strcmp(e, "0") == 0);
+    }();
+    return v;
+}
+
 template <typename T, int N, int OP> struct SegLaunch {
     using L = TileLayout<T, N, OP, OpRows<T, N, OP, false>::value, OpStages<T, N, OP, false>::value>;
     static int blocks_per_sm(int dev) {
@@ -538,9 +643,13 @@ static int launch_many(int nseg, const void* const* xs, const int64_t* ns, void*
         const int64_t work = std::max<int64_t>(tab.ntiles, 1);
         const int64_t per_sm = std::min<int64_t>(SL::blocks_per_sm(dev), ctas_per_sm_for<T, N, OP>(tab.ntiles, sms));
         const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(work, tab.nseg), per_sm * sms));
+        KArgs<T> kd = ka;
+        SchedLease lease = sched_lease(many_dyn_enabled() && tab.ntiles > (int64_t)L::S * grid, SchedBatch<OP>::value,
+                                       tab.ntiles / grid, dev, stream, kd);
         const cudaError_t le = launch_pdl(tma_segments_kernel<T, N, OP>, grid, Tile<T, N>::kThreads, L::kSmemBytes,
-                                          stream, tab, ka);
+                                          stream, tab, kd);
         if (le != cudaSuccess) return cuda_fail(le, "kernel launch");
+        lease.commit();
         tab.nseg = 0;
         tab.ntiles = 0;
         return FN_OK;
@@ -704,20 +813,10 @@ static int launch_soa(const void* const* xs, int64_t n, void* head, void* const*
         if (ntiles > 0) {
             // the dynamic tile schedule of launch_tma_as (same counters, same rules)
             KArgs<T> kd = ka;
-            kd.sched = kd.sched_next = nullptr;
-            SchedSlots* slots = (dyn_enabled() && soa_dyn_enabled() && ntiles > (int64_t)ST::S * grid)
-                                    ? sched_slots(dev, stream) : nullptr;
-            if (!slots) {
-                e = launch_pdl(kern, grid, ST::NT, (size_t)smem, stream, p, ntiles, kd);
-            } else {
-                std::lock_guard<std::mutex> lk(slots->mu);
-                const uint64_t i = slots->launches;
-                kd.sched = slots->ctr + (i & 1);
-                kd.sched_next = slots->ctr + ((i + 1) & 1);
-                kd.sched_batch = sched_batch_override() > 0 ? sched_batch_override() : 2;
-                e = launch_pdl(kern, grid, ST::NT, (size_t)smem, stream, p, ntiles, kd);
-                if (e == cudaSuccess) slots->launches = i + 1;
-            }
+            SchedLease lease = sched_lease(soa_dyn_enabled() && ntiles > (int64_t)ST::S * grid, SchedBatch<OP>::value,
+                                           ntiles / grid, dev, stream, kd);
+            e = launch_pdl(kern, grid, ST::NT, (size_t)smem, stream, p, ntiles, kd);
+            if (e == cudaSuccess) lease.commit();
         }
         if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
         const int64_t done = ntiles * ST::TR;

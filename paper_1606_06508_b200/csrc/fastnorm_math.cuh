@@ -119,7 +119,10 @@ template <typename T> struct KArgs {
     unsigned long long* invalid;  // rows rejected by the rotations (may be NULL)
     unsigned* sched;              // tma_stream_kernel's dynamic tile counter (NULL: the
                                   // static round-robin schedule)
-    unsigned* sched_next;         // the counter of the next launch on the stream (zeroed here)
+    unsigned* sched_next;         // the counter of the next launch on the stream (zeroed here;
+                                  // NULL for captured launches)
+    unsigned* sched_done;         // captured launches: CTAs finished; the last one re-zeroes
+                                  // sched and this word for the next replay (NULL otherwise)
     int sched_batch;              // tiles per claim of the dynamic schedule
     T rot[9];           // FN_OP_ROT_APPLY: the matrix, row-major
 };

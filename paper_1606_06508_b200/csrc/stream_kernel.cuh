@@ -192,6 +192,23 @@ __device__ __forceinline__ bool row_global(const T* __restrict__ x, const T* __r
     return ok;
 }
 
+// Captured launches (CUDA graphs) own their counter instead of alternating a per-stream
+// pair: every CTA's leader reports in after its last claim, and the last one to do so
+// zeroes the counter and the report word, so the node's next replay starts from zero.
+// (A graph's launches are ordered by the graph; griddepcontrol.wait in the successor
+// covers these stores like any other write of the predecessor.)
+template <typename T>
+__device__ __forceinline__ void sched_report_done(const KArgs<T>& ka) {
+    if (ka.sched != nullptr && ka.sched_done != nullptr) {
+        __threadfence();
+        if (atomicAdd(ka.sched_done, 1u) == gridDim.x - 1) {
+            *ka.sched = 0u;
+            *ka.sched_done = 0u;
+            __threadfence();
+        }
+    }
+}
+
 // Per-thread count of rejected rows -> one atomic per warp (rotations only).
 __device__ __forceinline__ void count_invalid(unsigned long long* counter, unsigned long long bad) {
     if (counter == nullptr) return;
@@ -720,7 +737,7 @@ __global__ void __launch_bounds__(NT, MinBlocks<T, OP>::value) tma_stream_kernel
     __syncthreads();
     grid_dependency_wait();
     grid_launch_dependents();
-    if (dyn && blockIdx.x == 0 && threadIdx.x == 0) *ka.sched_next = 0u;
+    if (dyn && blockIdx.x == 0 && threadIdx.x == 0 && ka.sched_next != nullptr) *ka.sched_next = 0u;
     timeline_mark(1);
     // One stage = the tile's input records (and its second-input records), one mbarrier.
     auto load_stage = [&](int st, int64_t tile) {
@@ -833,7 +850,10 @@ __global__ void __launch_bounds__(NT, MinBlocks<T, OP>::value) tma_stream_kernel
     }
     timeline_mark(3);
     count_invalid(ka.invalid, bad);
-    if (leader) bulk_wait_all();
+    if (leader) {
+        sched_report_done(ka);
+        bulk_wait_all();
+    }
     timeline_mark(4);
 }
 
@@ -890,10 +910,33 @@ __global__ void __launch_bounds__(NT) tma_segments_kernel(const __grid_constant_
     unsigned char* s_out = smem + S * L::kInBytes;
     uint64_t* full = reinterpret_cast<uint64_t*>(s_out + OB * L::kOutBytes);
     const int64_t ntiles = tab.ntiles;
-    const int64_t my_tiles =
-        ntiles > (int64_t)blockIdx.x ? (ntiles - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
+    // Tile schedule: static round-robin, or (ka.sched != NULL) tma_stream_kernel's dynamic
+    // one.  Either way a CTA's tiles come in increasing order, which the cursors need.
+    unsigned* const sched = ka.sched;
+    const bool dyn = sched != nullptr;
+    __shared__ int64_t s_tile[S];
+    const int64_t my_tiles = dyn ? INT64_MAX
+        : (ntiles > (int64_t)blockIdx.x ? (ntiles - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0);
     const bool leader = threadIdx.x == 0;
     unsigned long long bad = 0;
+    bool claiming = true;
+    unsigned ahead = 0;
+    int64_t cur = 0, end = 0;
+    const int batch = dyn ? ka.sched_batch : 1;
+    auto claim = [&](int64_t k) -> int64_t {
+        int64_t t;
+        if (k < S) {
+            t = (int64_t)blockIdx.x + k * gridDim.x;
+        } else {
+            if (cur == end) {
+                cur = (int64_t)S * gridDim.x + (int64_t)ahead * batch;
+                end = cur + batch;
+                if (cur < ntiles) ahead = atomicAdd(&sched[0], 1u);
+            }
+            t = cur++;
+        }
+        return t < ntiles ? t : -1;
+    };
     if (leader) {
 #pragma unroll
         for (int st = 0; st < S; ++st) mbar_init(&full[st], 1);
@@ -902,6 +945,7 @@ __global__ void __launch_bounds__(NT) tma_segments_kernel(const __grid_constant_
     __syncthreads();
     grid_dependency_wait();
     grid_launch_dependents();
+    if (dyn && blockIdx.x == 0 && threadIdx.x == 0 && ka.sched_next != nullptr) *ka.sched_next = 0u;
     SegmentCursor<T> lc, sc;  // segment cursors of the loads (S tiles ahead) and the stores
     auto load_stage = [&](int st, int64_t g) {
         lc.advance(tab, g);
@@ -909,12 +953,30 @@ __global__ void __launch_bounds__(NT) tma_segments_kernel(const __grid_constant_
         mbar_arrive_expect_tx(&full[st], L::kInBytes);
         bulk_load_plain(s_in + st * L::kInBytes, sg.x + (g - sg.tile0) * TR * N, L::kInBytes, &full[st]);
     };
-    if (leader)
-        for (int64_t k = 0; k < my_tiles && k < S; ++k) load_stage((int)k, (int64_t)blockIdx.x + k * gridDim.x);
+    auto fill_dyn = [&](int st, int64_t k) {
+        if (!claiming) return;
+        const int64_t t = claim(k);
+        s_tile[st] = t;
+        if (t >= 0) {
+            load_stage(st, t);
+        } else {
+            claiming = false;
+            mbar_arrive(&full[st]);  // completes the phase with no bytes: "no tile"
+        }
+    };
+    if (leader) {
+        if (dyn) {
+            for (int k = 0; k < S; ++k) fill_dyn(k, k);
+            if (claiming) ahead = atomicAdd(&sched[0], 1u);
+        } else {
+            for (int64_t k = 0; k < my_tiles && k < S; ++k) load_stage((int)k, (int64_t)blockIdx.x + k * gridDim.x);
+        }
+    }
     for (int64_t k = 0; k < my_tiles; ++k) {
         const int st = (int)(k % S), ob = (int)(k % OB);
-        const int64_t g = (int64_t)blockIdx.x + k * gridDim.x;
         mbar_wait(&full[st], (uint32_t)((k / S) & 1));
+        const int64_t g = dyn ? s_tile[st] : (int64_t)blockIdx.x + k * gridDim.x;
+        if (g < 0) break;  // dynamic schedule exhausted (uniform across the CTA)
         const T* tin = reinterpret_cast<const T*>(s_in + st * L::kInBytes);
         T* t0 = reinterpret_cast<T*>(s_out + ob * L::kOutBytes);
         T* t1 = t0 + TR * W0;
@@ -947,10 +1009,14 @@ __global__ void __launch_bounds__(NT) tma_segments_kernel(const __grid_constant_
             if (W1) bulk_store(sg.body + row0 * W1, t1, L::kB1);
             if (W2) bulk_store(sg.extra + row0 * W2, t2, L::kB2);
             bulk_commit();
-            if (k + S < my_tiles) load_stage(st, g + (int64_t)S * gridDim.x);
+            if (dyn)
+                fill_dyn(st, k + S);
+            else if (k + S < my_tiles)
+                load_stage(st, g + (int64_t)S * gridDim.x);
             bulk_wait_read<OB - 2>();
         }
     }
+    if (leader) sched_report_done(ka);
     // rows after each segment's last whole tile: segment j in CTA j % gridDim.x
     for (int j = (int)blockIdx.x; j < tab.nseg; j += (int)gridDim.x) {
         const Segment<T>& sg = tab.seg[j];
@@ -1050,7 +1116,7 @@ __global__ void __launch_bounds__(256) tma_soa_kernel(SoaPtrs<T, N> p, int64_t n
     __syncthreads();
     grid_dependency_wait();
     grid_launch_dependents();
-    if (dyn && blockIdx.x == 0 && threadIdx.x == 0) *ka.sched_next = 0u;
+    if (dyn && blockIdx.x == 0 && threadIdx.x == 0 && ka.sched_next != nullptr) *ka.sched_next = 0u;
     auto load_stage = [&](int st, int64_t tile) {
         mbar_arrive_expect_tx(&full[st], tx);
 #pragma unroll
@@ -1115,7 +1181,10 @@ __global__ void __launch_bounds__(256) tma_soa_kernel(SoaPtrs<T, N> p, int64_t n
             bulk_wait_read<OB - 2>();
         }
     }
-    if (leader) bulk_wait_all();
+    if (leader) {
+        sched_report_done(ka);
+        bulk_wait_all();
+    }
 }
 
 }  // namespace fnb

@@ -4,8 +4,8 @@ tiles per CTA; a {next, done} counter pair per stream, reset by the kernel's las
 The schedule changes which CTA computes a tile, never what is computed: outputs must be
 bit-identical to the oracle and to the static schedule (FASTNORM_B200_DYN=0), across
 back-to-back launches on one stream (the counter is reset between them, PDL included),
-on two streams at once (each stream has its own pair), and in CUDA graphs (captured
-launches take the static schedule)."""
+on two streams at once (each stream has its own pair), and in CUDA graphs (a captured
+launch owns a counter that its last CTA re-zeroes for the next replay)."""
 
 import os
 import subprocess
@@ -85,7 +85,11 @@ def test_two_streams_at_once(cuda_dev):
         assert torch.equal(ob[k][0].view(torch.int64), wb.length.view(torch.int64))
 
 
-def test_graph_capture_takes_static_schedule(cuda_dev):
+def _i64(t):
+    return t.view(torch.int64 if t.dtype == torch.float64 else torch.int32)
+
+
+def test_graph_capture_small_batch(cuda_dev):
     p = fn.preset("double")
     x = _rows(1_000_000, 1)
     want = fn.normalize3(p, x)
@@ -107,6 +111,66 @@ def test_graph_capture_takes_static_schedule(cuda_dev):
     assert torch.equal(r.view(torch.int64), want.length.view(torch.int64))
 
 
+def test_graph_capture_dynamic_schedule_replays(cuda_dev):
+    """Captured launches claim tiles from a counter of their own that the kernel's last CTA
+    re-zeroes: a graph holding AoS, SoA and many-batch launches (back to back, PDL edges
+    included) must give the eager results on every one of many replays, also when the
+    replays alternate between two streams."""
+    p = fn.preset("double")
+    n = (1 << 23) + 12345  # well past S tiles per CTA: the dynamic part does most tiles
+    x = _rows(n, 5)
+    x2 = _rows(n, 2, dim=2)
+    comps = [x[:, c].contiguous() for c in range(3)]
+    many = [_rows(m, 1) for m in (1_000_000, 700_001, 1_300_000, 999_999, 1_000_000, 1_200_000, 2_000_003, 1_500_000)]
+    w_aos, w_norm, w_2 = fn.normalize3(p, x), fn.norm3(p, x), fn.normalize2(p, x2)
+    w_soa = fn.normalize3(p, *comps)
+    w_many = fn.normalize_many(p, many)
+    w_q = fn.quotient3_robust(x)
+    torch.cuda.synchronize()
+    o_aos = (torch.empty_like(w_aos.length), torch.empty_like(w_aos.unit))
+    o_norm = torch.empty_like(w_norm)
+    o_2 = (torch.empty_like(w_2.length), torch.empty_like(w_2.unit))
+    o_q = (torch.empty_like(w_q.length), torch.empty_like(w_q.unit))
+    o_many = [(torch.empty_like(w.length), torch.empty_like(w.unit)) for w in w_many]
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    soa_out = {}
+    with torch.cuda.stream(s):
+        fn.normalize3(p, x, out=o_aos)  # eager warm-up on the capture stream (allocates the counter pool)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            fn.normalize3(p, x, out=o_aos)
+            fn.norm3(p, x, out=o_norm)
+            fn.normalize2(p, x2, out=o_2)
+            soa_out["res"] = fn.normalize3(p, *comps)
+            fn.normalize_many(p, many, out=o_many)
+            fn.quotient3_robust(x, out=o_q)
+            fn.normalize3(p, x, out=o_aos)  # the same node kind twice in one graph
+    s2 = torch.cuda.Stream()
+    for it in range(12):
+        for t in (o_aos[0], o_aos[1], o_norm, o_2[0], o_2[1], o_q[0], o_q[1]):
+            t.zero_()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(s if it % 2 == 0 else s2):
+            g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(_i64(o_aos[0]), _i64(w_aos.length)) and torch.equal(_i64(o_aos[1]), _i64(w_aos.unit)), it
+        assert torch.equal(_i64(o_norm), _i64(w_norm)), it
+        assert torch.equal(_i64(o_2[0]), _i64(w_2.length)) and torch.equal(_i64(o_2[1]), _i64(w_2.unit)), it
+        assert torch.equal(_i64(o_q[0]), _i64(w_q.length)) and torch.equal(_i64(o_q[1]), _i64(w_q.unit)), it
+        sr = soa_out["res"]
+        assert torch.equal(_i64(sr.length), _i64(w_soa.length)), it
+        for a, b in zip(sr.unit, w_soa.unit):
+            assert torch.equal(_i64(a), _i64(b)), it
+        for o, w in zip(o_many, w_many):
+            assert torch.equal(_i64(o[0]), _i64(w.length)) and torch.equal(_i64(o[1]), _i64(w.unit)), it
+    # eager launches still work after (and between) replays: the stream pair is untouched
+    again = fn.normalize3(p, x)
+    torch.cuda.synchronize()
+    assert torch.equal(_i64(again.unit), _i64(w_aos.unit))
+
+
 def test_static_and_dynamic_schedules_agree(cuda_dev, tmp_path):
     """The same batches under FASTNORM_B200_DYN=0 (static) and =1 (dynamic wherever a
     batch has more than S tiles per CTA, large ones included), in fresh processes."""
@@ -116,6 +180,10 @@ def test_static_and_dynamic_schedules_agree(cuda_dev, tmp_path):
             "for n in (1_000_000, 3_000_017, 1 << 25):\n"
             "    x = torch.empty((n, 3), dtype=torch.float64, device='cuda'); workloads.generate_device(5, x)\n"
             "    o = fn.normalize3(p, x); outs += [o.length.cpu().numpy(), o.unit.cpu().numpy().ravel()]\n"
+            "    o = fn.normalize3(p, *[x[:, c].contiguous() for c in range(3)])\n"
+            "    outs += [o.length.cpu().numpy()] + [c.cpu().numpy() for c in o.unit]\n"
+            "    for o in fn.normalize_many(p, [x[: n // 3], x[n // 3:]]):\n"
+            "        outs += [o.length.cpu().numpy(), o.unit.cpu().numpy().ravel()]\n"
             "np.save(sys.argv[1], np.concatenate(outs))\n")
     res = {}
     for mode in ("0", "1"):
