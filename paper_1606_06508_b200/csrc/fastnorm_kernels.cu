@@ -218,12 +218,15 @@ static bool dyn_enabled() {
     return v;
 }
 
-// Kernels that keep the static schedule.  Dynamic vs static, back-to-back launches, three
-// boxes (profiles/r02h_ab_dyn.txt, r02j_ab_dyn.txt, r02k_steady.jsonl): +5 to +23 % on the
-// quotient, norm, normalize2 and normalize4_sq kernels, +0.3 to +2 % on normalize3 f64 at
-// 2^30 rows, but -1.7 % on normalize3 f32 (config 4) on two boxes.
+// Kernels that keep the static schedule: none by default.  Dynamic vs static, back-to-back
+// launches, three boxes (profiles/r02h_ab_dyn.txt, r02j_ab_dyn.txt, r02k_steady.jsonl):
+// +5 to +23 % on the quotient, norm, normalize2 and normalize4_sq kernels, +0.3 to +2 % on
+// normalize3 f64 at 2^30 rows.  normalize3 f32 (config 4) lost 1.7 % at 2 CTAs per SM and
+// kept the static schedule until it was measured at 3 CTAs per SM, where the dynamic
+// schedule wins (6912 vs 6591 GB/s, profiles/r02ap_tables.txt); FNB_DYN_F32_NORMALIZE3=0
+// builds the old choice.
 #ifndef FNB_DYN_F32_NORMALIZE3
-#define FNB_DYN_F32_NORMALIZE3 0
+#define FNB_DYN_F32_NORMALIZE3 1
 #endif
 template <typename T, int N, int OP> struct DynamicSchedule {
     static constexpr bool value =

@@ -469,8 +469,11 @@ template <typename T, int N> struct Tile {
 //   with the dynamic schedule 3 CTAs measure better (profiles/r02w_ab_ctas_table.txt,
 //   2 -> 3: normalize2 f64 +8.8 %, normalize4_sq +4.1 %, normalize4 +2.4 %, scale3
 //   +2.6 %, normalize4_rotation +1.3 %, normalize3 f64 at 2^30 rows -0.7 to +2.8 %
-//   over three rounds, normalize2 f32 +7.9 %, normalize4 f32 +2.3 %), except 3-D
-//   binary32 rows (-8 % for normalize3 f32, which keeps the static schedule).
+//   over three rounds, normalize2 f32 +7.9 %, normalize4 f32 +2.3 %).  3-D binary32
+//   rows lose 8 % at 3 CTAs under the STATIC schedule, which normalize3 f32 kept until
+//   the two were measured together: dynamic at 3 CTAs gives normalize3 f32 6912 against
+//   6591 GB/s on config 4, scale3 f32 6889 against 5460, normalize3_sq f32 6889 against
+//   5919 (profiles/r02ao_sweep_table.txt, r02ap_tables.txt).
 // * The division-bound comparison kernels want full occupancy (FNB_DIV_CTAS).
 #ifndef FNB_DIV_CTAS
 #define FNB_DIV_CTAS 8
@@ -482,7 +485,6 @@ template <typename T, int N, int OP> struct CtasPerSm {
     static constexpr int value =
         (OP == FN_OP_NAIVE || OP == FN_OP_QUOTIENT || OP == FN_OP_QUOTIENT3_FAST) ? FNB_DIV_CTAS
         : OP == FN_OP_NORM                            ? 4
-        : (std::is_same<T, float>::value && N == 3)   ? 2
                                                       : FNB_STREAM_CTAS;
 };
 
@@ -584,10 +586,18 @@ template <typename T> struct Tile<T, 9> {
 // 112 B of it written) is tunable through FNB_NROT_ROWS / FNB_NROT_STAGES.  Through the
 // library (profiles/r01ca_nrot.txt): 128 x 3 (default) 6267 GB/s, 256 x 2 6308,
 // 128 x 4 5994, 256 x 3 5880 -- the tuner's ranking (r01bz_rot.csv) does not carry over.
+// normalize2_sq stages 16 B (f32) / 32 B (f64) of results per row, the most per input byte:
+// with the default 4-deep ring a CTA takes 80 KiB and only two fit per SM.  A 3-deep ring
+// (72 KiB, three CTAs): f32 5877 -> 6792 GB/s on in-band rows and 4859 -> 6594 on
+// full-range rows, f64 6871 -> 6825 and 6684 -> 6824 (profiles/r02ap_tables.txt).
+#ifndef FNB_SQ2_STAGES
+#define FNB_SQ2_STAGES 3
+#endif
 template <typename T, int N, int OP, bool BIG = true> struct OpStages {
     static constexpr int value = (DivBound<T, OP>::value && FNB_DIV_STAGES > 0) ? FNB_DIV_STAGES
                                  : Rows3<T, N, OP, BIG>::f64                   ? 3
                                  : Rows3<T, N, OP, BIG>::f32                   ? 5
+                                 : (N == 2 && OP == FN_OP_NORMALIZE_SQ)         ? FNB_SQ2_STAGES
                                                                                : Tile<T, N>::kStages;
 };
 // quotient2 f64 with two 512-row stages (4 CTAs per SM instead of 3) gained 9 % on

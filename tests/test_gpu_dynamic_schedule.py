@@ -42,9 +42,8 @@ def test_dynamic_schedule_matches_oracle(cuda_dev, n):
     assert bad == 0, first
 
 
-# normalize3 f32 keeps the static schedule (DynamicSchedule in fastnorm_kernels.cu), so the
-# binary32 case runs the quotient kernel, which takes the dynamic one
-@pytest.mark.parametrize("dtype,cfg,family", [(torch.float32, 4, "quotient3"), (torch.float64, 1, "normalize3")])
+@pytest.mark.parametrize("dtype,cfg,family", [(torch.float32, 4, "quotient3"), (torch.float32, 4, "normalize3"),
+                                              (torch.float64, 1, "normalize3")])
 def test_back_to_back_launches_reuse_the_counter(cuda_dev, dtype, cfg, family):
     p = fn.preset("single" if dtype == torch.float32 else "double")
     call = (lambda x, out=None: fn.quotient3_robust(x, out=out)) if family == "quotient3" else \
