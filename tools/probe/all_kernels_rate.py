@@ -26,17 +26,24 @@ def main():
     ap.add_argument("--log2-rows", type=int, default=26)
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--regimes", default="normal,mixed")
+    ap.add_argument("--precs", default="double,single")
+    ap.add_argument("--dims", default="2,3,4")
+    ap.add_argument("--kernels", default="")
     a = ap.parse_args()
     n = 1 << a.log2_rows
     peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6458.0
     for regime in a.regimes.split(","):
         for dt, prec in ((torch.float64, "double"), (torch.float32, "single")):
+            if prec not in a.precs.split(","):
+                continue
             ka = kernel_args_array(fn.preset(prec))
-            for dim in (2, 3, 4):
+            for dim in (int(d) for d in a.dims.split(",")):
                 x = torch.empty((n, dim), dtype=dt, device="cuda")
                 workloads.generate_regime_device(regime, x)
                 for name, op, needs_ka in OPS:
                     if op == _lib.OP_QUOTIENT3_FAST and dim != 3:
+                        continue
+                    if a.kernels and name not in a.kernels.split(","):
                         continue
                     k = ka if needs_ka else None
                     first = batch.run(op, dim, x, k)
