@@ -473,7 +473,10 @@ template <typename T, int N> struct Tile {
 //   rows lose 8 % at 3 CTAs under the STATIC schedule, which normalize3 f32 kept until
 //   the two were measured together: dynamic at 3 CTAs gives normalize3 f32 6912 against
 //   6591 GB/s on config 4, scale3 f32 6889 against 5460, normalize3_sq f32 6889 against
-//   5919 (profiles/r02ao_sweep_table.txt, r02ap_tables.txt).
+//   5919 (profiles/r02ao_sweep_table.txt, r02ap_tables.txt).  scale3 f32 and normalize3_sq
+//   f32 take 4 (in one process over both regimes and two sizes: normalize3_sq 6152-6827 at
+//   3 -> 6768-6886 at 4, scale3 6102-6913 -> 6761-6881; normalize3 f32 unchanged within
+//   0.3 %, so it stays at 3; profiles/r02as_f32_dim3.txt).
 // * The division-bound comparison kernels want full occupancy (FNB_DIV_CTAS).
 #ifndef FNB_DIV_CTAS
 #define FNB_DIV_CTAS 8
@@ -485,6 +488,7 @@ template <typename T, int N, int OP> struct CtasPerSm {
     static constexpr int value =
         (OP == FN_OP_NAIVE || OP == FN_OP_QUOTIENT || OP == FN_OP_QUOTIENT3_FAST) ? FNB_DIV_CTAS
         : OP == FN_OP_NORM                            ? 4
+        : (std::is_same<T, float>::value && N == 3 && (OP == FN_OP_SCALE || OP == FN_OP_NORMALIZE_SQ)) ? 4
                                                       : FNB_STREAM_CTAS;
 };
 

@@ -4,7 +4,7 @@ Per kernel: warp instructions, issue-active cycles and FP64-pipe instructions pe
 the SM clock ncu saw, and DRAM bytes per row.  bench.py reads the per-row instruction
 counts to put an instruction-issue roofline beside the HBM one for the division-bound
 comparison kernels.
-python tools/issue_json.py TAG ROWS_BY_NAME_JSON"""
+python tools/issue_json.py TAG [--merge]"""
 import csv
 import glob
 import json
@@ -13,7 +13,8 @@ import sys
 
 ROWS = {"quotient2_f64_cfg2": 1 << 26, "normalize2_f64_cfg2": 1 << 26, "quotient3_f64_cfg5": 1 << 28,
         "quotient3_fast_f64_cfg5": 1 << 28, "quotient3_f32_cfg4": 1 << 28, "quotient3_f64_cfg1": 1 << 20,
-        "normalize3_f64_cfg5": 1 << 30}
+        "normalize3_f64_cfg5": 1 << 30, "norm3_f32_cfg4": 1 << 28, "norm3_f64_cfg5": 1 << 28,
+        "normalize3_f32_cfg4": 1 << 28, "scale3_f32_cfg4": 1 << 28, "normalize3_sq_f32_cfg4": 1 << 28}
 
 
 _SCALE = {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9, "tbyte": 1e12, "inst": 1, "cycle": 1,
@@ -65,6 +66,9 @@ def main():
             "issue_frac_under_ncu": inst / (148 * 4 * clk) / t,
         }
     dst = os.path.join("profiles", "ncu_issue.json")
+    if "--merge" in sys.argv and os.path.exists(dst):  # keep the kernels of earlier passes
+        with open(dst) as f:
+            out = {**json.load(f), **out}
     with open(dst, "w") as f:
         json.dump(out, f, indent=1, sort_keys=True)
     print(json.dumps(out, indent=1))
