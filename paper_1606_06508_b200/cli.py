@@ -159,6 +159,8 @@ def cmd_bench(a) -> int:
     n = a.rows or c.rows
     dt = torch.float64 if c.dtype == "float64" else torch.float32
     prec = "double" if dt == torch.float64 else "single"
+    if a.devices:
+        return _bench_sharded(a, c, n, prec)
     x = torch.empty((n, c.dim), dtype=dt, device="cuda")
     workloads.generate_device(a.config, x)
     w = x.element_size()
@@ -178,6 +180,35 @@ def cmd_bench(a) -> int:
     print(json.dumps({"config": a.config, "algo": a.algo, "rows": n, "dim": c.dim, "dtype": c.dtype,
                       "ms_per_pass": t * 1e3, "vectors_per_s": n / t,
                       "GB_per_s": n * bytes_row / t / 1e9}))
+    return 0
+
+
+def _bench_sharded(a, c, n: int, prec: str) -> int:
+    """`bench --devices 0,1,...`: the config's rows as device-resident shards on several GPUs
+    of this one process (multigpu.DeviceShards, fn_run_sharded: one stream per shard, no
+    collective).  A pass takes as long as its slowest shard (CUDA events per shard)."""
+    import statistics
+
+    import paper_1606_06508_b200 as fn
+    from paper_1606_06508_b200 import multigpu
+
+    if a.algo != "scaling":
+        print("error: --devices runs the scaling algorithm", file=sys.stderr)
+        return 2
+    devs = [int(d) for d in a.devices.split(",")]
+    p = fn.preset(prec)
+    x = multigpu.DeviceShards.generate(a.config, n, devs)
+    out = None
+    for _ in range(max(a.warmup, 1)):
+        res = multigpu.normalize_sharded(p, x, out=out)
+        out = (res.head, res.body)
+    ms = [max(multigpu.normalize_sharded(p, x, out=out).elapsed_ms) for _ in range(a.steps)]
+    t = statistics.median(ms) / 1e3
+    w = x[0].element_size()
+    print(json.dumps({"config": a.config, "algo": a.algo, "rows": n, "dim": c.dim, "dtype": c.dtype,
+                      "devices": devs, "rows_per_shard": [int(s.shape[0]) for s in x.tensors],
+                      "ms_per_pass": t * 1e3, "vectors_per_s": n / t,
+                      "GB_per_s": n * (2 * c.dim + 1) * w / t / 1e9}))
     return 0
 
 
@@ -326,6 +357,8 @@ def build_parser() -> argparse.ArgumentParser:
     s.add_argument("--rows", type=int, default=0, help="override the config's row count")
     s.add_argument("--steps", type=int, default=20)
     s.add_argument("--warmup", type=int, default=3)
+    s.add_argument("--devices", default="", help="comma-separated GPU ordinals: shard the rows over these "
+                                                 "devices from this one process (a device may repeat)")
     s.set_defaults(fn=cmd_bench)
 
     s = sub.add_parser("ratios", help="per-vector times and the T3/T4 ratio tables on the GPU "

@@ -82,4 +82,8 @@ def test_gpu_subcommands(capsys, tmp_path, cuda_dev):
     assert o["unit"].shape == (1000, 3) and np.allclose(np.linalg.norm(o["unit"], axis=1), 1.0)
     assert cli.main(["bench", "--config", "1", "--steps", "3"]) == 0
     assert json.loads(capsys.readouterr().out)["vectors_per_s"] > 1e9
+    assert cli.main(["bench", "--config", "4", "--rows", "3000001", "--steps", "3", "--devices", "0,0,0"]) == 0
+    sharded = json.loads(capsys.readouterr().out)
+    assert sharded["devices"] == [0, 0, 0] and sum(sharded["rows_per_shard"]) == 3000001
+    assert sharded["vectors_per_s"] > 1e9
     assert cli.main(["selftest", "--pairs", "1000000"]) == 0
