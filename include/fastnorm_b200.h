@@ -118,7 +118,8 @@ int fn_run_many(int op, int dim, int dtype, int nseg, const void* const* xs, con
  * complete.  after[k] (after may be NULL, and so may any entry) is a stream of device
  * devices[k] whose already-enqueued work (the producer of xs[k]) the shard waits for.
  * elapsed_ms[k] (may be NULL) receives shard k's device time by CUDA events on its stream.
- * A device may be named more than once (one stream per shard).  Ops SCALE..NORMALIZE_SQ.
+ * A device may be named more than once (one stream per shard).  Calls from several host
+ * threads are serialised.  Ops SCALE..NORMALIZE_SQ.
  * No reference interface: the reference is CPU only and takes one row per call. */
 int fn_run_sharded(int op, int dim, int dtype, int nshard, const int* devices, const void* const* xs,
                    const int64_t* ns, void* const* heads, void* const* bodies, void* const* extras,

@@ -1862,6 +1862,10 @@ int run_sharded(int op, int dim, int dtype, int nshard, const int* devices, cons
                                   w.w2 ? extras[k] : nullptr);
         if (rc != FN_OK) return fail(rc, "shard " + std::to_string(k) + ": " + g_last_error);
     }
+    // One sharded call at a time: the shard streams and their events are shared by every
+    // caller (the call is synchronous, so concurrent callers would only interleave).
+    static std::mutex call_mu;
+    std::lock_guard<std::mutex> call_lock(call_mu);
     int home = 0;
     e = cudaGetDevice(&home);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
