@@ -559,11 +559,26 @@ template <typename T, int N, int OP, bool BIG = true> struct Rows3 {
 };
 constexpr int64_t kBigTileRows = int64_t(1) << 24;
 
+// The binary32 division-bound kernels ask for 8 CTAs per SM like the binary64 ones, but their
+// default tiles (512-1024 rows, 48-68 KiB per CTA) let only 3-4 fit.  Halving the tile
+// (FNB_DIV32_ROWS_SHIFT = 1) pays for 2-D rows only (1024 -> 512 rows: quotient2 f32
+// 4732 -> 5223 GB/s, naive2 f32 on full-range rows 3294 -> 4134; 3-D and 4-D rows lose
+// 2-37 %, a quarter tile loses everywhere; profiles/r02ay_div32_table.txt), so it applies
+// to N = 2.
+#ifndef FNB_DIV32_ROWS_SHIFT
+#define FNB_DIV32_ROWS_SHIFT 1
+#endif
+template <typename T, int OP> struct DivBound32 {
+    static constexpr bool value = std::is_same<T, float>::value &&
+                                  (OP == FN_OP_QUOTIENT || OP == FN_OP_QUOTIENT3_FAST || OP == FN_OP_NAIVE);
+};
 template <typename T, int N, int OP, bool BIG = true> struct OpRows {
     static constexpr int kOutRow = (RowOp<T, N, OP>::W0 + RowOp<T, N, OP>::W1 + RowOp<T, N, OP>::W2) * (int)sizeof(T);
     static constexpr int kTile = Rows3<T, N, OP, BIG>::f64 ? 512 : Tile<T, N>::kRows;
     static constexpr int kBase = (3 * kOutRow * kTile > 65536) ? kTile / 2 : kTile;
-    static constexpr int value = DivBound<T, OP>::value ? kBase >> FNB_DIV_ROWS_SHIFT : kBase;
+    static constexpr int value = DivBound<T, OP>::value     ? kBase >> FNB_DIV_ROWS_SHIFT
+                                 : (DivBound32<T, OP>::value && N == 2) ? kBase >> FNB_DIV32_ROWS_SHIFT
+                                                            : kBase;
 };
 
 // Per-row matrices are 72 B records: the default 8 KiB stage would hold only 64 of them
